@@ -1,0 +1,117 @@
+/*
+ * hdll_b200.h -- C ABI of the B200-native hdll encoder hot path.
+ *
+ * Drop-in boundary for the reference package `hdll` (/root/reference/pkg).
+ * The reference is pure Python, so "its FFI" for this path is a ctypes
+ * binding; each entry point below replaces one reference interface:
+ *
+ *   hdll_b200_encode_batch_device / hdll_b200_encode_host
+ *       replace hdll.container.encode (container.py:131-230) followed by
+ *       serialize (container.py:332-340): RGBE quads in, the serialized HDLL v1
+ *       stream out (byte-identical to the reference's).
+ *   hdll_b200_lossless_encode_plane
+ *       replaces the lossless coder plugin id 1 `_MedRicePlaneCoder.encode`
+ *       (codec_core.py:260-265) plus the CRC of lossless_encode (:306-313).
+ *   hdll_b200_lossy_encode
+ *       replaces the lossy coder plugin id 1 `_BlockDctCoder.encode`
+ *       (codec_core.py:430-453) plus the CRC of lossy_encode (:520-533).
+ *
+ * Plain pointers and sizes only.  Device pointers are CUDA global memory;
+ * `stream` is a cudaStream_t (NULL = legacy default stream).  Status codes are
+ * mapped to the reference's Python exceptions by paper_2309_11072_b200/_native.py.
+ */
+#ifndef HDLL_B200_H
+#define HDLL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hdll_b200_ctx hdll_b200_ctx;
+
+enum {
+  HDLL_B200_OK = 0,
+  HDLL_B200_E_ARG = 1,          /* bad argument (ValueError in the reference) */
+  HDLL_B200_E_EMPTY = 2,        /* empty image (StreamError, container.py:154-155) */
+  HDLL_B200_E_NONFINITE = 3,    /* float32 a/b overflow (ValueError, estimator.py:66-67) */
+  HDLL_B200_E_CUDA = 4,         /* CUDA runtime error */
+  HDLL_B200_E_INTERNAL = 5,     /* device-side consistency failure */
+  HDLL_B200_E_CAPACITY = 6      /* output buffer too small */
+};
+
+/* Encode parameters (container.py:131-142, TmoParams tonemap.py:22-37). */
+typedef struct hdll_b200_params {
+  int32_t quality;           /* 1..100 */
+  int32_t sigma_milli;       /* round(sigma * 1000), 0 = no prefilter */
+  int32_t slrme;             /* 0/1 */
+  int32_t global_regression; /* 0/1 */
+  int32_t blas_kernel;       /* sum-order model of np.dot: 0 OpenBLAS SKYLAKEX, 1 HASWELL */
+  int32_t blas_threads;      /* OpenBLAS thread count of the modelled reference run (>= 1) */
+  int32_t radius;            /* Gaussian radius ceil(3 sigma) */
+  int32_t want_trace;        /* keep sdr / s / m_star / residual planes for hdll_b200_trace */
+  double tmo_key;
+  double tmo_white_point;    /* <= 0: automatic (max of the scaled luminance) */
+  double tmo_inv_gamma;      /* 1.0 / gamma as the host computes it */
+  double tmo_epsilon;
+  const double *taps;        /* host pointer, 2*radius+1 Gaussian taps (numpy gaussian_kernel) */
+} hdll_b200_params;
+
+typedef struct hdll_b200_image {
+  const uint8_t *rgbe;       /* (height, width, 4) RGBE quads; device or host pointer per call */
+  uint32_t width, height;
+  const uint8_t *hdr_pre;    /* host bytes: magic .. sigma_milli + u16 len + TMO record */
+  uint32_t hdr_pre_len;
+  const uint8_t *hdr_post;   /* host bytes: u32 len + header text block */
+  uint32_t hdr_post_len;
+  hdll_b200_params params;
+} hdll_b200_image;
+
+int hdll_b200_ctx_create(hdll_b200_ctx **out, int device);
+void hdll_b200_ctx_destroy(hdll_b200_ctx *ctx);
+
+/* Upper bound of the serialized stream length for one image. */
+uint64_t hdll_b200_stream_capacity(uint32_t width, uint32_t height, uint32_t hdr_pre_len, uint32_t hdr_post_len);
+
+/* Batched encode, everything resident on the device.  d_out[i] receives image
+ * i's stream (capacity out_cap[i] bytes), d_out_len[i] (device) its length.
+ * Asynchronous on `stream`; hdll_b200_sync() reports device-side errors. */
+int hdll_b200_encode_batch_device(hdll_b200_ctx *ctx, const hdll_b200_image *imgs, int n, uint8_t *const *d_out,
+                                  const uint64_t *out_cap, uint64_t *d_out_len, void *stream);
+
+/* Wait for the last batch of this context and return its status. */
+int hdll_b200_sync(hdll_b200_ctx *ctx);
+
+/* Host -> host convenience: H2D of the RGBE quads, encode, D2H of the stream. */
+int hdll_b200_encode_host(hdll_b200_ctx *ctx, const hdll_b200_image *img, uint8_t *h_out, uint64_t cap,
+                          uint64_t *out_len);
+
+/* Per-stage trace of image `index` of the last batch (want_trace set):
+ * which = 0 sdr (h,w,3), 1 decoded S (h,w,3 interleaved), 2 m_star (3 planes),
+ * 3 residuals (3 planes).  nbytes must equal the array size. */
+int hdll_b200_trace(hdll_b200_ctx *ctx, int index, int which, uint8_t *h_dst, uint64_t nbytes);
+
+/* Lossless coder id 1 body (<II w,h> + bits) and the raw-plane CRC-32. */
+int hdll_b200_lossless_encode_plane(hdll_b200_ctx *ctx, const uint8_t *h_plane, uint32_t width, uint32_t height,
+                                    uint8_t *h_body, uint64_t cap, uint64_t *body_len, uint32_t *crc);
+
+/* Lossy coder id 1 body, the decoded image (h,w,3) and the CRC of its bytes. */
+int hdll_b200_lossy_encode(hdll_b200_ctx *ctx, const uint8_t *h_rgb, uint32_t width, uint32_t height,
+                           int32_t quality, uint8_t *h_body, uint64_t cap, uint64_t *body_len, uint8_t *h_decoded,
+                           uint32_t *crc);
+
+/* Number of kernel launches issued by the last encode call. */
+int hdll_b200_last_launch_count(hdll_b200_ctx *ctx);
+
+/* Device time (ms) of the 8 stages of the last batch, in order: tonemap stats,
+ * base layer, prefilter, fit, estimate, crc, entropy coders, assemble. */
+int hdll_b200_stage_times(hdll_b200_ctx *ctx, float *ms, int n);
+
+const char *hdll_b200_status_string(int status);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HDLL_B200_H */

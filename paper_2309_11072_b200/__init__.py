@@ -1,0 +1,33 @@
+"""B200-native (sm_100a) encoder for the dual-layer lossless Radiance HDR codec
+of arXiv 2309.11072 -- a drop-in for the reference package `hdll`'s encode path.
+
+`encode()` mirrors hdll.container.encode (reference container.py:131-230); all
+compute runs in the CUDA kernels of libhdll_b200.so (csrc/), reached through the
+C ABI in include/hdll_b200.h.  There is no CPU fallback.
+"""
+
+from .container import (
+    MAGIC,
+    VERSION,
+    ChecksumError,
+    CodecError,
+    CorruptPayloadError,
+    DualLayerStream,
+    LosslessCoderSpec,
+    LossyCoderSpec,
+    RadianceImage,
+    RegressionEntry,
+    RegressionTable,
+    SdrImage,
+    StreamError,
+    TmoParams,
+    UnknownCoderError,
+    bitrate_bpp,
+    deserialize,
+    encode,
+    encode_batch,
+    section_sizes,
+    serialize,
+)
+
+__version__ = "0.1.0"

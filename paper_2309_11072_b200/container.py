@@ -1,0 +1,543 @@
+"""Host side of the B200 encoder: the reference's `encode()` interface and the
+HDLL v1 data model, re-stated so this package runs without the reference.
+
+Drop-in for /root/reference/pkg/src/hdll/container.py:
+  * `encode(image, quality, sigma, slrme, global_regression, lossy_coder,
+    lossless_coder, tmo, timings, trace)` -- same signature, arguments and
+    errors as container.py:131-157, returning a `DualLayerStream` whose fields
+    and `serialize()` bytes equal the reference's (container.py:68-111,306-340);
+  * `encode_batch(images, ...)` -- many images in one batched device pass
+    (BASELINE configs 1 and 4); `encode_device(...)` -- inputs and outputs
+    resident in HBM (the bench's `value` path).
+Everything between the RGBE quads and the serialized stream runs in the CUDA
+kernels of libhdll_b200.so; the host builds only the fixed header, the TMO JSON
+record and the header text block, exactly as container.py:306-329 writes them.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import json
+import math
+import os
+import struct
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+
+__all__ = [
+    "MAGIC", "VERSION", "StreamError", "CodecError", "UnknownCoderError", "ChecksumError",
+    "CorruptPayloadError", "LossyCoderSpec", "LosslessCoderSpec", "TmoParams", "SdrImage",
+    "RadianceImage", "RegressionEntry", "RegressionTable", "DualLayerStream", "encode",
+    "encode_batch", "serialize", "deserialize", "section_sizes", "bitrate_bpp", "gaussian_kernel",
+]
+
+MAGIC = b"HDLL"
+VERSION = 1
+_ENTRY_FMT = "<BBffI"
+_ENTRY_SIZE = struct.calcsize(_ENTRY_FMT)  # 14 bytes (container.py:60-61)
+STAGES = ("tonemap", "base", "prefilter", "fit", "estimate", "crc", "entropy", "assemble")
+
+
+# --------------------------------------------------------------------------
+# errors (codec_core.py:55-68, container.py:64-65)
+# --------------------------------------------------------------------------
+class StreamError(ValueError):
+    """Malformed or inconsistent container stream."""
+
+
+class CodecError(ValueError):
+    """Base class for coder failures."""
+
+
+class UnknownCoderError(CodecError):
+    """Payload or spec names a coder id that is not registered."""
+
+
+class ChecksumError(CodecError):
+    """Decoded data does not match the transmitted CRC-32."""
+
+
+class CorruptPayloadError(CodecError):
+    """Payload structure cannot be decoded."""
+
+
+# --------------------------------------------------------------------------
+# data model
+# --------------------------------------------------------------------------
+@dataclass(frozen=True)
+class LossyCoderSpec:
+    coder_id: int = 1
+    quality: int = 85
+
+    def __post_init__(self):
+        if not 1 <= self.quality <= 100:
+            raise ValueError(f"quality must be in [1, 100], got {self.quality}")
+
+
+@dataclass(frozen=True)
+class LosslessCoderSpec:
+    coder_id: int = 1
+
+
+@dataclass(frozen=True)
+class TmoParams:
+    """tonemap.py:22-37: key, white point (None = auto), gamma, epsilon."""
+
+    key: float = 0.18
+    white_point: float | None = None
+    gamma: float = 2.2
+    epsilon: float = 1e-6
+
+    def __post_init__(self):
+        if not (self.key > 0 and self.gamma > 0 and self.epsilon > 0):
+            raise ValueError("key, gamma and epsilon must be strictly positive")
+        if self.epsilon > 1e-3:
+            raise ValueError("epsilon must be <= 1e-3")
+        if self.white_point is not None and not self.white_point > 0:
+            raise ValueError("white_point must be strictly positive or None")
+
+
+@dataclass(eq=False)
+class SdrImage:
+    width: int
+    height: int
+    r: np.ndarray
+    g: np.ndarray
+    b: np.ndarray
+
+    def __eq__(self, other) -> bool:
+        if not hasattr(other, "as_array"):
+            return NotImplemented
+        return (self.width == other.width and self.height == other.height
+                and np.array_equal(self.as_array(), other.as_array()))
+
+    def as_array(self) -> np.ndarray:
+        return np.stack((self.r, self.g, self.b), axis=-1)
+
+    @classmethod
+    def from_array(cls, arr: np.ndarray) -> "SdrImage":
+        arr = np.ascontiguousarray(arr, dtype=np.uint8)
+        h, w = arr.shape[:2]
+        return cls(w, h, arr[..., 0].copy(), arr[..., 1].copy(), arr[..., 2].copy())
+
+
+@dataclass(eq=False)
+class RadianceImage:
+    """radiance_io.py:53-86: (height, width, 4) uint8 RGBE quads + header."""
+
+    width: int
+    height: int
+    pixels: np.ndarray
+    header_vars: list = field(default_factory=list)
+    resolution_orientation: str = "-Y +X"
+
+    def __eq__(self, other) -> bool:
+        if not hasattr(other, "pixels"):
+            return NotImplemented
+        return (self.width == other.width and self.height == other.height
+                and self.resolution_orientation == other.resolution_orientation
+                and list(map(tuple, self.header_vars)) == list(map(tuple, other.header_vars))
+                and np.array_equal(self.pixels, other.pixels))
+
+
+@dataclass(frozen=True)
+class RegressionEntry:
+    channel: int
+    exponent: int
+    a: float
+    b: float
+    count: int
+
+
+@dataclass(eq=True)
+class RegressionTable:
+    """estimator.py:50-92: entries sorted by (channel, exponent), validated."""
+
+    entries: list = field(default_factory=list)
+
+    def __post_init__(self):
+        self.entries = sorted(self.entries, key=lambda e: (e.channel, e.exponent))
+        seen = set()
+        for e in self.entries:
+            if not 0 <= e.channel <= 2:
+                raise ValueError(f"bad channel {e.channel}")
+            if not 0 <= e.exponent <= 255:
+                raise ValueError(f"bad exponent {e.exponent}")
+            if e.count < 1:
+                raise ValueError("entry count must be >= 1")
+            if not (math.isfinite(e.a) and math.isfinite(e.b)):
+                raise ValueError("regression parameters must be finite")
+            key = (e.channel, e.exponent)
+            if key in seen:
+                raise ValueError(f"duplicate entry for channel {e.channel} exponent {e.exponent}")
+            seen.add(key)
+
+    def __len__(self) -> int:
+        return len(self.entries)
+
+
+@dataclass(eq=False)
+class DualLayerStream:
+    """container.py:68-111."""
+
+    width: int
+    height: int
+    slrme: bool
+    lossy_spec: LossyCoderSpec
+    lossless_spec: LosslessCoderSpec
+    sigma_milli: int
+    tmo_record: bytes
+    regression_table: RegressionTable
+    header_vars: list
+    resolution_orientation: str
+    base_payload: bytes
+    e_payload: bytes | None = None
+    residual_payloads: tuple | None = None
+
+    def __post_init__(self):
+        if self.slrme != bool(len(self.regression_table)):
+            raise StreamError("SLRME flag must match a nonempty regression table")
+        if (self.e_payload is None) != (self.residual_payloads is None):
+            raise StreamError("enhancement sections must be present or absent together")
+
+    def __eq__(self, other) -> bool:
+        if not hasattr(other, "base_payload"):
+            return NotImplemented
+        ent = lambda t: [(e.channel, e.exponent, e.a, e.b, e.count) for e in t.entries]  # noqa: E731
+        return (self.width == other.width and self.height == other.height
+                and self.slrme == other.slrme
+                and (self.lossy_spec.coder_id, self.lossy_spec.quality)
+                == (other.lossy_spec.coder_id, other.lossy_spec.quality)
+                and self.lossless_spec.coder_id == other.lossless_spec.coder_id
+                and self.sigma_milli == other.sigma_milli and self.tmo_record == other.tmo_record
+                and ent(self.regression_table) == ent(other.regression_table)
+                and list(map(tuple, self.header_vars)) == list(map(tuple, other.header_vars))
+                and self.resolution_orientation == other.resolution_orientation
+                and self.base_payload == other.base_payload and self.e_payload == other.e_payload
+                and (None if self.residual_payloads is None else tuple(self.residual_payloads))
+                == (None if other.residual_payloads is None else tuple(other.residual_payloads)))
+
+    @property
+    def sdr_only(self) -> bool:
+        return self.e_payload is None
+
+
+# --------------------------------------------------------------------------
+# serialization (container.py:287-426)
+# --------------------------------------------------------------------------
+def _header_block(header_vars, orientation: str) -> bytes:
+    lines = [v if k == "" else f"{k}={v}" for k, v in header_vars]
+    lines.append(orientation)
+    return "\n".join(lines).encode("latin-1")
+
+
+def _decode_header_block(block: bytes):
+    lines = block.decode("latin-1").split("\n")
+    header_vars = []
+    for line in lines[:-1]:
+        if "=" in line and not line.startswith("#"):
+            key, value = line.split("=", 1)
+            header_vars.append((key, value))
+        else:
+            header_vars.append(("", line))
+    return header_vars, lines[-1]
+
+
+def _fixed_header(width, height, slrme, lossy_id, quality, lossless_id, sigma_milli, tmo_record) -> bytes:
+    return (MAGIC + struct.pack("<BIIBBBBH", VERSION, width, height, 1 if slrme else 0, lossy_id, quality,
+                                lossless_id, sigma_milli)
+            + struct.pack("<H", len(tmo_record)) + tmo_record)
+
+
+def _header_bytes(stream: DualLayerStream) -> bytes:
+    out = bytearray(_fixed_header(stream.width, stream.height, stream.slrme, stream.lossy_spec.coder_id,
+                                  stream.lossy_spec.quality, stream.lossless_spec.coder_id,
+                                  stream.sigma_milli, stream.tmo_record))
+    entries = stream.regression_table.entries
+    out += struct.pack("<H", len(entries))
+    for e in entries:
+        out += struct.pack(_ENTRY_FMT, e.channel, e.exponent, e.a, e.b, e.count)
+    blk = _header_block(stream.header_vars, stream.resolution_orientation)
+    out += struct.pack("<I", len(blk)) + blk
+    return bytes(out)
+
+
+def serialize(stream: DualLayerStream) -> bytes:
+    out = bytearray(_header_bytes(stream))
+    out += stream.base_payload
+    if not stream.sdr_only:
+        out += stream.e_payload
+        for p in stream.residual_payloads:
+            out += p
+    return bytes(out)
+
+
+def deserialize(data: bytes) -> DualLayerStream:
+    """Parse HDLL v1 bytes (container.py:369-426)."""
+    pos = 0
+
+    def take(n, what):
+        nonlocal pos
+        if pos + n > len(data):
+            raise StreamError(f"stream truncated inside {what}")
+        chunk = data[pos:pos + n]
+        pos += n
+        return chunk
+
+    if take(4, "magic") != MAGIC:
+        raise StreamError("bad magic; not an HDLL stream")
+    (version,) = struct.unpack("<B", take(1, "version"))
+    if version != VERSION:
+        raise StreamError(f"unsupported version {version}")
+    w, h, flags, lossy_id, quality, lossless_id, sigma_milli = struct.unpack("<IIBBBBH", take(14, "fixed header"))
+    (tl,) = struct.unpack("<H", take(2, "tmo record length"))
+    tmo_record = take(tl, "tmo record")
+    (ne,) = struct.unpack("<H", take(2, "regression table count"))
+    entries = []
+    for _ in range(ne):
+        ch, ex, a, b, cnt = struct.unpack(_ENTRY_FMT, take(_ENTRY_SIZE, "regression entry"))
+        entries.append(RegressionEntry(ch, ex, float(a), float(b), cnt))
+    (bl,) = struct.unpack("<I", take(4, "header block length"))
+    header_vars, orientation = _decode_header_block(take(bl, "header block"))
+
+    def payload(what):
+        (ln,) = struct.unpack("<I", take(4, f"{what} length"))
+        return struct.pack("<I", ln) + take(ln, what)
+
+    base = payload("base payload")
+    e_payload = residuals = None
+    if pos < len(data):
+        e_payload = payload("exponent payload")
+        residuals = tuple(payload(f"residual payload {n}") for n in "RGB")
+        if pos < len(data):
+            raise StreamError(f"{len(data) - pos} trailing bytes after the last section")
+    slrme = bool(flags & 1)
+    table = RegressionTable(entries)
+    if slrme != bool(len(table)):
+        raise StreamError("SLRME flag does not match the regression table")
+    return DualLayerStream(w, h, slrme, LossyCoderSpec(lossy_id, quality), LosslessCoderSpec(lossless_id),
+                           sigma_milli, tmo_record, table, header_vars, orientation, base, e_payload, residuals)
+
+
+def section_sizes(stream: DualLayerStream) -> dict:
+    sizes = {"header": len(_header_bytes(stream)), "base": len(stream.base_payload)}
+    if stream.sdr_only:
+        sizes.update(exponent=0, residual_r=0, residual_g=0, residual_b=0)
+    else:
+        sizes["exponent"] = len(stream.e_payload)
+        for name, p in zip("rgb", stream.residual_payloads):
+            sizes[f"residual_{name}"] = len(p)
+    return sizes
+
+
+def bitrate_bpp(stream: DualLayerStream) -> float:
+    if stream.width * stream.height == 0:
+        raise StreamError("bpp undefined for an empty image")
+    return len(serialize(stream)) * 8.0 / (stream.width * stream.height)
+
+
+# --------------------------------------------------------------------------
+# encode
+# --------------------------------------------------------------------------
+def gaussian_kernel(sigma: float) -> np.ndarray:
+    """estimator.py:120-127 (host numpy, exactly the reference's ufunc calls):
+    the taps are encode parameters passed to the prefilter kernel."""
+    if not sigma > 0:
+        raise ValueError("sigma must be strictly positive")
+    radius = math.ceil(3.0 * sigma)
+    xs = np.arange(-radius, radius + 1, dtype=np.float64)
+    w = np.exp(-0.5 * (xs / sigma) ** 2)
+    return w / w.sum()
+
+
+def _blas_defaults(blas_kernel, blas_threads):
+    """Sum-order model of the reference's np.dot.  Defaults:
+    OpenBLAS SKYLAKEX with 1 thread, overridable per call or by HDLL_BLAS_KERNEL
+    ("skylakex" | "haswell") / HDLL_BLAS_THREADS."""
+    if blas_kernel is None:
+        blas_kernel = os.environ.get("HDLL_BLAS_KERNEL", "skylakex")
+    if isinstance(blas_kernel, str):
+        blas_kernel = {"skylakex": 0, "haswell": 1, "zen": 1}[blas_kernel.lower()]
+    if blas_threads is None:
+        blas_threads = int(os.environ.get("HDLL_BLAS_THREADS", "1"))
+    return int(blas_kernel), max(1, int(blas_threads))
+
+
+@dataclass
+class _Prepared:
+    image: object
+    w: int
+    h: int
+    sigma_milli: int
+    quality: int
+    slrme: bool
+    tmo_record: bytes
+    pre: bytes
+    post: bytes
+    taps: np.ndarray | None
+    params: _native.Params
+    pixels: np.ndarray
+
+
+def _prepare(image, quality, sigma, slrme, global_regression, lossy_coder, lossless_coder, tmo,
+             blas_kernel, blas_threads, want_trace) -> _Prepared:
+    if image.width <= 0 or image.height <= 0:
+        raise StreamError("cannot encode an empty image")
+    if not 0.0 <= sigma <= 65.535:
+        raise ValueError("sigma must be in [0, 65.535]")
+    sigma_milli = int(round(sigma * 1000.0))
+    tmo = tmo or TmoParams()
+    LossyCoderSpec(coder_id=lossy_coder, quality=quality)  # validates quality
+    if lossy_coder != 1:
+        raise UnknownCoderError(f"lossy coder id {lossy_coder} is not available on the B200 path")
+    if lossless_coder != 1:
+        raise UnknownCoderError(f"lossless coder id {lossless_coder} is not available on the B200 path")
+    px = image.pixels
+    if px.dtype != np.uint8:
+        vals = np.asarray(px, dtype=np.int64)
+        if ((vals < 0) | (vals > 255)).any():
+            raise ValueError("RGBE components must be in [0, 255]")
+        px = vals.astype(np.uint8)
+    if px.shape != (image.height, image.width, 4):
+        raise ValueError(f"pixels must be (height, width, 4), got {px.shape}")
+    tmo_record = json.dumps({"key": tmo.key, "white_point": tmo.white_point, "gamma": tmo.gamma,
+                             "epsilon": tmo.epsilon}, sort_keys=True).encode("ascii")
+    pre = _fixed_header(image.width, image.height, slrme, 1, quality, 1, sigma_milli, tmo_record)
+    blk = _header_block(image.header_vars, image.resolution_orientation)
+    post = struct.pack("<I", len(blk)) + blk
+    kern, nthr = _blas_defaults(blas_kernel, blas_threads)
+    taps = None
+    radius = 0
+    if slrme and sigma_milli:
+        taps = np.ascontiguousarray(gaussian_kernel(sigma_milli / 1000.0))
+        radius = (taps.size - 1) // 2
+    p = _native.Params()
+    p.quality, p.sigma_milli, p.slrme = quality, sigma_milli, int(bool(slrme))
+    p.global_regression = int(bool(global_regression))
+    p.blas_kernel, p.blas_threads, p.radius = kern, nthr, radius
+    p.want_trace = int(bool(want_trace))
+    p.tmo_key = float(tmo.key)
+    p.tmo_white_point = float(tmo.white_point) if tmo.white_point is not None else -1.0
+    p.tmo_inv_gamma = 1.0 / tmo.gamma
+    p.tmo_epsilon = float(tmo.epsilon)
+    p.taps = taps.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if taps is not None else None
+    return _Prepared(image, image.width, image.height, sigma_milli, quality, bool(slrme), tmo_record, pre,
+                     post, taps, p, np.ascontiguousarray(px))
+
+
+def _image_struct(prep: _Prepared, rgbe_ptr: int) -> _native.Image:
+    im = _native.Image()
+    im.rgbe = rgbe_ptr
+    im.width, im.height = prep.w, prep.h
+    im.hdr_pre = ctypes.cast(ctypes.c_char_p(prep.pre), ctypes.c_void_p)
+    im.hdr_pre_len = len(prep.pre)
+    im.hdr_post = ctypes.cast(ctypes.c_char_p(prep.post), ctypes.c_void_p)
+    im.hdr_post_len = len(prep.post)
+    im.params = prep.params
+    return im
+
+
+def stream_capacity(prep: _Prepared) -> int:
+    return int(_native.lib().hdll_b200_stream_capacity(prep.w, prep.h, len(prep.pre), len(prep.post)))
+
+
+def _collect_trace(ctx, index: int, prep: _Prepared, stream: DualLayerStream, trace: dict):
+    L = _native.lib()
+    h, w = prep.h, prep.w
+    n3 = 3 * w * h
+
+    def grab(which):
+        buf = np.empty(n3, np.uint8)
+        _native.check(L.hdll_b200_trace(ctx.handle, index, which, buf.ctypes.data, n3), "trace")
+        return buf
+
+    trace["sdr"] = SdrImage.from_array(grab(0).reshape(h, w, 3))
+    trace["s"] = SdrImage.from_array(grab(1).reshape(h, w, 3))
+    planes = grab(2).reshape(3, h, w)
+    if stream.slrme:
+        trace["m_star"] = tuple(planes[c].copy() for c in range(3))
+    else:
+        s = trace["s"]
+        trace["m_star"] = (s.r, s.g, s.b)
+    res = grab(3).reshape(3, h, w)
+    trace["residuals"] = tuple(res[c].copy() for c in range(3))
+    trace["table"] = stream.regression_table
+
+
+def _stage_times(ctx) -> dict:
+    ms = (ctypes.c_float * len(STAGES))()
+    _native.check(_native.lib().hdll_b200_stage_times(ctx.handle, ms, len(STAGES)), "stage_times")
+    return dict(zip(STAGES, [float(v) for v in ms]))
+
+
+def encode(image, quality: int = 85, sigma: float = 1.0, slrme: bool = True, global_regression: bool = False,
+           lossy_coder: int = 1, lossless_coder: int = 1, tmo: TmoParams | None = None,
+           timings: dict | None = None, trace: dict | None = None, *, device: int = 0,
+           blas_kernel=None, blas_threads=None) -> DualLayerStream:
+    """container.py:131-230 on the B200: RGBE quads -> DualLayerStream.
+
+    `image` is any object with width, height, pixels ((h, w, 4) uint8),
+    header_vars and resolution_orientation (the reference's RadianceImage works).
+    `timings` receives per-stage device milliseconds plus host-side
+    `h2d_encode_d2h`; `trace` receives sdr, s, m_star, residuals and table like
+    the reference's trace hook (container.py:224-229)."""
+    t0 = time.perf_counter()
+    prep = _prepare(image, quality, sigma, slrme, global_regression, lossy_coder, lossless_coder, tmo,
+                    blas_kernel, blas_threads, trace is not None)
+    ctx = _native.context(device)
+    cap = stream_capacity(prep)
+    out = np.empty(cap, np.uint8)
+    olen = ctypes.c_uint64(0)
+    im = _image_struct(prep, prep.pixels.ctypes.data)
+    _native.check(_native.lib().hdll_b200_encode_host(ctx.handle, ctypes.byref(im), out.ctypes.data, cap,
+                                                      ctypes.byref(olen)), "encode")
+    stream = deserialize(out[: olen.value].tobytes())
+    if timings is not None:
+        timings.update(_stage_times(ctx))
+        timings["h2d_encode_d2h"] = (time.perf_counter() - t0) * 1000.0
+    if trace is not None:
+        _collect_trace(ctx, 0, prep, stream, trace)
+    return stream
+
+
+def encode_batch(images, quality: int = 85, sigma: float = 1.0, slrme: bool = True,
+                 global_regression: bool = False, tmo: TmoParams | None = None, *, device: int = 0,
+                 blas_kernel=None, blas_threads=None) -> list:
+    """Encode many images in one batched device pass; returns serialized streams (bytes)."""
+    import torch
+
+    preps = [_prepare(img, quality, sigma, slrme, global_regression, 1, 1, tmo, blas_kernel, blas_threads, False)
+             for img in images]
+    dev = torch.device("cuda", device)
+    ins = [torch.from_numpy(p.pixels).to(dev) for p in preps]
+    caps = [stream_capacity(p) for p in preps]
+    outs = [torch.empty(c, dtype=torch.uint8, device=dev) for c in caps]
+    lens = torch.zeros(len(preps), dtype=torch.int64, device=dev)
+    encode_device(preps, [t.data_ptr() for t in ins], [t.data_ptr() for t in outs], caps, lens.data_ptr(),
+                  torch.cuda.current_stream(dev).cuda_stream, device)
+    _native.check(_native.lib().hdll_b200_sync(_native.context(device).handle), "encode_batch")
+    nl = lens.cpu().numpy()
+    return [outs[i][: int(nl[i])].cpu().numpy().tobytes() for i in range(len(preps))]
+
+
+def prepare(image, quality: int = 85, sigma: float = 1.0, slrme: bool = True, global_regression: bool = False,
+            tmo: TmoParams | None = None, blas_kernel=None, blas_threads=None) -> _Prepared:
+    """Validate arguments and build the host-side header pieces once (bench / batch callers)."""
+    return _prepare(image, quality, sigma, slrme, global_regression, 1, 1, tmo, blas_kernel, blas_threads, False)
+
+
+def encode_device(preps, rgbe_ptrs, out_ptrs, out_caps, lens_ptr: int, stream_handle: int, device: int = 0):
+    """Asynchronous batched encode with RGBE inputs and stream outputs in HBM."""
+    n = len(preps)
+    ctx = _native.context(device)
+    arr = (_native.Image * n)(*[_image_struct(p, int(ptr)) for p, ptr in zip(preps, rgbe_ptrs)])
+    outs = (ctypes.c_void_p * n)(*[int(p) for p in out_ptrs])
+    caps = (ctypes.c_uint64 * n)(*[int(c) for c in out_caps])
+    _native.check(_native.lib().hdll_b200_encode_batch_device(ctx.handle, arr, n, outs, caps,
+                                                              ctypes.c_void_p(lens_ptr),
+                                                              ctypes.c_void_p(stream_handle)), "encode_batch")
+    return ctx

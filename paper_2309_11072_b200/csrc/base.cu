@@ -1,0 +1,247 @@
+// base.cu -- tone-map pass B + the base-layer 8x8 DCT round trip, fused.
+//
+// Reference chain (container.py:167-172):
+//   tone_map mapping pass          tonemap.py:100-110, srgb_quantize :113-118
+//   _BlockDctCoder.encode          codec_core.py:430-453
+//     np.pad edge / _rgb_to_ycc    :432-436, :391-403
+//     dct_blocks                   _kernels.py:381-400
+//     round_half_away(coef / qt)   :447, zigzag :448
+//   _reconstruct (== lossy_decode) codec_core.py:478-489, idct_blocks _kernels.py:403-422,
+//                                  _ycc_to_rgb :406-411
+// The reference obtains S by entropy-decoding its own payload (container.py:172);
+// that decode reproduces exactly the zz it just coded, so S is reconstructed here
+// straight from zz -- the entropy coder (entropy.cu) runs
+// separately on the same zz.
+//
+// One CTA = 8 pixel rows x 128 columns (16 blocks) of one image, 128 threads.
+// All block transforms stay in shared memory; fp64 with no contraction and the
+// reference's summation order (s = 0.0; s += C * x for t = 0..7).
+#include "encoder.cuh"
+
+namespace hdll {
+
+__constant__ double c_dct[64];  // DCT_MATRIX, _kernels.py:23-43 (row u, column t)
+__constant__ int c_zigzag[64];  // ZIGZAG, codec_core.py:364-372
+
+constexpr int kTileBlocks = 16;
+constexpr int kTileCols = kTileBlocks * 8;  // 128
+constexpr int kRowStride = kTileCols + 1;   // doubles; padding against bank conflicts
+
+__device__ __forceinline__ double rgbe_scale_b(unsigned e) {
+  return __longlong_as_double((long long)((int)e - 136 + 1023) << 52);
+}
+
+// tone_map pass B for one pixel -> 3 SDR bytes
+__device__ __forceinline__ void sdr_pixel(const ImgDesc& d, uint32_t q, double log_avg, double white, bool allzero,
+                                          uint8_t* out3) {
+  if (allzero || q == 0u) {
+    out3[0] = out3[1] = out3[2] = 0;
+    return;
+  }
+  double sc = rgbe_scale_b(q >> 24);
+  double f[3];
+  f[0] = ((double)(q & 0xFF) + 0.5) * sc;
+  f[1] = ((double)((q >> 8) & 0xFF) + 0.5) * sc;
+  f[2] = ((double)((q >> 16) & 0xFF) + 0.5) * sc;
+  double lw = 0.2126 * f[0] + 0.7152 * f[1] + 0.0722 * f[2];
+  double scaled = d.key * lw / log_avg;
+  double disp = scaled * (1.0 + scaled / (white * white)) / (1.0 + scaled);
+  double ratio = lw > 0 ? disp / lw : 0.0;
+#pragma unroll
+  for (int c = 0; c < 3; c++) {
+    double mapped = f[c] * ratio;
+    double v = pow(fmax(mapped, 0.0), d.inv_gamma);
+    double x = 255.0 * clampd(v, 0.0, 1.0);
+    out3[c] = (uint8_t)rha(x);
+  }
+}
+
+__global__ void __launch_bounds__(128) k_base_layer(const ImgDesc* __restrict__ descs) {
+  const ImgDesc& d = descs[blockIdx.y];
+  const int tiles_x = (d.nbx + kTileBlocks - 1) / kTileBlocks;
+  const int tile = blockIdx.x;
+  if (tile >= tiles_x * d.nby) return;
+  const int by = tile / tiles_x;
+  const int bx0 = (tile % tiles_x) * kTileBlocks;
+  const int nblk = min(kTileBlocks, d.nbx - bx0);
+
+  extern __shared__ double smem[];
+  double* bufA = smem;                      // [3][8][kRowStride]
+  double* bufB = smem + 3 * 8 * kRowStride;  // [3][8][kRowStride]
+  const int t = threadIdx.x;
+
+  const double log_avg = d.sdr_in ? 0.0 : d.scalars[1], white = d.sdr_in ? 0.0 : d.scalars[2];
+  const bool allzero = d.sdr_in ? false : d.scalars[3] != 0.0;
+
+  // 1. SDR (tone-map pass B) and YCC for every padded pixel of the tile
+  for (int p = t; p < 8 * kTileCols; p += blockDim.x) {
+    int ry = p / kTileCols, rx = p % kTileCols;
+    if (rx >= nblk * 8) continue;
+    int y = by * 8 + ry, x = bx0 * 8 + rx;
+    int sy = min(y, d.h - 1), sx = min(x, d.w - 1);  // np.pad mode="edge"
+    uint8_t s3[3];
+    if (d.sdr_in) {
+      const uint8_t* sp = d.sdr_in + ((long long)sy * d.w + sx) * 3;
+      s3[0] = sp[0], s3[1] = sp[1], s3[2] = sp[2];
+    } else {
+      uint32_t q = reinterpret_cast<const uint32_t*>(d.rgbe)[(long long)sy * d.w + sx];
+      sdr_pixel(d, q, log_avg, white, allzero, s3);
+    }
+    if (d.want_trace && y < d.h && x < d.w) {
+      uint8_t* o = d.sdr + ((long long)y * d.w + x) * 3;
+      o[0] = s3[0];
+      o[1] = s3[1];
+      o[2] = s3[2];
+    }
+    double r = s3[0], g = s3[1], b = s3[2];
+    double Y = 0.299 * r + 0.587 * g + 0.114 * b;
+    double cb = -0.168736 * r - 0.331264 * g + 0.5 * b;
+    double cr = 0.5 * r - 0.418688 * g - 0.081312 * b;
+    bufA[(0 * 8 + ry) * kRowStride + rx] = clampd(rha(Y), 0.0, 255.0);
+    bufA[(1 * 8 + ry) * kRowStride + rx] = clampd(rha(cb), -128.0, 127.0);
+    bufA[(2 * 8 + ry) * kRowStride + rx] = clampd(rha(cr), -128.0, 127.0);
+  }
+  __syncthreads();
+
+  // task t: block b = t / 8, line l = t % 8, for each of the 3 components
+  const int b = t >> 3, l = t & 7;
+  const bool live = b < nblk;
+  const int col0 = b * 8;
+
+  // 2. forward pass 1 (dct_blocks first loop): tmp[u][x] = sum_t C[u][t] * blk[t][x], x = l
+  if (live) {
+#pragma unroll
+    for (int ci = 0; ci < 3; ci++) {
+      double in[8];
+#pragma unroll
+      for (int tt = 0; tt < 8; tt++) in[tt] = bufA[(ci * 8 + tt) * kRowStride + col0 + l];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        double s = 0.0;
+#pragma unroll
+        for (int tt = 0; tt < 8; tt++) s += c_dct[u * 8 + tt] * in[tt];
+        bufB[(ci * 8 + u) * kRowStride + col0 + l] = s;
+      }
+    }
+  }
+  __syncthreads();
+
+  // 3. forward pass 2: out[u][v] = sum_t tmp[u][t] * C[v][t], u = l; quantise, zigzag, dequantise
+  const long long bi = (long long)by * d.nbx + bx0 + b;
+  if (live) {
+#pragma unroll
+    for (int ci = 0; ci < 3; ci++) {
+      const double* qt = d.qt + (ci == 0 ? 0 : 64);
+      double in[8];
+#pragma unroll
+      for (int tt = 0; tt < 8; tt++) in[tt] = bufB[(ci * 8 + l) * kRowStride + col0 + tt];
+      int16_t* zz = d.zz + ((long long)ci * d.nblocks + bi) * 64;
+#pragma unroll
+      for (int v = 0; v < 8; v++) {
+        double s = 0.0;
+#pragma unroll
+        for (int tt = 0; tt < 8; tt++) s += in[tt] * c_dct[v * 8 + tt];
+        double qv = qt[l * 8 + v];
+        double qz = rha(s / qv);
+        zz[c_zigzag[l * 8 + v]] = (int16_t)qz;
+        bufA[(ci * 8 + l) * kRowStride + col0 + v] = qz * qv;  // dequantised coefficient
+      }
+    }
+  }
+  __syncthreads();
+
+  // 4. inverse pass 1 (idct_blocks first loop): tmp[x][v] = sum_t C[t][x] * coef[t][v], v = l
+  if (live) {
+#pragma unroll
+    for (int ci = 0; ci < 3; ci++) {
+      double in[8];
+#pragma unroll
+      for (int tt = 0; tt < 8; tt++) in[tt] = bufA[(ci * 8 + tt) * kRowStride + col0 + l];
+#pragma unroll
+      for (int x = 0; x < 8; x++) {
+        double s = 0.0;
+#pragma unroll
+        for (int tt = 0; tt < 8; tt++) s += c_dct[tt * 8 + x] * in[tt];
+        bufB[(ci * 8 + x) * kRowStride + col0 + l] = s;
+      }
+    }
+  }
+  __syncthreads();
+
+  // 5. inverse pass 2: out[x][y] = sum_t tmp[x][t] * C[t][y], x = l
+  if (live) {
+#pragma unroll
+    for (int ci = 0; ci < 3; ci++) {
+      double in[8];
+#pragma unroll
+      for (int tt = 0; tt < 8; tt++) in[tt] = bufB[(ci * 8 + l) * kRowStride + col0 + tt];
+#pragma unroll
+      for (int y = 0; y < 8; y++) {
+        double s = 0.0;
+#pragma unroll
+        for (int tt = 0; tt < 8; tt++) s += in[tt] * c_dct[tt * 8 + y];
+        bufA[(ci * 8 + l) * kRowStride + col0 + y] = s;
+      }
+    }
+  }
+  __syncthreads();
+
+  // 6. _ycc_to_rgb on the cropped planes -> decoded S (3 planes)
+  for (int p = t; p < 8 * kTileCols; p += blockDim.x) {
+    int ry = p / kTileCols, rx = p % kTileCols;
+    int y = by * 8 + ry, x = bx0 * 8 + rx;
+    if (rx >= nblk * 8 || y >= d.h || x >= d.w) continue;
+    double Y = bufA[(0 * 8 + ry) * kRowStride + rx];
+    double cb = bufA[(1 * 8 + ry) * kRowStride + rx];
+    double cr = bufA[(2 * 8 + ry) * kRowStride + rx];
+    double v[3];
+    v[0] = Y + 1.402 * cr;
+    v[1] = Y - 0.344136 * cb - 0.714136 * cr;
+    v[2] = Y + 1.772 * cb;
+    long long pi = (long long)y * d.w + x;
+#pragma unroll
+    for (int c = 0; c < 3; c++) d.s_planes[c * d.n + pi] = (uint8_t)clampd(rha(v[c]), 0.0, 255.0);
+  }
+}
+
+void upload_base_constants() {
+  static const double dct[64] = {
+      0.35355339059327373, 0.35355339059327373, 0.35355339059327373, 0.35355339059327373,
+      0.35355339059327373, 0.35355339059327373, 0.35355339059327373, 0.35355339059327373,
+      0.4903926402016152,  0.4157348061512726,  0.27778511650980114, 0.09754516100806417,
+      -0.0975451610080641, -0.277785116509801,  -0.4157348061512727, -0.4903926402016152,
+      0.46193976625564337, 0.19134171618254492, -0.19134171618254486, -0.46193976625564337,
+      -0.4619397662556434, -0.19134171618254517, 0.191341716182545,   0.46193976625564326,
+      0.4157348061512726,  -0.0975451610080641, -0.4903926402016152, -0.2777851165098011,
+      0.2777851165098009,  0.4903926402016152,  0.09754516100806439, -0.41573480615127256,
+      0.3535533905932738,  -0.35355339059327373, -0.35355339059327384, 0.3535533905932737,
+      0.35355339059327384, -0.35355339059327334, -0.35355339059327356, 0.3535533905932733,
+      0.27778511650980114, -0.4903926402016152, 0.09754516100806415, 0.41573480615127273,
+      -0.41573480615127256, -0.09754516100806401, 0.4903926402016153, -0.27778511650980076,
+      0.19134171618254492, -0.4619397662556434, 0.46193976625564326, -0.19134171618254495,
+      -0.19134171618254528, 0.46193976625564337, -0.4619397662556432, 0.19134171618254478,
+      0.09754516100806417, -0.2777851165098011, 0.41573480615127273, -0.4903926402016153,
+      0.4903926402016152,  -0.4157348061512725, 0.27778511650980076, -0.09754516100806429};
+  static const int zig[64] = {0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25, 18, 11, 4,  5,
+                              12, 19, 26, 33, 40, 48, 41, 34, 27, 20, 13, 6,  7,  14, 21, 28,
+                              35, 42, 49, 56, 57, 50, 43, 36, 29, 22, 15, 23, 30, 37, 44, 51,
+                              58, 59, 52, 45, 38, 31, 39, 46, 53, 60, 61, 54, 47, 55, 62, 63};
+  // zz index k holds natural coefficient ZIGZAG[k]; the kernel scatters natural
+  // position j to zz slot inv[j] where ZIGZAG[inv[j]] == j.
+  int inv[64];
+  for (int k = 0; k < 64; k++) inv[zig[k]] = k;
+  cudaMemcpyToSymbol(c_dct, dct, sizeof(dct));
+  cudaMemcpyToSymbol(c_zigzag, inv, sizeof(inv));
+}
+
+void launch_base_layer(const ImgDesc* d_descs, int nimg, int max_tiles, cudaStream_t st) {
+  size_t smem = sizeof(double) * 2 * 3 * 8 * kRowStride;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_base_layer, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_base_layer<<<dim3(max_tiles, nimg), 128, smem, st>>>(d_descs);
+}
+
+}  // namespace hdll

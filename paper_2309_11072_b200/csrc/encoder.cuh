@@ -1,0 +1,149 @@
+// encoder.cuh -- per-image descriptor shared by every stage of the batched
+// B200 encode pipeline, plus the host-side launcher declarations.
+//
+// One batch = a list of independent images (BASELINE configs 1 and 4).  Every
+// kernel takes the device array of ImgDesc and derives its image from the
+// grid (blockIdx.y) or from a flattened tile index, so a whole batch runs as
+// one launch per stage.  All per-image intermediates live in one device arena
+// carved by the host (api.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace hdll {
+
+struct ImgDesc {
+  // geometry
+  int w, h;
+  long long n;          // w*h
+  int pw, ph;           // padded to a multiple of 8
+  int nbx, nby;         // blocks per row / column
+  long long nblocks;    // nbx*nby
+
+  // parameters (container.py:131-142)
+  int quality;
+  int sigma_milli;
+  int slrme;
+  int global_regression;
+  int blas_kernel;      // 0 SKYLAKEX, 1 HASWELL
+  int blas_threads;
+  int radius;           // Gaussian radius ceil(3 sigma)
+  int want_trace;
+  double key, white_point /* <=0: auto */, inv_gamma, epsilon;
+  const double* taps;   // 2*radius+1 taps computed on the host with numpy (estimator.py:120-127)
+  const double* qt;     // 128 doubles: luma[64] then chroma[64], natural order
+
+  // input
+  const uint8_t* rgbe;  // (h, w, 4), 16-byte aligned
+  const uint8_t* sdr_in;  // lossy-coder plugin mode: (h, w, 3) SDR given directly (codec_core.py:430)
+  int crc_mask;           // which of the 5 CRC jobs to run
+
+  // tone-map stage
+  double* logv;               // n: log(eps + Lw)
+  unsigned long long* maxlw;  // bits of max Lw (Lw >= 0)
+  double* tm_nodes;           // pairwise-sum level-L node values
+  int tm_level;               // L for the image-wide pairwise tree
+  double* scalars;            // [0] log-sum, [1] log_avg, [2] white, [3] allzero flag
+
+  // base layer
+  uint8_t* sdr;               // trace: (h, w, 3) pre-coding SDR (optional)
+  uint8_t* s_planes;          // 3 planes (h, w): decoded S
+  int16_t* zz;                // [3][nblocks][64] zigzag quantised coefficients
+
+  // enhancement
+  double* sstar;              // 3 planes (h, w) f64 (sigma > 0)
+  double* sstar_tmp;          // vertical-pass scratch (h, w)
+  uint8_t* e_plane;           // (h, w)
+  uint8_t* res_planes;        // 3 planes (h, w)
+  uint8_t* mstar;             // trace: 3 planes (optional)
+
+  // SLRME fit
+  int sort_tiles;             // tiles of kSortTile pixels
+  unsigned* tile_hist;        // [sort_tiles][256] (then tile offsets)
+  unsigned* order;            // n: pixel indices stable-sorted by E
+  unsigned* bin_count;        // 256
+  unsigned* bin_start;        // 257
+  long long* sum_y;           // [3][256] exact integer sums of M per bin
+  double* seg_nodes;          // pairwise node values of every (channel, bin) segment
+  int* seg_level;             // [3*256] L per segment
+  long long* seg_node_off;    // [3*256+1] node offsets
+  double* dot_part;           // [3*256][kMaxBlasThreads][2] ddot partials (xx, xy)
+  float* a32;                 // [3][256]
+  float* b32;                 // [3][256]
+
+  // CRCs: 0 base (decoded RGB), 1 E, 2..4 residual R,G,B
+  unsigned* crc;              // [5]
+  unsigned* crc_part;         // per-chunk partial crcs
+  long long crc_chunks[5];
+  long long crc_part_off[5];
+
+  // entropy engines (bitstreams live in per-tile staging, see entropy.cu)
+  int n_dct_tiles;            // 3 * ceil(nblocks / 32)
+  int n_plane_tiles;          // 4 * h (one tile per row per plane)
+
+  // output
+  uint8_t* out;               // serialized stream
+  unsigned long long* out_len;
+  long long out_cap;
+  const uint8_t* hdr_pre;     // fixed header + TMO record (host-built)
+  int hdr_pre_len;
+  const uint8_t* hdr_post;    // u32 length + header text block
+  int hdr_post_len;
+  unsigned* status;           // error bits
+};
+
+constexpr int kMaxBlasThreads = 64;
+constexpr int kSortTile = 4096;
+constexpr int kCrcChunk = 1024;       // bytes per CRC partial
+constexpr int kNodeTarget = 1024;     // pairwise-sum level-L node size target
+
+// pairwise tree level so level-L nodes hold >= kNodeTarget elements
+inline __host__ __device__ int pairwise_level(long long n) {
+  int L = 0;
+  while ((n >> (L + 1)) >= kNodeTarget) L++;
+  return L;
+}
+
+constexpr int kMaxCtx = 6;
+
+// Sequential-coder chains for the entropy kernel (entropy.cu).
+struct ChainTab {
+  int nchains;
+  const long long* tile_base;  // [nchains+1] global tile index of each chain's tile 0
+  const int* img;              // image of the chain
+  const int* kind;             // 0 = DCT stream, 1..4 = plane (E, R, G, B)
+  uint8_t* const* out;         // chain byte stream (4-byte aligned)
+  const long long* cap;        // capacity in bytes
+  unsigned long long* bits;    // [nchains] total bits (written by the last tile)
+  // per global tile status (epoch-tagged)
+  int* flags;                  // [ntiles][4]: cnt, map, bit, done
+  long long* cnt;              // [ntiles][2][kMaxCtx]: aggregate, inclusive
+  AMap* maps;                  // [ntiles][kMaxCtx]: aggregate
+  int* states;                 // [ntiles][kMaxCtx]: inclusive A
+  unsigned long long* bitv;    // [ntiles][2]
+  int* ticket;
+  long long ntiles;
+  int epoch;
+};
+
+struct AsmTab {
+  uint8_t* const* chain_out;                 // per chain byte streams
+  const unsigned long long* chain_bits;      // per chain bit totals
+  const int* img_chain0;                     // first chain (the DCT chain) of each image; planes follow
+};
+
+void upload_base_constants();
+void upload_crc_constants();
+void launch_tonemap_stats(const ImgDesc*, int nimg, long long max_n, int max_level, cudaStream_t);
+void launch_base_layer(const ImgDesc*, int nimg, int max_tiles, cudaStream_t);
+void launch_prefilter(const ImgDesc*, int nimg, int max_w, int max_h, int max_radius, cudaStream_t);
+void launch_fit(const ImgDesc*, int nimg, int max_sort_tiles, long long max_nodes, cudaStream_t);
+void launch_estimate(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
+void launch_crc(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
+void launch_entropy(const ImgDesc*, const ChainTab&, cudaStream_t);
+void launch_assemble(const ImgDesc*, int nimg, const AsmTab&, long long max_out, cudaStream_t);
+
+}  // namespace hdll

@@ -1,0 +1,67 @@
+// estimate.cu -- M* estimate, mod-256 residuals and the exponent plane.
+//
+// estimate_mantissa (estimator.py:217-244): M* = clip(rha(a_E * S* + b_E), 0, 255)
+// with float32-valued a/b (multiply then add, no FMA); residuals
+// r = (M - M*) & 255 (container.py:187-190); slrme=False uses M* = S
+// (container.py:182-185).  The E plane is split_planes' 4th byte
+// (radiance_io.py:328-338).  4 pixels per thread through one 128-bit load.
+#include "encoder.cuh"
+
+namespace hdll {
+
+__global__ void __launch_bounds__(256) k_estimate(const ImgDesc* __restrict__ descs) {
+  const ImgDesc& d = descs[blockIdx.y];
+  __shared__ float sa[3 * 256], sb[3 * 256];
+  if (d.slrme)
+    for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) {
+      sa[i] = d.a32[i];
+      sb[i] = d.b32[i];
+    }
+  __syncthreads();
+  const bool real = d.sigma_milli != 0;
+  long long nq = (d.n + 3) / 4;
+  for (long long qi = (long long)blockIdx.x * blockDim.x + threadIdx.x; qi < nq;
+       qi += (long long)gridDim.x * blockDim.x) {
+    long long p0 = qi * 4;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(d.rgbe);
+    uint32_t qs[4];
+    if (p0 + 3 < d.n) {
+      uint4 v = __ldg(reinterpret_cast<const uint4*>(d.rgbe) + qi);
+      qs[0] = v.x, qs[1] = v.y, qs[2] = v.z, qs[3] = v.w;
+    } else {
+      for (int k = 0; k < 4; k++) qs[k] = p0 + k < d.n ? src[p0 + k] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      long long p = p0 + k;
+      if (p >= d.n) break;
+      uint32_t q = qs[k];
+      unsigned e = q >> 24;
+      d.e_plane[p] = (uint8_t)e;
+#pragma unroll
+      for (int c = 0; c < 3; c++) {
+        unsigned m = (q >> (8 * c)) & 0xFF;
+        unsigned ms;
+        if (d.slrme) {
+          double s = real ? d.sstar[(long long)c * d.n + p] : (double)d.s_planes[(long long)c * d.n + p];
+          double est = (double)sa[c * 256 + e] * s + (double)sb[c * 256 + e];
+          ms = (unsigned)clampd(rha(est), 0.0, 255.0);
+        } else {
+          ms = d.s_planes[(long long)c * d.n + p];
+        }
+        if (d.want_trace) d.mstar[(long long)c * d.n + p] = (uint8_t)ms;
+        d.res_planes[(long long)c * d.n + p] = (uint8_t)((m - ms) & 255u);
+      }
+    }
+  }
+}
+
+void launch_estimate(const ImgDesc* d_descs, int nimg, long long max_n, cudaStream_t st) {
+  long long nq = (max_n + 3) / 4;
+  int gx = (int)((nq + 255) / 256);
+  if (gx > 148 * 8) gx = 148 * 8;
+  if (gx < 1) gx = 1;
+  k_estimate<<<dim3(gx, nimg), 256, 0, st>>>(d_descs);
+}
+
+}  // namespace hdll

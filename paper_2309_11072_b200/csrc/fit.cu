@@ -1,0 +1,415 @@
+// fit.cu -- SLRME per-(channel, exponent) regression (estimator.py:145-214).
+//
+// For every channel c and exponent e present (ascending), the reference fits
+// x = S*[E == e], y = M[E == e] in raster order with
+//   sx = x.sum()        numpy pairwise sum              (estimator.py:159)
+//   sy = y.sum()        exact (integer-valued)          (:160)
+//   sxx = np.dot(x, x), sxy = np.dot(x, y)   OpenBLAS ddot (:161-162)
+//   den = n*sxx - sx*sx; a = (n*sxy - sx*sy)/den; b = (sy - a*sx)/n, with the
+//   degenerate fallback (0, sy/n)           (:163-169), then float32 RNE (:205-214).
+// With sigma > 0 S* is real-valued and the float sums are order dependent, so
+// the GPU follows the reference's order exactly:
+//   1. stable counting sort of pixel indices by E (raster order inside a bin);
+//   2. pairwise tree for sx (pairwise.cuh) over each bin's sorted samples;
+//   3. the OpenBLAS kernel's lane structure for sxx/sxy: 32 (SKYLAKEX) or 16
+//      (HASWELL) sequential FMA chains, its fold order, its tail, and the
+//      level-1 thread split (n > 10000) as a parameter (blas_threads);
+//   4. the fit formula in fp64 and __double2float_rn.
+// sy and the counts are exact integers (int64 atomics).
+#include "encoder.cuh"
+#include "pairwise.cuh"
+
+namespace hdll {
+
+constexpr int kSegs = 3 * 256;
+
+// ---------------------------------------------------------------------------
+// 1. stable counting sort by exponent
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_sort_hist(const ImgDesc* __restrict__ descs) {
+  const ImgDesc& d = descs[blockIdx.y];
+  if (!d.slrme) return;
+  const int tile = blockIdx.x;
+  if (tile >= d.sort_tiles) return;
+  __shared__ unsigned hist[256];
+  __shared__ unsigned long long sy[3][256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    hist[i] = 0;
+    sy[0][i] = sy[1][i] = sy[2][i] = 0;
+  }
+  __syncthreads();
+  const long long p0 = (long long)tile * kSortTile;
+  const long long p1 = min(d.n, p0 + kSortTile);
+  const uint32_t* px = reinterpret_cast<const uint32_t*>(d.rgbe);
+  for (long long p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+    uint32_t q = px[p];
+    unsigned e = q >> 24;
+    atomicAdd(&hist[e], 1u);
+    atomicAdd(&sy[0][e], (unsigned long long)(q & 0xFF));
+    atomicAdd(&sy[1][e], (unsigned long long)((q >> 8) & 0xFF));
+    atomicAdd(&sy[2][e], (unsigned long long)((q >> 16) & 0xFF));
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 256; e += blockDim.x) {
+    d.tile_hist[(long long)tile * 256 + e] = hist[e];
+    if (hist[e]) {
+      atomicAdd(&d.bin_count[e], hist[e]);
+      for (int c = 0; c < 3; c++)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&d.sum_y[c * 256 + e]), sy[c][e]);
+    }
+  }
+}
+
+// bin starts + per-tile absolute offsets (in place over tile_hist)
+__global__ void __launch_bounds__(256) k_sort_scan(const ImgDesc* __restrict__ descs) {
+  const ImgDesc& d = descs[blockIdx.x];
+  if (!d.slrme) return;
+  const int e = threadIdx.x;
+  __shared__ unsigned cnt[256];
+  cnt[e] = d.bin_count[e];
+  __syncthreads();
+  if (e == 0) {
+    unsigned run = 0;
+    for (int k = 0; k < 256; k++) {
+      d.bin_start[k] = run;
+      run += cnt[k];
+    }
+    d.bin_start[256] = run;
+  }
+  __syncthreads();
+  unsigned run = d.bin_start[e];
+  for (int t = 0; t < d.sort_tiles; t++) {
+    unsigned* slot = &d.tile_hist[(long long)t * 256 + e];
+    unsigned c = *slot;
+    *slot = run;
+    run += c;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_sort_scatter(const ImgDesc* __restrict__ descs) {
+  const ImgDesc& d = descs[blockIdx.y];
+  if (!d.slrme) return;
+  const int tile = blockIdx.x;
+  if (tile >= d.sort_tiles) return;
+  __shared__ unsigned wcnt[8][256];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&wcnt[0][0])[i] = 0;
+  __syncthreads();
+  const long long base = (long long)tile * kSortTile + (long long)w * (kSortTile / 8);
+  const uint32_t* px = reinterpret_cast<const uint32_t*>(d.rgbe);
+  const unsigned lt = (1u << lane) - 1u;
+  for (int step = 0; step < kSortTile / 8 / 32; step++) {
+    long long p = base + step * 32 + lane;
+    bool valid = p < d.n;
+    unsigned act = __ballot_sync(0xffffffffu, valid);
+    if (valid) {
+      unsigned e = px[p] >> 24;
+      unsigned peers = __match_any_sync(act, e);
+      if ((peers & lt) == 0) wcnt[w][e] += __popc(peers);
+    }
+  }
+  __syncthreads();
+  {
+    const int e = threadIdx.x;
+    unsigned run = d.tile_hist[(long long)tile * 256 + e];
+    for (int k = 0; k < 8; k++) {
+      unsigned c = wcnt[k][e];
+      wcnt[k][e] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (int step = 0; step < kSortTile / 8 / 32; step++) {
+    long long p = base + step * 32 + lane;
+    bool valid = p < d.n;
+    unsigned act = __ballot_sync(0xffffffffu, valid);
+    unsigned e = 0, peers = 0, pos = 0;
+    if (valid) {
+      e = px[p] >> 24;
+      peers = __match_any_sync(act, e);
+      pos = wcnt[w][e] + __popc(peers & lt);
+      d.order[pos] = (unsigned)p;
+    }
+    __syncwarp();
+    if (valid && (peers & lt) == 0) wcnt[w][e] += __popc(peers);
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 2. segments: (channel, bin) or (channel, whole plane) for global_regression
+// ---------------------------------------------------------------------------
+struct SegView {
+  long long n, off;
+  bool identity;
+};
+
+__device__ __forceinline__ SegView seg_view(const ImgDesc& d, int s) {
+  int e = s & 255;
+  SegView v;
+  if (d.global_regression) {
+    v.n = e == 0 ? d.n : 0;
+    v.off = 0;
+    v.identity = true;
+  } else {
+    v.n = d.bin_count[e];
+    v.off = d.bin_start[e];
+    v.identity = false;
+  }
+  return v;
+}
+
+struct XAcc {  // x[i] = S*_c at the i-th sorted sample of a segment
+  const double* sf;
+  const uint8_t* s8;
+  const unsigned* ord;
+  __device__ double operator()(long long i) const {
+    long long p = ord ? (long long)ord[i] : i;
+    return sf ? sf[p] : (double)s8[p];
+  }
+};
+
+__device__ __forceinline__ XAcc x_acc(const ImgDesc& d, int c, const SegView& v) {
+  XAcc a;
+  bool real = d.sigma_milli != 0;
+  a.sf = real ? d.sstar + (long long)c * d.n : nullptr;
+  a.s8 = real ? nullptr : d.s_planes + (long long)c * d.n;
+  a.ord = v.identity ? nullptr : d.order + v.off;
+  return a;
+}
+
+__global__ void k_seg_setup(const ImgDesc* __restrict__ descs) {
+  const ImgDesc& d = descs[blockIdx.x];
+  if (!d.slrme || threadIdx.x != 0) return;
+  long long off = 0;
+  for (int s = 0; s < kSegs; s++) {
+    SegView v = seg_view(d, s);
+    int L = v.n > 0 ? pairwise_level(v.n) : 0;
+    d.seg_level[s] = L;
+    d.seg_node_off[s] = off;
+    off += v.n > 0 ? (1LL << L) : 0;
+  }
+  d.seg_node_off[kSegs] = off;
+}
+
+__global__ void __launch_bounds__(128) k_seg_nodes(const ImgDesc* __restrict__ descs) {
+  const ImgDesc& d = descs[blockIdx.y];
+  if (!d.slrme) return;
+  long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= d.seg_node_off[kSegs]) return;
+  int lo = 0, hi = kSegs;  // find s with off[s] <= g < off[s+1]
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (d.seg_node_off[mid] <= g) lo = mid; else hi = mid;
+  }
+  const int s = lo;
+  SegView v = seg_view(d, s);
+  long long off, sz;
+  pairwise_node(v.n, d.seg_level[s], g - d.seg_node_off[s], &off, &sz);
+  d.seg_nodes[g] = pairwise_seq(x_acc(d, s >> 8, v), off, sz);
+}
+
+// ---------------------------------------------------------------------------
+// 3. OpenBLAS ddot models (oracle/hdll_oracle.c ddot_compute), one warp per
+//    (segment, thread-chunk); both dots (x.x and x.y) in one sweep.
+// ---------------------------------------------------------------------------
+struct MAcc {  // y[i] = M_c (mantissa byte c of the RGBE quad) at the i-th sorted sample
+  const uint8_t* px;
+  const unsigned* ord;
+  int c;
+  __device__ double operator()(long long i) const {
+    long long p = ord ? (long long)ord[i] : i;
+    return (double)px[p * 4 + c];
+  }
+};
+
+template <class XA, class YA>
+__device__ void warp_ddot2(const XA& X, const YA& Y, long long start, long long len, int kernel, double* out_xx,
+                           double* out_xy) {
+  const int lane = threadIdx.x & 31;
+  long long n1 = len & ~15LL;
+  double dxx = 0.0, dxy = 0.0;
+  if (kernel == 0) {  // SKYLAKEX
+    long long n32 = n1 & ~31LL;
+    double axx = 0.0, axy = 0.0;
+    for (long long i = lane; i < n32; i += 32) {
+      double x = X(start + i), y = Y(start + i);
+      axx = __fma_rn(x, x, axx);
+      axy = __fma_rn(x, y, axy);
+    }
+    // fold 512 -> 256: lane 8k+l (l < 4) holds acc[8k+l] + acc[8k+l+4]
+    double fxx = axx + __shfl_down_sync(0xffffffffu, axx, 4);
+    double fxy = axy + __shfl_down_sync(0xffffffffu, axy, 4);
+    // 256-bit loop over [n32, n1): four 4-lane accumulators, 16 elements per step
+    if ((lane & 7) < 4) {
+      int k = lane >> 3, l = lane & 7;
+      for (long long i = n32; i < n1; i += 16) {
+        double x = X(start + i + 4 * k + l), y = Y(start + i + 4 * k + l);
+        fxx = __fma_rn(x, x, fxx);
+        fxy = __fma_rn(x, y, fxy);
+      }
+    }
+    // s[l] = ((a0[l] + a1[l]) + a2[l]) + a3[l]; dot = (s0 + s2) + (s1 + s3)
+    double s_xx[4], s_xy[4];
+#pragma unroll
+    for (int l = 0; l < 4; l++) {
+      double v0 = __shfl_sync(0xffffffffu, fxx, l), v1 = __shfl_sync(0xffffffffu, fxx, 8 + l);
+      double v2 = __shfl_sync(0xffffffffu, fxx, 16 + l), v3 = __shfl_sync(0xffffffffu, fxx, 24 + l);
+      s_xx[l] = ((v0 + v1) + v2) + v3;
+      v0 = __shfl_sync(0xffffffffu, fxy, l);
+      v1 = __shfl_sync(0xffffffffu, fxy, 8 + l);
+      v2 = __shfl_sync(0xffffffffu, fxy, 16 + l);
+      v3 = __shfl_sync(0xffffffffu, fxy, 24 + l);
+      s_xy[l] = ((v0 + v1) + v2) + v3;
+    }
+    if (n1) {
+      dxx = (s_xx[0] + s_xx[2]) + (s_xx[1] + s_xx[3]);
+      dxy = (s_xy[0] + s_xy[2]) + (s_xy[1] + s_xy[3]);
+    }
+    if (lane == 0)  // tail: dot = fma(y, x, dot)
+      for (long long i = n1; i < len; i++) {
+        double x = X(start + i), y = Y(start + i);
+        dxx = __fma_rn(x, x, dxx);
+        dxy = __fma_rn(y, x, dxy);
+      }
+  } else {  // HASWELL: 16 lanes, lane 4k+l = acc[k][l]
+    double axx = 0.0, axy = 0.0;
+    if (lane < 16)
+      for (long long i = lane; i < n1; i += 16) {
+        double x = X(start + i), y = Y(start + i);
+        axx = __fma_rn(x, x, axx);
+        axy = __fma_rn(x, y, axy);
+      }
+    double a[16], b[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+      a[j] = __shfl_sync(0xffffffffu, axx, j);
+      b[j] = __shfl_sync(0xffffffffu, axy, j);
+    }
+    if (n1) {
+      double t0[4], t1[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        t0[k] = a[4 * k + 0] + a[4 * k + 2];
+        t1[k] = a[4 * k + 1] + a[4 * k + 3];
+      }
+      double u0 = t0[0] + t0[1], u1 = t1[0] + t1[1], v0 = t0[2] + t0[3], v1 = t1[2] + t1[3];
+      dxx = (u0 + v0) + (u1 + v1);
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        t0[k] = b[4 * k + 0] + b[4 * k + 2];
+        t1[k] = b[4 * k + 1] + b[4 * k + 3];
+      }
+      u0 = t0[0] + t0[1];
+      u1 = t1[0] + t1[1];
+      v0 = t0[2] + t0[3];
+      v1 = t1[2] + t1[3];
+      dxy = (u0 + v0) + (u1 + v1);
+    }
+    if (lane == 0)  // tail without fma
+      for (long long i = n1; i < len; i++) {
+        double x = X(start + i), y = Y(start + i);
+        dxx = dxx + x * x;
+        dxy = dxy + y * x;
+      }
+  }
+  *out_xx = dxx;
+  *out_xy = dxy;
+}
+
+// grid: (kSegs, nimg), blockDim = 32 * warps; warp j handles thread-chunk j
+__global__ void __launch_bounds__(256) k_seg_dot(const ImgDesc* __restrict__ descs) {
+  const ImgDesc& d = descs[blockIdx.y];
+  if (!d.slrme) return;
+  const int s = blockIdx.x;
+  SegView v = seg_view(d, s);
+  if (v.n == 0) return;
+  const int c = s >> 8;
+  const XAcc X = x_acc(d, c, v);
+  const MAcc M{d.rgbe, X.ord, c};
+  const int T = (v.n > 10000 && d.blas_threads > 1) ? min(d.blas_threads, kMaxBlasThreads) : 1;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = warp; j < T; j += nw) {
+    // chunk j of OpenBLAS's level-1 split: width = ceil(rem / (T - used))
+    long long start = 0, rem = v.n, width = 0;
+    for (int u = 0; u <= j; u++) {
+      width = (rem + (T - u) - 1) / (T - u);
+      if (width > rem) width = rem;
+      if (u < j) {
+        start += width;
+        rem -= width;
+      }
+    }
+    double xx, xy;
+    warp_ddot2(X, M, start, width, d.blas_kernel, &xx, &xy);
+    if ((threadIdx.x & 31) == 0) {
+      d.dot_part[((long long)s * kMaxBlasThreads + j) * 2 + 0] = xx;
+      d.dot_part[((long long)s * kMaxBlasThreads + j) * 2 + 1] = xy;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 4. coefficients (fit_region, estimator.py:145-169) -> float32 table
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_seg_reduce_coef(const ImgDesc* __restrict__ descs) {
+  const ImgDesc& d = descs[blockIdx.y];
+  if (!d.slrme) return;
+  const int s = blockIdx.x;
+  SegView v = seg_view(d, s);
+  if (v.n == 0) return;
+  __shared__ double sm[256];
+  double sx = tree_reduce_block(d.seg_nodes + d.seg_node_off[s], d.seg_level[s], sm);
+  if (threadIdx.x != 0) return;
+  sx = 0.0 + sx;
+  const int c = s >> 8;
+  long long sy_i = 0;
+  if (d.global_regression) {
+    for (int e = 0; e < 256; e++) sy_i += d.sum_y[c * 256 + e];
+  } else {
+    sy_i = d.sum_y[s];
+  }
+  const double sy = (double)sy_i;
+  const int T = (v.n > 10000 && d.blas_threads > 1) ? min(d.blas_threads, kMaxBlasThreads) : 1;
+  double sxx = 0.0, sxy = 0.0;
+  for (int j = 0; j < T; j++) {  // OpenBLAS: dot = dot + partial_j
+    sxx = sxx + d.dot_part[((long long)s * kMaxBlasThreads + j) * 2 + 0];
+    sxy = sxy + d.dot_part[((long long)s * kMaxBlasThreads + j) * 2 + 1];
+  }
+  sxx = 0.0 + sxx;  // numpy DOUBLE_dot: sum = 0.0; sum += cblas_ddot(...)
+  sxy = 0.0 + sxy;
+  const double dn = (double)v.n;
+  double a = 0.0, b = sy / dn;
+  double den = dn * sxx - sx * sx;
+  if (den > 0.0) {
+    double aa = (dn * sxy - sx * sy) / den;
+    double bb = (sy - aa * sx) / dn;
+    if (isfinite(aa) && isfinite(bb)) {
+      a = aa;
+      b = bb;
+    }
+  }
+  float a32 = __double2float_rn(a), b32 = __double2float_rn(b);
+  if (d.global_regression) {
+    for (int e = 0; e < 256; e++) {
+      d.a32[c * 256 + e] = a32;
+      d.b32[c * 256 + e] = b32;
+    }
+  } else {
+    d.a32[s] = a32;
+    d.b32[s] = b32;
+  }
+  if (!isfinite(a32) || !isfinite(b32)) atomicOr(d.status, kErrNonFinite);
+}
+
+void launch_fit(const ImgDesc* d_descs, int nimg, int max_sort_tiles, long long max_nodes, cudaStream_t st) {
+  k_sort_hist<<<dim3(max_sort_tiles, nimg), 256, 0, st>>>(d_descs);
+  k_sort_scan<<<nimg, 256, 0, st>>>(d_descs);
+  k_sort_scatter<<<dim3(max_sort_tiles, nimg), 256, 0, st>>>(d_descs);
+  k_seg_setup<<<nimg, 32, 0, st>>>(d_descs);
+  k_seg_nodes<<<dim3((unsigned)((max_nodes + 127) / 128), nimg), 128, 0, st>>>(d_descs);
+  k_seg_dot<<<dim3(kSegs, nimg), 256, 0, st>>>(d_descs);
+  k_seg_reduce_coef<<<dim3(kSegs, nimg), 256, 0, st>>>(d_descs);
+}
+
+}  // namespace hdll

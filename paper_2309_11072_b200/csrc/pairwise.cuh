@@ -1,0 +1,116 @@
+// pairwise.cuh -- numpy's float64 pairwise summation, restated for the GPU.
+//
+// numpy reduces a contiguous float64 array as 0.0 + pairwise(a, n) with
+// (numpy/_core/src/umath/loops_utils.h pairwise_sum_DOUBLE):
+//   n < 8     : sequential from 0.0
+//   n <= 128  : 8 strided accumulators, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)),
+//               then the sequential tail
+//   otherwise : n2 = n/2 - (n/2 % 8); pairwise(a, n2) + pairwise(a+n2, n-n2)
+// Call sites on the hot path: np.mean in tone_map (tonemap.py:101) and
+// x.sum() in fit_region (estimator.py:159).  Verified against numpy in
+// tests/test_oracle.py (oracle/hdll_oracle.c ho_pairwise_sum).
+//
+// GPU form: the recursion tree is cut at depth L (pairwise_level); each
+// depth-L node is summed sequentially by one thread (its subtree is exactly
+// numpy's), and the 2^L node sums are combined by a perfect binary tree,
+// which is the same sequence of `left + right` additions numpy performs.
+#pragma once
+
+#include "encoder.cuh"
+
+namespace hdll {
+
+// (offset, size) of node `idx` at depth L of the pairwise tree over n elements.
+__device__ __forceinline__ void pairwise_node(long long n, int L, long long idx, long long* off, long long* size) {
+  long long o = 0, m = n;
+  for (int l = L - 1; l >= 0; l--) {
+    long long n2 = m / 2;
+    n2 -= n2 % 8;
+    if ((idx >> l) & 1) {
+      o += n2;
+      m -= n2;
+    } else {
+      m = n2;
+    }
+  }
+  *off = o;
+  *size = m;
+}
+
+template <class Acc>
+__device__ double pairwise_seq(const Acc& a, long long off, long long n) {
+  if (n < 8) {
+    double res = 0.;
+    for (long long i = 0; i < n; i++) res += a(off + i);
+    return res;
+  } else if (n <= 128) {
+    double r0 = a(off + 0), r1 = a(off + 1), r2 = a(off + 2), r3 = a(off + 3);
+    double r4 = a(off + 4), r5 = a(off + 5), r6 = a(off + 6), r7 = a(off + 7);
+    long long i;
+    long long lim = n - (n % 8);
+    for (i = 8; i < lim; i += 8) {
+      r0 += a(off + i + 0);
+      r1 += a(off + i + 1);
+      r2 += a(off + i + 2);
+      r3 += a(off + i + 3);
+      r4 += a(off + i + 4);
+      r5 += a(off + i + 5);
+      r6 += a(off + i + 6);
+      r7 += a(off + i + 7);
+    }
+    double res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+    for (; i < n; i++) res += a(off + i);
+    return res;
+  } else {
+    long long n2 = n / 2;
+    n2 -= n2 % 8;
+    double left = pairwise_seq(a, off, n2);
+    return left + pairwise_seq(a, off + n2, n - n2);
+  }
+}
+
+// Perfect-binary-tree sum of vals[0 .. 2^L) by one CTA (blockDim.x = 256).
+// Returns the result in thread 0.
+__device__ __forceinline__ double tree_reduce_block(const double* vals, int L, double* smem /*256*/) {
+  long long m = 1LL << L;
+  int t = threadIdx.x;
+  int nt = blockDim.x;  // power of two
+  double v = 0.0;
+  if (m >= nt) {
+    // each thread reduces a perfect subtree of m/nt consecutive leaves with a
+    // binary-counter stack (equal-height partials combine left + right)
+    long long chunk = m / nt;
+    double stk[40];
+    int hgt[40];
+    int sp = 0;
+    for (long long i = 0; i < chunk; i++) {
+      double x = vals[(long long)t * chunk + i];
+      int hh = 0;
+      while (sp > 0 && hgt[sp - 1] == hh) {
+        x = stk[sp - 1] + x;
+        sp--;
+        hh++;
+      }
+      stk[sp] = x;
+      hgt[sp] = hh;
+      sp++;
+    }
+    v = stk[0];
+    smem[t] = v;
+    __syncthreads();
+    for (int s = 1; s < nt; s <<= 1) {
+      if ((t % (2 * s)) == 0) smem[t] = smem[t] + smem[t + s];
+      __syncthreads();
+    }
+  } else {
+    if (t < m) smem[t] = vals[t];
+    __syncthreads();
+    for (long long s = 1; s < m; s <<= 1) {
+      if (t < m && (t % (2 * s)) == 0) smem[t] = smem[t] + smem[t + s];
+      __syncthreads();
+    }
+  }
+  return smem[0];
+}
+
+}  // namespace hdll

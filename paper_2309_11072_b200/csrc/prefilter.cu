@@ -1,0 +1,74 @@
+// prefilter.cu -- Gaussian prefilter S -> S* (estimator.py:130-142).
+//
+// scipy.ndimage.correlate1d with a symmetric odd kernel and mode="reflect",
+// axis 0 then axis 1 (scipy/ndimage/src/ni_filters.c NI_Correlate1D,
+// symmetric branch):
+//   out[i] = x[i] * w[r];  for jj = -r .. -1: out[i] += (x[i+jj] + x[i-jj]) * w[r+jj]
+// reflect index: m = i mod 2n; m >= n -> 2n - 1 - m (lines shorter than r
+// reflect repeatedly).  Verified in oracle/hdll_oracle.c ho_prefilter.
+//
+// Two passes: vertical (u8 S -> f64 scratch, coalesced along x) and horizontal
+// (f64 scratch -> f64 S*, the row staged in shared memory with its reflected
+// halo).  Taps come from the host (numpy gaussian_kernel) via d.taps.
+#include "encoder.cuh"
+
+namespace hdll {
+
+__device__ __forceinline__ int reflect_idx(long long i, long long n) {
+  long long m = i % (2 * n);
+  if (m < 0) m += 2 * n;
+  if (m >= n) m = 2 * n - 1 - m;
+  return (int)m;
+}
+
+// grid: (ceil(w/128), h, nimg*3) ; one thread per output pixel
+__global__ void __launch_bounds__(128) k_prefilter_v(const ImgDesc* __restrict__ descs) {
+  const ImgDesc& d = descs[blockIdx.z / 3];
+  const int c = blockIdx.z % 3;
+  if (!d.slrme || d.sigma_milli == 0) return;
+  const int y = blockIdx.y, x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (y >= d.h || x >= d.w) return;
+  const uint8_t* S = d.s_planes + (long long)c * d.n;
+  const int r = d.radius;
+  const double* fw = d.taps + r;
+  double o = (double)S[(long long)y * d.w + x] * fw[0];
+  for (int jj = -r; jj < 0; jj++) {
+    double lo = S[(long long)reflect_idx(y + jj, d.h) * d.w + x];
+    double hi = S[(long long)reflect_idx(y - jj, d.h) * d.w + x];
+    o += (lo + hi) * fw[jj];
+  }
+  d.sstar_tmp[(long long)c * d.n + (long long)y * d.w + x] = o;
+}
+
+// grid: (ceil(w/256), h, nimg*3); the row segment plus reflected halo in smem
+__global__ void __launch_bounds__(256) k_prefilter_h(const ImgDesc* __restrict__ descs) {
+  const ImgDesc& d = descs[blockIdx.z / 3];
+  const int c = blockIdx.z % 3;
+  if (!d.slrme || d.sigma_milli == 0) return;
+  const int y = blockIdx.y;
+  if (y >= d.h) return;
+  const int x0 = blockIdx.x * blockDim.x;
+  if (x0 >= d.w) return;
+  const int r = d.radius;
+  const double* fw = d.taps + r;
+  const double* row = d.sstar_tmp + (long long)c * d.n + (long long)y * d.w;
+  extern __shared__ double seg[];  // blockDim.x + 2r values: logical x in [x0 - r, x0 + blockDim.x + r)
+  const int span = blockDim.x + 2 * r;
+  for (int i = threadIdx.x; i < span; i += blockDim.x) seg[i] = row[reflect_idx((long long)x0 - r + i, d.w)];
+  __syncthreads();
+  const int x = x0 + threadIdx.x;
+  if (x >= d.w) return;
+  const double* s = seg + r + threadIdx.x;
+  double o = s[0] * fw[0];
+  for (int jj = -r; jj < 0; jj++) o += (s[jj] + s[-jj]) * fw[jj];
+  d.sstar[(long long)c * d.n + (long long)y * d.w + x] = o;
+}
+
+void launch_prefilter(const ImgDesc* d_descs, int nimg, int max_w, int max_h, int max_radius, cudaStream_t st) {
+  k_prefilter_v<<<dim3((max_w + 127) / 128, max_h, nimg * 3), 128, 0, st>>>(d_descs);
+  size_t smem = sizeof(double) * (256 + 2 * (size_t)max_radius);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_prefilter_h, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_prefilter_h<<<dim3((max_w + 255) / 256, max_h, nimg * 3), 256, smem, st>>>(d_descs);
+}
+
+}  // namespace hdll
