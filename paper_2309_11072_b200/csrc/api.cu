@@ -212,7 +212,7 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
 
   // --- build descriptors and the host staging block (qt, taps, header bytes) ---
   std::vector<ImgDesc> ds(n);
-  size_t stage_bytes = 0;
+  size_t stage_bytes = (size_t)n * 4 * kAlign;  // per-image alignment padding of the 4 staged blocks
   for (int i = 0; i < n; i++)
     stage_bytes += 128 * 8 + 8 * (2 * (size_t)std::max(0, imgs[i].params.radius) + 1) + imgs[i].hdr_pre_len +
                    imgs[i].hdr_post_len;
@@ -244,7 +244,7 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   }
   tile_base[nchains] = ntiles;
   size_t tab_bytes = align_up(sizeof(ImgDesc) * n) + align_up(8 * (nchains + 1)) + 2 * align_up(4 * nchains) +
-                     align_up(8 * nchains) * 3 + align_up(4 * n) + 256;
+                     align_up(8 * nchains) * 3 + align_up(4 * n) + 16 * kAlign;
   // the previous batch may still read the pinned staging / tables
   if (c->done_ev) CK(cudaEventSynchronize(c->done_ev));
   if (ensure(&c->pinned, &c->pinned_cap, stage_bytes + tab_bytes + 4096, false)) return HDLL_B200_E_CUDA;
@@ -254,7 +254,7 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   size_t so = 0;
   auto stage = [&](const void* src, size_t bytes) {
     size_t r = so;
-    if (bytes) memcpy(H + so, src, bytes);
+    if (bytes && src) memcpy(H + so, src, bytes);
     so = align_up(so + bytes);
     return r;
   };

@@ -58,7 +58,8 @@ __global__ void __launch_bounds__(256) k_crc_chunks(const ImgDesc* __restrict__ 
   } else {
     const uint8_t* src = job == 1 ? d.e_plane : d.res_planes + (long long)(job - 2) * d.n;
     long long i = b0;
-    // planes are allocated 16-byte aligned and chunks are 1 KiB aligned: word loop
+    // planes c > 0 start at c * n, which need not be word aligned
+    for (; i < b1 && (reinterpret_cast<uintptr_t>(src + i) & 3); i++) c = tab[0][(c ^ src[i]) & 0xFF] ^ (c >> 8);
     for (; i + 4 <= b1; i += 4) {
       uint32_t w = *reinterpret_cast<const uint32_t*>(src + i) ^ c;
       c = tab[3][w & 0xFF] ^ tab[2][(w >> 8) & 0xFF] ^ tab[1][(w >> 16) & 0xFF] ^ tab[0][w >> 24];
