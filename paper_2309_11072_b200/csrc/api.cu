@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <vector>
 
 #include "../../include/hdll_b200.h"
@@ -66,6 +67,8 @@ struct ImgLayout {
 // stage boundaries recorded with CUDA events (hdll_b200_stage_times)
 enum { kStTonemap, kStBase, kStPrefilter, kStFit, kStEstimate, kStCrc, kStEntropy, kStAssemble, kStages };
 
+constexpr size_t kEstatPerTile = 16 + 16 * kMaxCtx + sizeof(AMap) * kMaxCtx + 4 * kMaxCtx + 16 + 8;
+
 constexpr size_t kZeroBytes = 8 /*maxlw*/ + 8 /*status*/ + 1024 /*bin_count*/ + 8 * 768 /*sum_y*/;
 
 struct Ctx {
@@ -76,12 +79,15 @@ struct Ctx {
   void* estat = nullptr;
   long long estat_tiles = 0;
   int epoch = 0;
-  // small per-batch device tables
-  void* tabs = nullptr;
-  size_t tabs_cap = 0;
-  // pinned host staging for uploads
-  void* pinned = nullptr;
-  size_t pinned_cap = 0;
+  // small per-batch device tables and their pinned host staging, double-buffered
+  // so the host prepares batch k+1 while batch k runs
+  void* tabs_slot[2] = {nullptr, nullptr};
+  size_t tabs_cap_slot[2] = {0, 0};
+  void* pinned_slot[2] = {nullptr, nullptr};
+  size_t pinned_cap_slot[2] = {0, 0};
+  cudaEvent_t slot_ev[2] = {nullptr, nullptr};
+  int slot = 0;
+  void* tabs = nullptr;  // slot of the last batch
   cudaEvent_t done_ev = nullptr;
   cudaEvent_t stage_ev[kStages + 1] = {};
   bool stage_valid[kStages] = {};
@@ -243,14 +249,52 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
     }
   }
   tile_base[nchains] = ntiles;
+  // round-robin ticket schedule: chains sorted longest first; segment k spans the
+  // rounds in which exactly seg_active[k] chains still have tiles
+  std::vector<int> rr_chain;
+  for (int ch = 0; ch < nchains; ch++)
+    if (tile_base[ch + 1] > tile_base[ch]) rr_chain.push_back(ch);
+  std::stable_sort(rr_chain.begin(), rr_chain.end(), [&](int a, int b) {
+    return tile_base[a + 1] - tile_base[a] > tile_base[b + 1] - tile_base[b];
+  });
+  std::vector<long long> seg_r0, seg_t0;
+  std::vector<int> seg_active;
+  {
+    long long r = 0, t = 0;
+    int act = (int)rr_chain.size();
+    while (act > 0) {
+      long long len_last = tile_base[rr_chain[act - 1] + 1] - tile_base[rr_chain[act - 1]];
+      if (len_last > r) {
+        seg_r0.push_back(r);
+        seg_t0.push_back(t);
+        seg_active.push_back(act);
+        t += (len_last - r) * act;
+        r = len_last;
+      }
+      act--;
+    }
+    if (seg_r0.empty()) {
+      seg_r0.push_back(0);
+      seg_t0.push_back(0);
+      seg_active.push_back(1);
+    }
+    if (rr_chain.empty()) rr_chain.push_back(0);
+  }
   size_t tab_bytes = align_up(sizeof(ImgDesc) * n) + align_up(8 * (nchains + 1)) + 2 * align_up(4 * nchains) +
-                     align_up(8 * nchains) * 3 + align_up(4 * n) + 16 * kAlign;
-  // the previous batch may still read the pinned staging / tables
-  if (c->done_ev) CK(cudaEventSynchronize(c->done_ev));
-  if (ensure(&c->pinned, &c->pinned_cap, stage_bytes + tab_bytes + 4096, false)) return HDLL_B200_E_CUDA;
-  if (ensure(&c->tabs, &c->tabs_cap, stage_bytes + tab_bytes + 4096, true)) return HDLL_B200_E_CUDA;
-  uint8_t* H = (uint8_t*)c->pinned;
-  uint8_t* D = (uint8_t*)c->tabs;
+                     align_up(8 * nchains) * 3 + align_up(4 * n) + 3 * align_up(8 * (nchains + 2)) +
+                     align_up(4 * (nchains + 2)) + 16 * kAlign;
+  // the batch that last used this staging slot may still read it
+  const int slot = c->slot;
+  c->slot ^= 1;
+  if (c->slot_ev[slot]) CK(cudaEventSynchronize(c->slot_ev[slot]));
+  else CK(cudaEventCreateWithFlags(&c->slot_ev[slot], cudaEventDisableTiming));
+  if (ensure(&c->pinned_slot[slot], &c->pinned_cap_slot[slot], stage_bytes + tab_bytes + 4096, false))
+    return HDLL_B200_E_CUDA;
+  if (ensure(&c->tabs_slot[slot], &c->tabs_cap_slot[slot], stage_bytes + tab_bytes + 4096, true))
+    return HDLL_B200_E_CUDA;
+  c->tabs = c->tabs_slot[slot];
+  uint8_t* H = (uint8_t*)c->pinned_slot[slot];
+  uint8_t* D = (uint8_t*)c->tabs_slot[slot];
   size_t so = 0;
   auto stage = [&](const void* src, size_t bytes) {
     size_t r = so;
@@ -267,6 +311,10 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   const size_t t_bits = stage(nullptr, 8 * nchains);
   const size_t t_chain0 = stage(img_chain0.data(), 4 * n);
   const size_t t_ticket = stage(nullptr, 16);
+  const size_t t_seg_r0 = stage(seg_r0.data(), 8 * seg_r0.size());
+  const size_t t_seg_t0 = stage(seg_t0.data(), 8 * seg_t0.size());
+  const size_t t_seg_active = stage(seg_active.data(), 4 * seg_active.size());
+  const size_t t_rr_chain = stage(rr_chain.data(), 4 * rr_chain.size());
 
   long long max_n = 0, max_sort_tiles = 0, max_nodes = 0, max_out = 0;
   int max_w = 0, max_h = 0, max_radius = 0, max_level = 0, max_base_tiles = 0;
@@ -377,7 +425,7 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   if (ntiles > c->estat_tiles) {
     if (c->estat) cudaFree(c->estat);
     long long cap = ntiles + ntiles / 4 + 1024;
-    size_t bytes = (size_t)cap * (16 + 16 * kMaxCtx + sizeof(AMap) * kMaxCtx + 4 * kMaxCtx + 16);
+    size_t bytes = (size_t)cap * kEstatPerTile;
     CK(cudaMalloc(&c->estat, bytes));
     CK(cudaMemset(c->estat, 0, bytes));
     c->estat_tiles = cap;
@@ -385,7 +433,7 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   }
   c->epoch++;
   if (c->epoch >= (1 << 28)) {  // epoch wrap: re-zero
-    size_t bytes = (size_t)c->estat_tiles * (16 + 16 * kMaxCtx + sizeof(AMap) * kMaxCtx + 4 * kMaxCtx + 16);
+    size_t bytes = (size_t)c->estat_tiles * kEstatPerTile;
     CK(cudaMemsetAsync(c->estat, 0, bytes, st));
     c->epoch = 1;
   }
@@ -404,6 +452,12 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   ct.maps = (AMap*)(E + cap_t * (16 + 16 * kMaxCtx));
   ct.states = (int*)(E + cap_t * (16 + 16 * kMaxCtx + sizeof(AMap) * kMaxCtx));
   ct.bitv = (unsigned long long*)(E + cap_t * (16 + 16 * kMaxCtx + sizeof(AMap) * kMaxCtx + 4 * kMaxCtx));
+  ct.edge = (uint32_t*)(E + cap_t * (16 + 16 * kMaxCtx + sizeof(AMap) * kMaxCtx + 4 * kMaxCtx + 16));
+  ct.nseg = (int)seg_r0.size();
+  ct.seg_r0 = (const long long*)(D + t_seg_r0);
+  ct.seg_t0 = (const long long*)(D + t_seg_t0);
+  ct.seg_active = (const int*)(D + t_seg_active);
+  ct.rr_chain = (const int*)(D + t_rr_chain);
   ct.ticket = (int*)(D + t_ticket);
   ct.ntiles = ntiles;
   ct.epoch = c->epoch;
@@ -447,7 +501,8 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   mark(kStCrc);
   if (ntiles > 0) {
     launch_entropy(dd, ct, st);
-    c->launches += 1;
+    launch_entropy_fixup(ct, st);
+    c->launches += 2;
   }
   mark(kStEntropy);
   if (mode == 0) {
@@ -462,6 +517,7 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   CK(cudaGetLastError());
   if (!c->done_ev) CK(cudaEventCreateWithFlags(&c->done_ev, cudaEventDisableTiming));
   CK(cudaEventRecord(c->done_ev, st));
+  CK(cudaEventRecord(c->slot_ev[slot], st));
   c->last_stream = st;
   c->descs = ds;
   c->lays = lays;
@@ -505,8 +561,11 @@ void hdll_b200_ctx_destroy(hdll_b200_ctx* ctx) {
   if (c->last_stream) cudaStreamSynchronize(c->last_stream);
   if (c->arena) cudaFree(c->arena);
   if (c->estat) cudaFree(c->estat);
-  if (c->tabs) cudaFree(c->tabs);
-  if (c->pinned) cudaFreeHost(c->pinned);
+  for (int k = 0; k < 2; k++) {
+    if (c->tabs_slot[k]) cudaFree(c->tabs_slot[k]);
+    if (c->pinned_slot[k]) cudaFreeHost(c->pinned_slot[k]);
+    if (c->slot_ev[k]) cudaEventDestroy(c->slot_ev[k]);
+  }
   if (c->h2d) cudaFreeHost(c->h2d);
   if (c->d_out) cudaFree(c->d_out);
   if (c->d_len) cudaFree(c->d_len);

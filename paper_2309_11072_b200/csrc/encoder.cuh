@@ -123,10 +123,18 @@ struct ChainTab {
   long long* cnt;              // [ntiles][2][kMaxCtx]: aggregate, inclusive
   AMap* maps;                  // [ntiles][kMaxCtx]: aggregate
   int* states;                 // [ntiles][kMaxCtx]: inclusive A
-  unsigned long long* bitv;    // [ntiles][2]
+  unsigned long long* bitv;    // [ntiles][2]: aggregate bits, inclusive end bit
+  uint32_t* edge;              // [ntiles][2]: head / tail partial words (merged by k_entropy_fixup)
   int* ticket;
   long long ntiles;
   int epoch;
+  // ticket -> (chain, tile) round-robin schedule: rounds [seg_r0[k], seg_r0[k+1]) have
+  // seg_active[k] chains (the first ones of rr_chain, longest first) starting at ticket seg_t0[k]
+  int nseg;
+  const long long* seg_r0;
+  const long long* seg_t0;
+  const int* seg_active;
+  const int* rr_chain;
 };
 
 struct AsmTab {
@@ -144,6 +152,7 @@ void launch_fit(const ImgDesc*, int nimg, int max_sort_tiles, long long max_node
 void launch_estimate(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
 void launch_crc(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
 void launch_entropy(const ImgDesc*, const ChainTab&, cudaStream_t);
+void launch_entropy_fixup(const ChainTab&, cudaStream_t);
 void launch_assemble(const ImgDesc*, int nimg, const AsmTab&, long long max_out, cudaStream_t);
 
 }  // namespace hdll

@@ -19,8 +19,10 @@
 //   2. A-maps per context      -> look-back -> incoming A of the tile (common.cuh AMap)
 //   3. code lengths            -> look-back -> bit offset of the tile in the chain
 //   4. emit MSB-first bits straight into the chain's byte stream; words shared
-//      between lanes are merged through a warp carry, words shared with the
-//      previous tile are OR-ed in after that tile's `done` flag.
+//      between lanes are merged through a warp carry, the (at most two) words
+//      a tile shares with its neighbours are parked and merged by the
+//      k_entropy_fixup launch, so no warp ever waits on another's emission.
+// Tickets are dealt round-robin over chains, so every chain advances at once.
 // Flags carry the launch epoch, so status memory is never re-zeroed.
 #include "encoder.cuh"
 
@@ -56,32 +58,21 @@ struct WordSink {
   long long cap_words;
   long long tile_first_word;
   bool tile_start_partial;
-  const ChainTab* ct;
-  long long g_prev;  // previous tile of the chain (-1 if none)
+  uint32_t* edge;  // this tile's [head, tail] slots
   unsigned* status;
 
+  // complete words owned by this tile; the word it shares with the previous
+  // tile (its first word when it starts mid-word) is parked in edge[0]
   __device__ void write(long long idx, uint32_t w) const {
+    if (idx == tile_first_word && tile_start_partial) {
+      edge[0] = w;
+      return;
+    }
     if (idx >= cap_words) {
       atomicOr(status, kErrCapacity);
       return;
     }
-    uint32_t m = __byte_perm(w, 0, 0x0123);  // MSB-first word -> stream byte order
-    if (idx == tile_first_word && tile_start_partial) {
-      if (g_prev >= 0) {
-        const int* f = ct->flags + g_prev * 4 + 3;
-        for (long long it = 0;; it++) {
-          if (ld_acquire(f) == ct->epoch) break;
-          if (it > kSpinLimit) {
-            atomicOr(status, kErrLookback);
-            break;
-          }
-          __nanosleep(32);
-        }
-      }
-      atomicOr(words + idx, m);
-    } else {
-      words[idx] = m;
-    }
+    words[idx] = __byte_perm(w, 0, 0x0123);  // MSB-first word -> stream byte order
   }
 };
 
@@ -251,6 +242,7 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
   if (lane == 0) {
     unsigned long long* bv = ct.bitv + g * 2;
     if (chain_start) {
+      bv[0] = (unsigned long long)tbits;
       bv[1] = (unsigned long long)tbits;
       publish(ct, g, 2, 2);
     } else {
@@ -282,8 +274,7 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
   sink.cap_words = ct.cap[chain] / 4;
   sink.tile_first_word = toff >> 5;
   sink.tile_start_partial = (toff & 31) != 0;
-  sink.ct = &ct;
-  sink.g_prev = chain_start ? -1 : g - 1;
+  sink.edge = ct.edge + g * 2;
   sink.status = status;
   const long long s_l = toff + loff, e_l = s_l + nbits;
   LaneBits lb;
@@ -336,10 +327,11 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
     cw = __shfl_sync(0xffffffffu, ncw, l);
     cb = __shfl_sync(0xffffffffu, ncb, l);
   }
-  if (lane == 0 && cw >= 0) sink.write(cw, cb);
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) st_release(ct.flags + g * 4 + 3, ct.epoch);
+  // the tile's last partial word: parked for the fix-up pass (a later tile may add bits)
+  if (lane == 0 && cw >= 0) {
+    if (cw == sink.tile_first_word && sink.tile_start_partial) sink.edge[0] = cb;
+    else sink.edge[1] = cb;
+  }
   (void)e_l;
 }
 
@@ -473,7 +465,7 @@ struct DctBlock {
 // ---------------------------------------------------------------------------
 // Kernels: a warp takes the next ticket = next global tile.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int find_chain(const ChainTab& ct, long long g) {
+__device__ __forceinline__ int find_chain(const ChainTab& ct, long long g) {  // chain of global tile g
   int lo = 0, hi = ct.nchains;
   while (hi - lo > 1) {
     int mid = (lo + hi) >> 1;
@@ -485,12 +477,18 @@ __device__ __forceinline__ int find_chain(const ChainTab& ct, long long g) {
 __global__ void __launch_bounds__(128) k_entropy(const ImgDesc* __restrict__ descs, ChainTab ct) {
   const int lane = threadIdx.x & 31;
   for (;;) {
-    long long g = 0;
-    if (lane == 0) g = atomicAdd(ct.ticket, 1);
-    g = __shfl_sync(0xffffffffu, g, 0);
-    if (g >= ct.ntiles) return;
-    const int chain = find_chain(ct, g);
-    const long long tin = g - ct.tile_base[chain];
+    long long t = 0;
+    if (lane == 0) t = atomicAdd(ct.ticket, 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= ct.ntiles) return;
+    // round-robin over chains: all chains advance together, every wait is on an older ticket
+    int k = 0;
+    while (k + 1 < ct.nseg && ct.seg_t0[k + 1] <= t) k++;
+    const long long rel = t - ct.seg_t0[k];
+    const int act = ct.seg_active[k];
+    const long long tin = ct.seg_r0[k] + rel / act;
+    const int chain = ct.rr_chain[rel % act];
+    const long long g = ct.tile_base[chain] + tin;
     const ImgDesc& d = descs[ct.img[chain]];
     const int kind = ct.kind[chain];
     if (kind == 0) {
@@ -555,6 +553,35 @@ __global__ void __launch_bounds__(128) k_entropy(const ImgDesc* __restrict__ des
       run_tile<5>(ct, chain, tin, g, pr, d.status);
     }
   }
+}
+
+// Merge the words shared between tiles.  Word w belongs to the tile holding
+// its first bit; that tile's tail plus the heads of the following tiles that
+// start inside w (several, if tiles are tiny) are OR-ed and stored once.
+__global__ void __launch_bounds__(256) k_entropy_fixup(ChainTab ct) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= ct.ntiles) return;
+  const int chain = find_chain(ct, g);
+  const long long gend = ct.tile_base[chain + 1];
+  const long long e = (long long)ct.bitv[g * 2 + 1];
+  const long long s = e - (long long)ct.bitv[g * 2 + 0];
+  if (e == s || (e & 31) == 0) return;
+  const long long w = (e - 1) >> 5;
+  if ((s >> 5) == w && (s & 31) != 0) return;  // starts inside w: not the owner
+  uint32_t v = ct.edge[g * 2 + 1];
+  for (long long j = g + 1; j < gend; j++) {
+    const long long ej = (long long)ct.bitv[j * 2 + 1];
+    const long long sj = ej - (long long)ct.bitv[j * 2 + 0];
+    if (sj >= ((w + 1) << 5)) break;
+    if (ej > sj) v |= ct.edge[j * 2 + 0];
+    if (ej >= ((w + 1) << 5)) break;
+  }
+  uint32_t* words = reinterpret_cast<uint32_t*>(ct.out[chain]);
+  if (w < ct.cap[chain] / 4) words[w] = __byte_perm(v, 0, 0x0123);
+}
+
+void launch_entropy_fixup(const ChainTab& ct, cudaStream_t st) {
+  k_entropy_fixup<<<(unsigned)((ct.ntiles + 255) / 256), 256, 0, st>>>(ct);
 }
 
 void launch_entropy(const ImgDesc* d_descs, const ChainTab& ct, cudaStream_t st) {
