@@ -94,7 +94,7 @@ struct Ctx {
   cudaStream_t last_stream = nullptr;
   int launches = 0;
   int last_status = 0;
-  size_t bits_off = 0;  // device offset (in tabs) of the chain bit totals of the last batch
+  size_t bits_off_dct = 0, bits_off_pln = 0;  // device offsets (in tabs) of the chain bit totals
   // last batch (for traces / status)
   std::vector<ImgDesc> descs;
   std::vector<ImgLayout> lays;
@@ -190,6 +190,110 @@ int map_status(unsigned bits) {
   return HDLL_B200_OK;
 }
 
+// Host side of a ChainTab: chains, their tiles and the round-robin ticket schedule.
+struct HostChains {
+  std::vector<long long> tile_base{0};
+  std::vector<int> img, kind;
+  std::vector<uint8_t*> out;
+  std::vector<long long> cap;
+  std::vector<int> rr_chain;
+  std::vector<long long> seg_r0, seg_t0;
+  std::vector<int> seg_active;
+
+  void add(int i, int k, long long tiles, uint8_t* o, long long c) {
+    img.push_back(i);
+    kind.push_back(k);
+    out.push_back(o);
+    cap.push_back(c);
+    tile_base.push_back(tile_base.back() + tiles);
+  }
+  int nchains() const { return (int)img.size(); }
+  long long ntiles() const { return tile_base.back(); }
+  long long len(int ch) const { return tile_base[ch + 1] - tile_base[ch]; }
+  // chains sorted longest first; segment k spans the rounds in which exactly
+  // seg_active[k] chains still have tiles; ticket t of a segment is chain
+  // rr_chain[(t - t0) % active], tile r0 + (t - t0) / active
+  void schedule() {
+    for (int ch = 0; ch < nchains(); ch++)
+      if (len(ch) > 0) rr_chain.push_back(ch);
+    std::stable_sort(rr_chain.begin(), rr_chain.end(), [&](int a, int b) { return len(a) > len(b); });
+    long long r = 0, t = 0;
+    for (int act = (int)rr_chain.size(); act > 0; act--) {
+      long long l = len(rr_chain[act - 1]);
+      if (l > r) {
+        seg_r0.push_back(r);
+        seg_t0.push_back(t);
+        seg_active.push_back(act);
+        t += (l - r) * act;
+        r = l;
+      }
+    }
+    if (seg_r0.empty()) {
+      seg_r0.push_back(0);
+      seg_t0.push_back(0);
+      seg_active.push_back(1);
+    }
+    if (rr_chain.empty()) rr_chain.push_back(0);
+    if (img.empty()) add(0, 0, 0, nullptr, 0);  // keep device arrays non-empty
+  }
+  size_t staged_bytes() const {
+    size_t nc = img.size() + 2;
+    return 10 * kAlign + 8 * (nc + 1) + 4 * nc * 2 + 8 * nc * 3 + 8 * 2 * seg_r0.size() + 4 * seg_active.size() +
+           4 * rr_chain.size();
+  }
+  struct Staged {
+    size_t tile_base, img, kind, out, cap, bits, seg_r0, seg_t0, seg_active, rr_chain;
+  };
+  template <class F>
+  Staged stage(F& st) const {
+    Staged s;
+    s.tile_base = st(tile_base.data(), 8 * tile_base.size());
+    s.img = st(img.data(), 4 * img.size());
+    s.kind = st(kind.data(), 4 * kind.size());
+    s.out = st(out.data(), 8 * out.size());
+    s.cap = st(cap.data(), 8 * cap.size());
+    s.bits = st(nullptr, 8 * img.size());
+    s.seg_r0 = st(seg_r0.data(), 8 * seg_r0.size());
+    s.seg_t0 = st(seg_t0.data(), 8 * seg_t0.size());
+    s.seg_active = st(seg_active.data(), 4 * seg_active.size());
+    s.rr_chain = st(rr_chain.data(), 4 * rr_chain.size());
+    return s;
+  }
+  // status arrays live in the shared entropy arena at tile offset `t0`
+  ChainTab table(const Staged& s, uint8_t* D, uint8_t* E, long long cap_t, long long t0, int* ticket,
+                 int epoch) const {
+    ChainTab ct;
+    ct.nchains = nchains();
+    ct.tile_base = (const long long*)(D + s.tile_base);
+    ct.img = (const int*)(D + s.img);
+    ct.kind = (const int*)(D + s.kind);
+    ct.out = (uint8_t* const*)(D + s.out);
+    ct.cap = (const long long*)(D + s.cap);
+    ct.bits = (unsigned long long*)(D + s.bits);
+    size_t o = 0;
+    ct.flags = (int*)(E + o) + t0 * 4;
+    o += cap_t * 16;
+    ct.cnt = (long long*)(E + o) + t0 * 2 * kMaxCtx;
+    o += cap_t * 16 * kMaxCtx;
+    ct.maps = (AMap*)(E + o) + t0 * kMaxCtx;
+    o += cap_t * sizeof(AMap) * kMaxCtx;
+    ct.states = (int*)(E + o) + t0 * kMaxCtx;
+    o += cap_t * 4 * kMaxCtx;
+    ct.bitv = (unsigned long long*)(E + o) + t0 * 2;
+    o += cap_t * 16;
+    ct.edge = (uint32_t*)(E + o) + t0 * 2;
+    ct.ticket = ticket;
+    ct.ntiles = ntiles();
+    ct.epoch = epoch;
+    ct.nseg = (int)seg_r0.size();
+    ct.seg_r0 = (const long long*)(D + s.seg_r0);
+    ct.seg_t0 = (const long long*)(D + s.seg_t0);
+    ct.seg_active = (const int*)(D + s.seg_active);
+    ct.rr_chain = (const int*)(D + s.rr_chain);
+    return ct;
+  }
+};
+
 // mode: 0 full encode, 1 lossless plane (rgbe -> plane bytes), 2 lossy image (rgbe -> sdr rgb)
 int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out, const uint64_t* out_cap,
               uint64_t* d_out_len, cudaStream_t st, int mode) {
@@ -222,67 +326,22 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   for (int i = 0; i < n; i++)
     stage_bytes += 128 * 8 + 8 * (2 * (size_t)std::max(0, imgs[i].params.radius) + 1) + imgs[i].hdr_pre_len +
                    imgs[i].hdr_post_len;
-  // chain table sizes
-  const int chains_per_img = 5;
-  const int nchains = n * chains_per_img;
-  long long ntiles = 0;
-  std::vector<long long> tile_base(nchains + 1);
-  std::vector<int> ch_img(nchains), ch_kind(nchains);
-  std::vector<uint8_t*> ch_out(nchains);
-  std::vector<long long> ch_cap(nchains);
-  std::vector<int> img_chain0(n);
+  // sequential-coder chains: the DCT stream of every image (kind 0) and its 4
+  // plane streams (kinds 1..4), each family driven by its own kernel
+  HostChains hc_dct, hc_pln;
   for (int i = 0; i < n; i++) {
     const long long w = imgs[i].width, h = imgs[i].height;
     const long long nb = ((w + 7) / 8) * ((h + 7) / 8);
-    img_chain0[i] = i * chains_per_img;
-    for (int k = 0; k < chains_per_img; k++) {
-      int ch = i * chains_per_img + k;
-      long long tiles = 0;
+    for (int k = 0; k < 5; k++) {
       bool active = (mode == 0) || (mode == 1 && k == 1) || (mode == 2 && k == 0);
-      if (active) tiles = (k == 0) ? 3 * ((nb + 31) / 32) : h;
-      tile_base[ch] = ntiles;
-      ntiles += tiles;
-      ch_img[ch] = i;
-      ch_kind[ch] = k;
-      ch_out[ch] = A + base[i] + lays[i].off_chain[k];
-      ch_cap[ch] = lays[i].chain_cap[k];
+      long long tiles = active ? ((k == 0) ? 3 * ((nb + 31) / 32) : h) : 0;
+      (k == 0 ? hc_dct : hc_pln).add(i, k, tiles, A + base[i] + lays[i].off_chain[k], lays[i].chain_cap[k]);
     }
   }
-  tile_base[nchains] = ntiles;
-  // round-robin ticket schedule: chains sorted longest first; segment k spans the
-  // rounds in which exactly seg_active[k] chains still have tiles
-  std::vector<int> rr_chain;
-  for (int ch = 0; ch < nchains; ch++)
-    if (tile_base[ch + 1] > tile_base[ch]) rr_chain.push_back(ch);
-  std::stable_sort(rr_chain.begin(), rr_chain.end(), [&](int a, int b) {
-    return tile_base[a + 1] - tile_base[a] > tile_base[b + 1] - tile_base[b];
-  });
-  std::vector<long long> seg_r0, seg_t0;
-  std::vector<int> seg_active;
-  {
-    long long r = 0, t = 0;
-    int act = (int)rr_chain.size();
-    while (act > 0) {
-      long long len_last = tile_base[rr_chain[act - 1] + 1] - tile_base[rr_chain[act - 1]];
-      if (len_last > r) {
-        seg_r0.push_back(r);
-        seg_t0.push_back(t);
-        seg_active.push_back(act);
-        t += (len_last - r) * act;
-        r = len_last;
-      }
-      act--;
-    }
-    if (seg_r0.empty()) {
-      seg_r0.push_back(0);
-      seg_t0.push_back(0);
-      seg_active.push_back(1);
-    }
-    if (rr_chain.empty()) rr_chain.push_back(0);
-  }
-  size_t tab_bytes = align_up(sizeof(ImgDesc) * n) + align_up(8 * (nchains + 1)) + 2 * align_up(4 * nchains) +
-                     align_up(8 * nchains) * 3 + align_up(4 * n) + 3 * align_up(8 * (nchains + 2)) +
-                     align_up(4 * (nchains + 2)) + 16 * kAlign;
+  hc_dct.schedule();
+  hc_pln.schedule();
+  const long long ntiles = hc_dct.ntiles() + hc_pln.ntiles();
+  size_t tab_bytes = align_up(sizeof(ImgDesc) * n) + hc_dct.staged_bytes() + hc_pln.staged_bytes() + 16 * kAlign;
   // the batch that last used this staging slot may still read it
   const int slot = c->slot;
   c->slot ^= 1;
@@ -303,18 +362,8 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
     return r;
   };
   const size_t t_descs = stage(nullptr, sizeof(ImgDesc) * n);
-  const size_t t_tile_base = stage(tile_base.data(), 8 * (nchains + 1));
-  const size_t t_img = stage(ch_img.data(), 4 * nchains);
-  const size_t t_kind = stage(ch_kind.data(), 4 * nchains);
-  const size_t t_out = stage(ch_out.data(), 8 * nchains);
-  const size_t t_cap = stage(ch_cap.data(), 8 * nchains);
-  const size_t t_bits = stage(nullptr, 8 * nchains);
-  const size_t t_chain0 = stage(img_chain0.data(), 4 * n);
+  const HostChains::Staged sc_dct = hc_dct.stage(stage), sc_pln = hc_pln.stage(stage);
   const size_t t_ticket = stage(nullptr, 16);
-  const size_t t_seg_r0 = stage(seg_r0.data(), 8 * seg_r0.size());
-  const size_t t_seg_t0 = stage(seg_t0.data(), 8 * seg_t0.size());
-  const size_t t_seg_active = stage(seg_active.data(), 4 * seg_active.size());
-  const size_t t_rr_chain = stage(rr_chain.data(), 4 * rr_chain.size());
 
   long long max_n = 0, max_sort_tiles = 0, max_nodes = 0, max_out = 0;
   int max_w = 0, max_h = 0, max_radius = 0, max_level = 0, max_base_tiles = 0;
@@ -439,28 +488,8 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   }
   uint8_t* E = (uint8_t*)c->estat;
   const long long cap_t = c->estat_tiles;
-  ChainTab ct;
-  ct.nchains = nchains;
-  ct.tile_base = (const long long*)(D + t_tile_base);
-  ct.img = (const int*)(D + t_img);
-  ct.kind = (const int*)(D + t_kind);
-  ct.out = (uint8_t* const*)(D + t_out);
-  ct.cap = (const long long*)(D + t_cap);
-  ct.bits = (unsigned long long*)(D + t_bits);
-  ct.flags = (int*)E;
-  ct.cnt = (long long*)(E + cap_t * 16);
-  ct.maps = (AMap*)(E + cap_t * (16 + 16 * kMaxCtx));
-  ct.states = (int*)(E + cap_t * (16 + 16 * kMaxCtx + sizeof(AMap) * kMaxCtx));
-  ct.bitv = (unsigned long long*)(E + cap_t * (16 + 16 * kMaxCtx + sizeof(AMap) * kMaxCtx + 4 * kMaxCtx));
-  ct.edge = (uint32_t*)(E + cap_t * (16 + 16 * kMaxCtx + sizeof(AMap) * kMaxCtx + 4 * kMaxCtx + 16));
-  ct.nseg = (int)seg_r0.size();
-  ct.seg_r0 = (const long long*)(D + t_seg_r0);
-  ct.seg_t0 = (const long long*)(D + t_seg_t0);
-  ct.seg_active = (const int*)(D + t_seg_active);
-  ct.rr_chain = (const int*)(D + t_rr_chain);
-  ct.ticket = (int*)(D + t_ticket);
-  ct.ntiles = ntiles;
-  ct.epoch = c->epoch;
+  ChainTab ct_dct = hc_dct.table(sc_dct, D, E, cap_t, 0, (int*)(D + t_ticket), c->epoch);
+  ChainTab ct_pln = hc_pln.table(sc_pln, D, E, cap_t, hc_dct.ntiles(), (int*)(D + t_ticket) + 2, c->epoch);
 
   // --- stages ---
   if (!c->stage_ev[0])
@@ -499,17 +528,23 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   launch_crc(dd, n, max_n, st);
   c->launches += 2;
   mark(kStCrc);
-  if (ntiles > 0) {
-    launch_entropy(dd, ct, st);
-    launch_entropy_fixup(ct, st);
+  if (ct_dct.ntiles > 0) {
+    launch_entropy_dct(dd, ct_dct, st);
+    launch_entropy_fixup(ct_dct, st);
+    c->launches += 2;
+  }
+  if (ct_pln.ntiles > 0) {
+    launch_entropy_plane(dd, ct_pln, max_w, st);
+    launch_entropy_fixup(ct_pln, st);
     c->launches += 2;
   }
   mark(kStEntropy);
   if (mode == 0) {
     AsmTab at;
-    at.chain_out = ct.out;
-    at.chain_bits = ct.bits;
-    at.img_chain0 = (const int*)(D + t_chain0);
+    at.dct_out = ct_dct.out;
+    at.dct_bits = ct_dct.bits;
+    at.plane_out = ct_pln.out;
+    at.plane_bits = ct_pln.bits;
     launch_assemble(dd, n, at, max_out, st);
     c->launches += 1;
   }
@@ -521,7 +556,8 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   c->last_stream = st;
   c->descs = ds;
   c->lays = lays;
-  c->bits_off = t_bits;
+  c->bits_off_dct = sc_dct.bits;
+  c->bits_off_pln = sc_pln.bits;
   return HDLL_B200_OK;
 }
 
@@ -680,7 +716,9 @@ static int plugin_common(Ctx* c, const uint8_t* h_src, size_t src_bytes, uint32_
   const ImgLayout& L = c->lays[0];
   uint8_t* chain = (uint8_t*)c->arena + L.off_chain[k];
   unsigned long long bits = 0;
-  CK(cudaMemcpy(&bits, (uint8_t*)c->tabs + c->bits_off + 8 * k, 8, cudaMemcpyDeviceToHost));
+  // mode 1: the only plane chain is image 0's E chain (index 1 of 4); mode 2: the DCT chain
+  const size_t boff = mode == 1 ? c->bits_off_pln + 8 * 0 : c->bits_off_dct;
+  CK(cudaMemcpy(&bits, (uint8_t*)c->tabs + boff, 8, cudaMemcpyDeviceToHost));
   const uint64_t nbytes = (bits + 7) / 8;
   *body_len = 8 + nbytes;
   if (8 + nbytes > cap) return HDLL_B200_E_CAPACITY;

@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(256) k_assemble(const ImgDesc* __restrict__ de
   __shared__ uint8_t present[256];
   __shared__ int prefix[257];
   __shared__ uint8_t frame[5][17];
-  const int c0 = at.img_chain0[blockIdx.y];
+  const int img = blockIdx.y;
   if (threadIdx.x < 256) present[threadIdx.x] = (d.slrme && d.bin_count[threadIdx.x] > 0) ? 1 : 0;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(256) k_assemble(const ImgDesc* __restrict__ de
     L.post = o;
     o += d.hdr_post_len;
     for (int k = 0; k < 5; k++) {
-      unsigned long long bits = at.chain_bits[c0 + k];
+      unsigned long long bits = k == 0 ? at.dct_bits[img] : at.plane_bits[img * 4 + k - 1];
       L.body_len[k] = 8 + (long long)((bits + 7) / 8);
       L.pay[k] = o;
       o += 9 + L.body_len[k];
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(256) k_assemble(const ImgDesc* __restrict__ de
       while (i < L.pay[k]) k--;
       long long r = i - L.pay[k];
       if (r < 17) v = frame[k][r];
-      else v = at.chain_out[c0 + k][r - 17];
+      else v = (k == 0 ? at.dct_out[img] : at.plane_out[img * 4 + k - 1])[r - 17];
     }
     d.out[i] = v;
   }

@@ -138,9 +138,10 @@ struct ChainTab {
 };
 
 struct AsmTab {
-  uint8_t* const* chain_out;                 // per chain byte streams
-  const unsigned long long* chain_bits;      // per chain bit totals
-  const int* img_chain0;                     // first chain (the DCT chain) of each image; planes follow
+  uint8_t* const* dct_out;                   // [nimg] base-layer DCT byte streams
+  const unsigned long long* dct_bits;        // [nimg] their bit totals
+  uint8_t* const* plane_out;                 // [nimg*4] E, R, G, B plane byte streams
+  const unsigned long long* plane_bits;      // [nimg*4]
 };
 
 void upload_base_constants();
@@ -151,7 +152,8 @@ void launch_prefilter(const ImgDesc*, int nimg, int max_w, int max_h, int max_ra
 void launch_fit(const ImgDesc*, int nimg, int max_sort_tiles, long long max_nodes, cudaStream_t);
 void launch_estimate(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
 void launch_crc(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
-void launch_entropy(const ImgDesc*, const ChainTab&, cudaStream_t);
+void launch_entropy_dct(const ImgDesc*, const ChainTab&, cudaStream_t);
+void launch_entropy_plane(const ImgDesc*, const ChainTab&, int max_w, cudaStream_t);
 void launch_entropy_fixup(const ChainTab&, cudaStream_t);
 void launch_assemble(const ImgDesc*, int nimg, const AsmTab&, long long max_out, cudaStream_t);
 

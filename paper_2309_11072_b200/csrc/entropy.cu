@@ -2,8 +2,8 @@
 //
 // Reference (sequential, numba):
 //   encode_plane          _kernels.py:169-216  (lossless coder id 1: MED + 5 contexts + runs)
-//   encode_dct_component  _kernels.py:280-324  (base layer symbols, 6 contexts shared by Y/Cb/Cr,
-//                                               codec_core.py:439-450)
+//   encode_dct_component  _kernels.py:280-324  (base layer symbols, 6 contexts; Y uses 0-2,
+//                                               Cb and Cr share 3-5, codec_core.py:439-450)
 //   _rice_put / _select_k / _update_state      _kernels.py:65-128
 //
 // Parallel form.  A *chain* is one sequential coder invocation (one DCT stream
@@ -11,26 +11,63 @@
 // (a plane row, or 32 consecutive DCT blocks of one component), one warp per
 // tile, lane = contiguous slice of the tile.  The symbols of a tile depend
 // only on the data; the coder state carried between tiles is, per context,
-// (count, A).  Each warp, in ONE pass with three chained decoupled look-backs
-// (tiles are taken in order from an atomic ticket so every wait is on an
-// already-running warp):
-//   1. counts per context      -> look-back -> global symbol index of each symbol
-//                                 (halving points and N follow from the index)
-//   2. A-maps per context      -> look-back -> incoming A of the tile (common.cuh AMap)
-//   3. code lengths            -> look-back -> bit offset of the tile in the chain
+// (count, A).  Each warp generates its tile's symbols once into shared memory,
+// then runs three chained decoupled look-backs (tickets are dealt round-robin
+// over the chains in order, so every wait is on an older, running warp):
+//   1. counts per context  -> global symbol index (halving points, N)
+//   2. A-maps per context  -> incoming A of the tile (common.cuh AMap)
+//   3. code lengths        -> bit offset of the tile in its chain
 //   4. emit MSB-first bits straight into the chain's byte stream; words shared
-//      between lanes are merged through a warp carry, the (at most two) words
-//      a tile shares with its neighbours are parked and merged by the
-//      k_entropy_fixup launch, so no warp ever waits on another's emission.
-// Tickets are dealt round-robin over chains, so every chain advances at once.
+//      between lanes merge through a warp carry, the (at most two) words a
+//      tile shares with its neighbours are parked in `edge` and merged by
+//      k_entropy_fixup, so no warp ever waits on another's emission.
 // Flags carry the launch epoch, so status memory is never re-zeroed.
+#include <algorithm>
+
 #include "encoder.cuh"
 
 namespace hdll {
 
 constexpr int kRunCtx = 4;  // _kernels.py:17
+constexpr long long kSpinLimit = 1LL << 24;
+constexpr int kDctLaneCap = 129;  // >= 127 symbols per block; odd stride against bank conflicts
 
-constexpr long long kSpinLimit = 1LL << 26;
+// ---------------------------------------------------------------------------
+// small helpers
+// ---------------------------------------------------------------------------
+// smallest k <= 15 with (N << k) >= A  (_select_k, _kernels.py:114-119), closed form
+__device__ __forceinline__ int kfast(int a, int n) {
+  if (a <= n) return 0;
+  int k0 = __clz(n) - __clz(a - 1);  // bitlen(a-1) - bitlen(n) >= 0
+  int k = ((n << k0) >= a) ? k0 : k0 + 1;
+  return k < kRiceMaxK ? k : kRiceMaxK;
+}
+
+__device__ __noinline__ AMap amap_push_slow(AMap m, int u, int h) { return amap_push(m, u, h); }
+__device__ __noinline__ AMap amap_then_slow(AMap f, AMap g) { return amap_then(f, g); }
+
+__device__ __forceinline__ void amap_push_fast(AMap& m, int u, int h) {
+  if (m.s >= 0 && m.s + h < kADomainBits) {
+    m.c += (long long)u << m.s;
+    m.s += h;
+  } else {
+    m = amap_push_slow(m, u, h);
+  }
+}
+
+__device__ __forceinline__ AMap warp_excl_amap_small(const AMap& m, AMap* total) {
+  const unsigned lane = threadIdx.x & 31u;
+  AMap x = m;
+#pragma unroll 1
+  for (int d = 1; d < 32; d <<= 1) {
+    AMap y = shfl_up_amap(x, d);
+    if (lane >= (unsigned)d) x = amap_then_slow(y, x);
+  }
+  *total = shfl_amap(x, 31);
+  AMap ex = shfl_up_amap(x, 1);
+  if (lane == 0) ex = amap_identity();
+  return ex;
+}
 
 __device__ __forceinline__ int wait_state(const ChainTab& ct, long long g, int which, unsigned* status) {
   const int* f = ct.flags + g * 4 + which;
@@ -41,7 +78,7 @@ __device__ __forceinline__ int wait_state(const ChainTab& ct, long long g, int w
       atomicOr(status, kErrLookback);
       return 0;
     }
-    __nanosleep(32);
+    __nanosleep(20);
   }
 }
 
@@ -50,8 +87,25 @@ __device__ __forceinline__ void publish(const ChainTab& ct, long long g, int whi
   st_release(ct.flags + g * 4 + which, (ct.epoch << 2) | state);
 }
 
+// ticket -> (chain, tile-in-chain, global tile) through the round-robin schedule
+__device__ __forceinline__ bool next_tile(const ChainTab& ct, int* chain, long long* tin, long long* g) {
+  const int lane = threadIdx.x & 31;
+  long long t = 0;
+  if (lane == 0) t = atomicAdd(ct.ticket, 1);
+  t = __shfl_sync(0xffffffffu, t, 0);
+  if (t >= ct.ntiles) return false;
+  int k = 0;
+  while (k + 1 < ct.nseg && ct.seg_t0[k + 1] <= t) k++;
+  const long long rel = t - ct.seg_t0[k];
+  const int act = ct.seg_active[k];
+  *tin = ct.seg_r0[k] + rel / act;
+  *chain = ct.rr_chain[rel % act];
+  *g = ct.tile_base[*chain] + *tin;
+  return true;
+}
+
 // ---------------------------------------------------------------------------
-// Bit emission with lane carry (see file comment).
+// Bit emission
 // ---------------------------------------------------------------------------
 struct WordSink {
   uint32_t* words;
@@ -61,11 +115,9 @@ struct WordSink {
   uint32_t* edge;  // this tile's [head, tail] slots
   unsigned* status;
 
-  // complete words owned by this tile; the word it shares with the previous
-  // tile (its first word when it starts mid-word) is parked in edge[0]
-  __device__ void write(long long idx, uint32_t w) const {
+  __device__ __forceinline__ void write(long long idx, uint32_t w) const {
     if (idx == tile_first_word && tile_start_partial) {
-      edge[0] = w;
+      edge[0] = w;  // shared with the previous tile: merged by the fix-up pass
       return;
     }
     if (idx >= cap_words) {
@@ -77,37 +129,31 @@ struct WordSink {
 };
 
 struct LaneBits {
-  // streaming accumulator for one lane's bits starting at global bit s
   unsigned long long acc;
   int nacc;
-  long long wpos;   // word index being filled
-  long long first;  // first word index of the lane
-  bool head_partial;
-  bool have_head;
+  long long wpos, first;
+  bool head_partial, have_head;
   uint32_t head;
-  const WordSink* sink;
 
-  __device__ void init(long long s, const WordSink* k) {
-    sink = k;
+  __device__ __forceinline__ void init(long long s) {
     wpos = first = s >> 5;
     nacc = (int)(s & 31);
     acc = 0;
     head_partial = nacc != 0;
     have_head = false;
   }
-  __device__ __forceinline__ void put(uint32_t bits, int len) {
-    if (len == 0) return;
+  __device__ __forceinline__ void put(const WordSink& sink, uint32_t bits, int len) {
     acc = (acc << len) | (unsigned long long)bits;
     nacc += len;
     if (nacc >= 32) {
       uint32_t w = (uint32_t)(acc >> (nacc - 32));
       nacc -= 32;
-      acc &= (nacc ? ((1ULL << nacc) - 1) : 0ULL);
+      acc &= (1ULL << nacc) - 1ULL;
       if (wpos == first && head_partial) {
         head = w;
         have_head = true;
       } else {
-        sink->write(wpos, w);
+        sink.write(wpos, w);
       }
       wpos++;
     }
@@ -115,141 +161,184 @@ struct LaneBits {
 };
 
 // ---------------------------------------------------------------------------
-// The tile engine (one warp).
+// Symbol formats in shared memory
+//   plane: u16 = ctx << 8 | value
+//   dct  : u32 = xb << 14 | xl << 9 | lctx << 7 | value   (value <= 64, xl <= 17)
 // ---------------------------------------------------------------------------
-template <int NCTX, class Gen>
-__device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long g, const Gen& gen, unsigned* status) {
+struct PlaneSym {
+  typedef uint16_t T;
+  static __device__ __forceinline__ void dec(T s, int& c, int& v, int& xl, uint32_t& xb) {
+    c = s >> 8;
+    v = s & 0xFF;
+    xl = 0;
+    xb = 0;
+  }
+};
+struct DctSym {
+  typedef uint32_t T;
+  static __device__ __forceinline__ T enc(int c, int v, int xl, uint32_t xb) {
+    return (xb << 14) | ((uint32_t)xl << 9) | ((uint32_t)c << 7) | (uint32_t)v;
+  }
+  static __device__ __forceinline__ void dec(T s, int& c, int& v, int& xl, uint32_t& xb) {
+    v = s & 0x7F;
+    c = (s >> 7) & 3;
+    xl = (s >> 9) & 31;
+    xb = s >> 14;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// The tile engine over a lane's symbol list in shared memory.
+//   NL local contexts used by the tile, mapped to chain contexts base..base+NL-1,
+//   NC contexts carried by the chain.
+// ---------------------------------------------------------------------------
+template <int NL, int NC, class S>
+__device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long g, int base,
+                         const typename S::T* syms, int nsym, const int* cnt_in, unsigned* status) {
   const int lane = threadIdx.x & 31;
   const bool chain_start = tin == 0;
 
-  // ---- 1. counts ----
-  int cnt[NCTX];
+  // ---- 1. counts -> global symbol index of this lane's first symbol per context ----
+  long long lbase[NL], tot[NL];
 #pragma unroll
-  for (int c = 0; c < NCTX; c++) cnt[c] = 0;
-  gen.for_each([&](int ctx, int v, int xl, uint32_t xb) { cnt[ctx]++; });
-  long long lbase[NCTX], tot[NCTX], incnt[NCTX];
-#pragma unroll
-  for (int c = 0; c < NCTX; c++) {
+  for (int c = 0; c < NL; c++) {
     long long t;
-    lbase[c] = warp_excl_sum((long long)cnt[c], &t);
+    lbase[c] = warp_excl_sum((long long)cnt_in[c], &t);
     tot[c] = t;
-    incnt[c] = 0;
   }
+  long long incnt[NC];
+#pragma unroll
+  for (int c = 0; c < NC; c++) incnt[c] = 0;
   if (lane == 0) {
     long long* cv = ct.cnt + g * 2 * kMaxCtx;
-    if (chain_start) {
-      for (int c = 0; c < NCTX; c++) cv[kMaxCtx + c] = tot[c];
-      publish(ct, g, 0, 2);
-    } else {
-      for (int c = 0; c < NCTX; c++) cv[c] = tot[c];
+    if (!chain_start) {
+#pragma unroll
+      for (int c = 0; c < NC; c++) cv[c] = (c >= base && c < base + NL) ? tot[c - base] : 0;
       publish(ct, g, 0, 1);
-      long long j = g - 1;
-      long long jmin = g - tin;
-      for (;;) {
+      const long long jmin = g - tin;
+      for (long long j = g - 1;; j--) {
         int st = wait_state(ct, j, 0, status);
         volatile const long long* pv = ct.cnt + j * 2 * kMaxCtx;
         if (st == 2) {
-          for (int c = 0; c < NCTX; c++) incnt[c] += pv[kMaxCtx + c];
+#pragma unroll
+          for (int c = 0; c < NC; c++) incnt[c] += pv[kMaxCtx + c];
           break;
         }
-        for (int c = 0; c < NCTX; c++) incnt[c] += pv[c];
-        if (st == 0 || j == jmin) break;
-        j--;
-      }
-      for (int c = 0; c < NCTX; c++) cv[kMaxCtx + c] = incnt[c] + tot[c];
-      publish(ct, g, 0, 2);
-    }
-  }
 #pragma unroll
-  for (int c = 0; c < NCTX; c++) incnt[c] = __shfl_sync(0xffffffffu, incnt[c], 0);
+        for (int c = 0; c < NC; c++) incnt[c] += pv[c];
+        if (st == 0 || j == jmin) break;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NC; c++) cv[kMaxCtx + c] = incnt[c] + ((c >= base && c < base + NL) ? tot[c - base] : 0);
+    publish(ct, g, 0, 2);
+  }
+  long long idx[NL];
+#pragma unroll
+  for (int c = 0; c < NL; c++) idx[c] = __shfl_sync(0xffffffffu, incnt[base + c], 0) + lbase[c];
 
   // ---- 2. A-maps ----
-  AMap m[NCTX];
-  long long idx[NCTX];
+  AMap m[NL];
+  {
+    long long j[NL];
 #pragma unroll
-  for (int c = 0; c < NCTX; c++) {
-    m[c] = amap_identity();
-    idx[c] = incnt[c] + lbase[c];
+    for (int c = 0; c < NL; c++) {
+      m[c] = amap_identity();
+      j[c] = idx[c];
+    }
+    for (int i = 0; i < nsym; i++) {
+      int c, v, xl;
+      uint32_t xb;
+      S::dec(syms[i], c, v, xl, xb);
+#pragma unroll
+      for (int q = 0; q < NL; q++)
+        if (c == q) {
+          amap_push_fast(m[q], v, halves_after(j[q]));
+          j[q]++;
+        }
+    }
   }
-  gen.for_each([&](int ctx, int v, int xl, uint32_t xb) {
-    m[ctx] = amap_push(m[ctx], v, halves_after(idx[ctx]));
-    idx[ctx]++;
-  });
-  AMap pre[NCTX], agg[NCTX];
+  AMap pre[NL], agg[NL];
+#pragma unroll 1
+  for (int c = 0; c < NL; c++) pre[c] = warp_excl_amap_small(m[c], &agg[c]);
+  int ain[NC];
 #pragma unroll
-  for (int c = 0; c < NCTX; c++) pre[c] = warp_excl_amap(m[c], &agg[c]);
-  int ain[NCTX];
+  for (int c = 0; c < NC; c++) ain[c] = 4;  // AdaptiveRiceState: A = 4, N = 1
   if (lane == 0) {
-    int* sv = ct.states + g * kMaxCtx;
-    for (int c = 0; c < NCTX; c++) ain[c] = 4;  // AdaptiveRiceState: A = 4, N = 1
     if (!chain_start) {
       AMap* mv = ct.maps + g * kMaxCtx;
-      for (int c = 0; c < NCTX; c++) mv[c] = agg[c];
+#pragma unroll
+      for (int c = 0; c < NC; c++) mv[c] = (c >= base && c < base + NL) ? agg[c - base] : amap_identity();
       publish(ct, g, 1, 1);
-      AMap acc[NCTX];
-      for (int c = 0; c < NCTX; c++) acc[c] = amap_identity();
-      long long j = g - 1;
-      long long jmin = g - tin;
-      for (;;) {
+      AMap acc[NC];
+#pragma unroll
+      for (int c = 0; c < NC; c++) acc[c] = amap_identity();
+      const long long jmin = g - tin;
+      for (long long j = g - 1;; j--) {
         int st = wait_state(ct, j, 1, status);
         if (st == 2) {
           volatile const int* ps = ct.states + j * kMaxCtx;
-          for (int c = 0; c < NCTX; c++) ain[c] = (int)amap_apply(acc[c], ps[c]);
+#pragma unroll
+          for (int c = 0; c < NC; c++) ain[c] = (int)amap_apply(acc[c], ps[c]);
           break;
         }
         volatile const AMap* pm = ct.maps + j * kMaxCtx;
-        for (int c = 0; c < NCTX; c++) {
+#pragma unroll 1
+        for (int c = 0; c < NC; c++) {
           AMap a;
           a.c = pm[c].c;
           a.s = pm[c].s;
           a.t = pm[c].t;
-          acc[c] = amap_then(a, acc[c]);
+          acc[c] = amap_then_slow(a, acc[c]);
         }
         if (st == 0 || j == jmin) {
-          for (int c = 0; c < NCTX; c++) ain[c] = (int)amap_apply(acc[c], 4);
+#pragma unroll
+          for (int c = 0; c < NC; c++) ain[c] = (int)amap_apply(acc[c], 4);
           break;
         }
-        j--;
       }
     }
-    for (int c = 0; c < NCTX; c++) sv[c] = (int)amap_apply(agg[c], ain[c]);
+    int* sv = ct.states + g * kMaxCtx;
+#pragma unroll
+    for (int c = 0; c < NC; c++)
+      sv[c] = (c >= base && c < base + NL) ? (int)amap_apply(agg[c - base], ain[c]) : ain[c];
     publish(ct, g, 1, 2);
   }
-  long long A[NCTX];
+  int A[NL];
 #pragma unroll
-  for (int c = 0; c < NCTX; c++) {
-    ain[c] = __shfl_sync(0xffffffffu, ain[c], 0);
-    A[c] = amap_apply(pre[c], ain[c]);
-    idx[c] = incnt[c] + lbase[c];
-  }
+  for (int c = 0; c < NL; c++) A[c] = (int)amap_apply(pre[c], __shfl_sync(0xffffffffu, ain[base + c], 0));
 
   // ---- 3. code lengths ----
   long long nbits = 0;
   {
-    long long A2[NCTX], i2[NCTX];
+    int a2[NL];
+    long long j[NL];
 #pragma unroll
-    for (int c = 0; c < NCTX; c++) A2[c] = A[c], i2[c] = idx[c];
-    gen.for_each([&](int ctx, int v, int xl, uint32_t xb) {
-      int k = select_k(A2[ctx], n_before(i2[ctx]));
-      nbits += rice_len(v, k) + xl;
-      A2[ctx] = (A2[ctx] + v) >> halves_after(i2[ctx]);
-      i2[ctx]++;
-    });
+    for (int c = 0; c < NL; c++) a2[c] = A[c], j[c] = idx[c];
+    for (int i = 0; i < nsym; i++) {
+      int c, v, xl;
+      uint32_t xb;
+      S::dec(syms[i], c, v, xl, xb);
+#pragma unroll
+      for (int q = 0; q < NL; q++)
+        if (c == q) {
+          int k = kfast(a2[q], n_before(j[q]));
+          nbits += rice_len(v, k) + xl;
+          a2[q] = (a2[q] + v) >> halves_after(j[q]);
+          j[q]++;
+        }
+    }
   }
   long long tbits;
-  long long loff = warp_excl_sum(nbits, &tbits);
+  const long long loff = warp_excl_sum(nbits, &tbits);
   long long toff = 0;
   if (lane == 0) {
     unsigned long long* bv = ct.bitv + g * 2;
-    if (chain_start) {
-      bv[0] = (unsigned long long)tbits;
-      bv[1] = (unsigned long long)tbits;
-      publish(ct, g, 2, 2);
-    } else {
-      bv[0] = (unsigned long long)tbits;
+    bv[0] = (unsigned long long)tbits;
+    if (!chain_start) {
       publish(ct, g, 2, 1);
-      long long j = g - 1, jmin = g - tin;
-      for (;;) {
+      const long long jmin = g - tin;
+      for (long long j = g - 1;; j--) {
         int st = wait_state(ct, j, 2, status);
         volatile const unsigned long long* pv = ct.bitv + j * 2;
         if (st == 2) {
@@ -258,13 +347,11 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
         }
         toff += (long long)pv[0];
         if (st == 0 || j == jmin) break;
-        j--;
       }
-      bv[1] = (unsigned long long)(toff + tbits);
-      publish(ct, g, 2, 2);
     }
-    long long ntile_chain = ct.tile_base[chain + 1] - ct.tile_base[chain];
-    if (tin == ntile_chain - 1) ct.bits[chain] = (unsigned long long)(toff + tbits);
+    bv[1] = (unsigned long long)(toff + tbits);
+    publish(ct, g, 2, 2);
+    if (tin == ct.tile_base[chain + 1] - ct.tile_base[chain] - 1) ct.bits[chain] = (unsigned long long)(toff + tbits);
   }
   toff = __shfl_sync(0xffffffffu, toff, 0);
 
@@ -276,52 +363,47 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
   sink.tile_start_partial = (toff & 31) != 0;
   sink.edge = ct.edge + g * 2;
   sink.status = status;
-  const long long s_l = toff + loff, e_l = s_l + nbits;
   LaneBits lb;
-  lb.init(s_l, &sink);
-  gen.for_each([&](int ctx, int v, int xl, uint32_t xb) {
-    int k = select_k(A[ctx], n_before(idx[ctx]));
-    lb.put(rice_bits(v, k), rice_len(v, k));
-    if (xl) {
-      if (xl > 16) {
-        lb.put(xb >> 16, xl - 16);
-        lb.put(xb & 0xFFFFu, 16);
-      } else {
-        lb.put(xb, xl);
-      }
+  lb.init(toff + loff);
+  {
+    long long j[NL];
+#pragma unroll
+    for (int c = 0; c < NL; c++) j[c] = idx[c];
+    for (int i = 0; i < nsym; i++) {
+      int c, v, xl;
+      uint32_t xb;
+      S::dec(syms[i], c, v, xl, xb);
+      int k = 0;
+#pragma unroll
+      for (int q = 0; q < NL; q++)
+        if (c == q) {
+          k = kfast(A[q], n_before(j[q]));
+          A[q] = (A[q] + v) >> halves_after(j[q]);
+          j[q]++;
+        }
+      lb.put(sink, rice_bits(v, k), rice_len(v, k));
+      if (xl) lb.put(sink, xb, xl);
     }
-    A[ctx] = (A[ctx] + v) >> halves_after(idx[ctx]);
-    idx[ctx]++;
-  });
-  // lane partial words: head (word s_l>>5, started mid-word) and/or tail (bits left in acc)
+  }
+  // lane partial words: head (started mid-word, completed) and tail (bits left)
   const bool has_tail = lb.nacc > 0 && nbits > 0;
-  uint32_t tail = has_tail ? (uint32_t)(lb.acc << (32 - lb.nacc)) : 0u;
+  const uint32_t tail = has_tail ? (uint32_t)(lb.acc << (32 - lb.nacc)) : 0u;
   const long long tail_word = lb.wpos;
-  // single: the lane's bits sit inside one word that it does not complete
-  const bool single = nbits > 0 && has_tail && tail_word == lb.first && lb.head_partial;
-  // carry loop over lanes, in order
+  const bool single = has_tail && tail_word == lb.first && lb.head_partial;
   long long cw = -1;
   uint32_t cb = 0;
+#pragma unroll 1
   for (int l = 0; l < 32; l++) {
     long long ncw = cw;
     uint32_t ncb = cb;
     if (lane == l && nbits > 0) {
       if (single) {
-        uint32_t w = (cw == lb.first ? cb : 0u) | tail;
         ncw = lb.first;
-        ncb = w;
+        ncb = (cw == lb.first ? cb : 0u) | tail;
       } else {
-        if (lb.have_head) {
-          uint32_t w = (cw == lb.first ? cb : 0u) | lb.head;
-          sink.write(lb.first, w);
-        }
-        if (has_tail) {
-          ncw = tail_word;
-          ncb = tail;
-        } else {
-          ncw = -1;
-          ncb = 0;
-        }
+        if (lb.have_head) sink.write(lb.first, (cw == lb.first ? cb : 0u) | lb.head);
+        ncw = has_tail ? tail_word : -1;
+        ncb = has_tail ? tail : 0u;
       }
     }
     cw = __shfl_sync(0xffffffffu, ncw, l);
@@ -332,59 +414,127 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
     if (cw == sink.tile_first_word && sink.tile_start_partial) sink.edge[0] = cb;
     else sink.edge[1] = cb;
   }
-  (void)e_l;
 }
 
 // ---------------------------------------------------------------------------
-// Plane coder tile = one row (encode_plane, _kernels.py:169-216)
+// Plane coder: tile = one row (encode_plane, _kernels.py:169-216)
 // ---------------------------------------------------------------------------
 enum { kFree = 0, kForced = 1, kInRun = 2 };
 
-struct PlaneRow {
+struct RowView {
   const uint8_t* cur;
   const uint8_t* prev;  // nullptr on row 0
-  int w;
-  int x0, x1;           // lane slice
-  int entry;            // automaton state entering the slice
-  long long cont_next;  // run continuation entering the next lane
-
   // _neighbors, _kernels.py:131-143
   __device__ __forceinline__ void abc(int x, int& a, int& b, int& c) const {
     a = x > 0 ? cur[x - 1] : (prev ? prev[x] : 128);
     b = prev ? prev[x] : a;
     c = (x > 0 && prev) ? prev[x - 1] : b;
   }
-  __device__ __forceinline__ bool ebit(int x) const {
-    int a, b, c;
-    abc(x, a, b, c);
-    return cur[x] == a;
-  }
+};
 
-  template <class Fn>
-  __device__ __forceinline__ void for_each(Fn&& f) const {
-    int st = entry;
+__device__ __forceinline__ int slice_transition(const RowView& rv, int x0, int x1, int st) {
+  for (int x = x0; x < x1; x++) {
+    int a, b, c;
+    rv.abc(x, a, b, c);
+    bool E = rv.cur[x] == a;
+    if (st == kFree && a == b && b == c) st = kInRun;
+    if (st == kInRun && E) continue;
+    st = kFree;
+  }
+  return st;
+}
+
+// grid-persistent; dynamic smem per warp: 2 row copies + 32 lane symbol lists
+__global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict__ descs, ChainTab ct, int row_bytes,
+                                                       int lane_cap) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const size_t per_warp = 2 * (size_t)row_bytes + 32 * (size_t)lane_cap * sizeof(uint16_t);
+  uint8_t* wbase = smem_raw + warp * per_warp;
+  uint8_t* srow_prev = wbase;
+  uint8_t* srow_cur = wbase + row_bytes;
+  uint16_t* ssym = reinterpret_cast<uint16_t*>(wbase + 2 * row_bytes) + lane * lane_cap;
+  int chain;
+  long long tin, g;
+  while (next_tile(ct, &chain, &tin, &g)) {
+    const ImgDesc& d = descs[ct.img[chain]];
+    const int kind = ct.kind[chain];
+    const int y = (int)tin, W = d.w;
+    const uint8_t* src = kind == 1 ? d.e_plane : d.res_planes + (long long)(kind - 2) * d.n;
+    const uint8_t* gcur = src + (long long)y * W;
+    for (int x = lane; x < W; x += 32) {
+      srow_cur[x] = gcur[x];
+      if (y > 0) srow_prev[x] = gcur[x - W];
+    }
+    __syncwarp();
+    RowView rv{srow_cur, y > 0 ? srow_prev : nullptr};
+    const int P = (W + 31) / 32;
+    const int x0 = min(W, lane * P), x1 = min(W, x0 + P);
+    // automaton state entering each slice: compose the 3-state transition maps
+    int T = slice_transition(rv, x0, x1, kFree) | (slice_transition(rv, x0, x1, kForced) << 2) |
+            (slice_transition(rv, x0, x1, kInRun) << 4);
+    int comp = T;
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+      int o = __shfl_up_sync(0xffffffffu, comp, dd);
+      if (lane >= dd) {
+        int r = 0;
+#pragma unroll
+        for (int s = 0; s < 3; s++) r |= ((comp >> (2 * ((o >> (2 * s)) & 3))) & 3) << (2 * s);
+        comp = r;
+      }
+    }
+    const int excl = __shfl_up_sync(0xffffffffu, comp, 1);
+    int st = lane == 0 ? kFree : (excl & 3);
+    // run continuation into the next slices: leading E-ones, passing whole slices
+    int lead = 0;
     for (int x = x0; x < x1; x++) {
       int a, b, c;
-      abc(x, a, b, c);
-      const int xv = cur[x];
+      rv.abc(x, a, b, c);
+      if (rv.cur[x] != a) break;
+      lead++;
+    }
+    int val = lead;
+    bool fl = lead == x1 - x0;
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+      int ov = __shfl_down_sync(0xffffffffu, val, dd);
+      bool of = __shfl_down_sync(0xffffffffu, fl, dd);
+      if (lane + dd < 32) {
+        if (fl) {
+          val += ov;
+          fl = of;
+        }
+      } else {
+        fl = false;
+      }
+    }
+    const int nx = __shfl_down_sync(0xffffffffu, val, 1);
+    const int cont_next = lane == 31 ? 0 : nx;
+    // generate the lane's symbols
+    int n = 0;
+    int cnt[5] = {0, 0, 0, 0, 0};
+    for (int x = x0; x < x1; x++) {
+      int a, b, c;
+      rv.abc(x, a, b, c);
+      const int xv = rv.cur[x];
       const bool E = xv == a;
       if (st == kFree && a == b && b == c) {
-        // run mode: run = samples equal to a from x; chunks of <= 255, 255 continues
-        long long L = 0;
-        int xx = x;
+        // run mode: samples equal to a from x; chunks of <= 255, 255 continues
+        int L = 0, xx = x;
         bool e = E;
         while (e) {
           L++;
-          xx++;
-          if (xx >= x1) break;
-          e = cur[xx] == cur[xx - 1];
+          if (++xx >= x1) break;
+          e = rv.cur[xx] == rv.cur[xx - 1];
         }
         if (xx >= x1 && e) L += cont_next;
-        long long rem = L;
         for (;;) {
-          int ch = rem >= 255 ? 255 : (int)rem;
-          f(kRunCtx, ch, 0, 0u);
-          rem -= ch;
+          int ch = L >= 255 ? 255 : L;
+          if (n < lane_cap) ssym[n] = (uint16_t)((kRunCtx << 8) | ch);
+          n++;
+          cnt[kRunCtx]++;
+          L -= ch;
           if (ch < 255) break;
         }
         st = kInRun;
@@ -394,78 +544,100 @@ struct PlaneRow {
         st = kForced;
       }
       // regular sample: MED prediction, activity context, folded residual
-      int mx = max(a, b), mn = min(a, b);
-      int pred = c >= mx ? mn : (c <= mn ? mx : a + b - c);
-      int g = abs(a - c) + abs(c - b);
-      int ctx = g == 0 ? 0 : (g <= 2 ? 1 : (g <= 8 ? 2 : 3));
+      const int mx = max(a, b), mn = min(a, b);
+      const int pred = c >= mx ? mn : (c <= mn ? mx : a + b - c);
+      const int gg = abs(a - c) + abs(c - b);
+      const int ctx = gg == 0 ? 0 : (gg <= 2 ? 1 : (gg <= 8 ? 2 : 3));
       int r = (xv - pred) & 255;
       if (r > 127) r -= 256;
-      int u = r >= 0 ? 2 * r : -2 * r - 1;
-      f(ctx, u, 0, 0u);
+      const int u = r >= 0 ? 2 * r : -2 * r - 1;
+      if (n < lane_cap) ssym[n] = (uint16_t)((ctx << 8) | u);
+      n++;
+#pragma unroll
+      for (int q = 0; q < 4; q++) cnt[q] += ctx == q;
       st = kFree;
     }
-  }
-};
-
-__device__ __forceinline__ int slice_transition(const PlaneRow& pr, int st0) {
-  int st = st0;
-  for (int x = pr.x0; x < pr.x1; x++) {
-    int a, b, c;
-    pr.abc(x, a, b, c);
-    bool E = pr.cur[x] == a;
-    if (st == kFree && a == b && b == c) st = kInRun;
-    if (st == kInRun) {
-      if (E) continue;
-      st = kForced;
+    if (n > lane_cap) {
+      atomicOr(d.status, kErrCapacity);
+      n = lane_cap;
     }
-    st = kFree;
+    run_tile<5, 5, PlaneSym>(ct, chain, tin, g, 0, ssym, n, cnt, d.status);
+    __syncwarp();
   }
-  return st;
 }
 
 // ---------------------------------------------------------------------------
-// DCT coder tile = 32 blocks of one component (encode_dct_component)
+// DCT coder: tile = 32 blocks of one component, lane = block (encode_dct_component)
 // ---------------------------------------------------------------------------
-struct DctBlock {
-  const int16_t* z;  // this block's 64 zigzag coefficients (nullptr: lane idle)
-  int prev_dc;
-  int base;          // context bank: 0 luma, 3 chroma
-
-  __device__ __forceinline__ static int bitlen(unsigned u) { return u ? 32 - __clz(u) : 0; }
-  __device__ __forceinline__ static unsigned interleave(int v) { return v >= 0 ? 2u * v : (unsigned)(-2 * v - 1); }
-
-  template <class Fn>
-  __device__ __forceinline__ void for_each(Fn&& f) const {
-    if (!z) return;
-    int dc = z[0];
-    unsigned u = interleave(dc - prev_dc);
-    int s = bitlen(u);
-    f(base, s, s, u);
-    int pos = 1;
-    while (pos < 64) {
-      int nz = -1;
-      for (int j = pos; j < 64; j++)
-        if (z[j] != 0) {
-          nz = j;
+__global__ void __launch_bounds__(128) k_entropy_dct(const ImgDesc* __restrict__ descs, ChainTab ct) {
+  extern __shared__ __align__(16) uint32_t sbuf[];  // per warp, per lane symbol list (<= 127 per block)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* ssym = sbuf + (warp * 32 + lane) * kDctLaneCap;
+  int chain;
+  long long tin, g;
+  while (next_tile(ct, &chain, &tin, &g)) {
+    const ImgDesc& d = descs[ct.img[chain]];
+    const long long tpc = (d.nblocks + 31) / 32;
+    const int ci = (int)(tin / tpc);
+    const long long bi = (tin % tpc) * 32 + lane;
+    int n = 0;
+    int cnt[3] = {0, 0, 0};
+    if (bi < d.nblocks) {
+      const int16_t* z = d.zz + ((long long)ci * d.nblocks + bi) * 64;
+      // nonzero mask of the 64 zigzag coefficients, 128-bit loads
+      const uint4* z4 = reinterpret_cast<const uint4*>(z);
+      unsigned long long nzm = 0;
+      int dc = 0;
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        uint4 v = z4[q];
+        uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+        if (q == 0) dc = (int)(int16_t)(ws[0] & 0xFFFF);
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+          nzm |= (unsigned long long)((ws[r] & 0xFFFFu) != 0) << (q * 8 + r * 2);
+          nzm |= (unsigned long long)((ws[r] >> 16) != 0) << (q * 8 + r * 2 + 1);
+        }
+      }
+      nzm &= ~1ULL;
+      const int prev_dc = bi > 0 ? d.zz[((long long)ci * d.nblocks + bi - 1) * 64] : 0;
+      // DC: size s of the interleaved difference (ctx 0) + s raw bits
+      int dv = dc - prev_dc;
+      unsigned u = dv >= 0 ? 2u * dv : (unsigned)(-2 * dv - 1);
+      int s = u ? 32 - __clz(u) : 0;
+      ssym[n++] = DctSym::enc(0, s, s, u);
+      cnt[0]++;
+      // AC: (zero run ctx 1, size ctx 2 + raw bits), EOB = run 64 unless position 63 is coded
+      int pos = 1;
+      while (pos < 64) {
+        unsigned long long rest = nzm >> pos;
+        if (rest == 0) {
+          ssym[n++] = DctSym::enc(1, kEOB, 0, 0u);
+          cnt[1]++;
           break;
         }
-      if (nz < 0) {
-        f(base + 1, kEOB, 0, 0u);
-        break;
+        int nz = pos + __ffsll((long long)rest) - 1;
+        ssym[n++] = DctSym::enc(1, nz - pos, 0, 0u);
+        cnt[1]++;
+        int zv = z[nz];
+        u = zv >= 0 ? 2u * zv : (unsigned)(-2 * zv - 1);
+        s = 32 - __clz(u);
+        ssym[n++] = DctSym::enc(2, s, s, u);
+        cnt[2]++;
+        pos = nz + 1;
       }
-      f(base + 1, nz - pos, 0, 0u);
-      u = interleave(z[nz]);
-      s = bitlen(u);
-      f(base + 2, s, s, u);
-      pos = nz + 1;
     }
+    run_tile<3, 6, DctSym>(ct, chain, tin, g, ci == 0 ? 0 : 3, ssym, n, cnt, d.status);
+    __syncwarp();
   }
-};
+}
 
 // ---------------------------------------------------------------------------
-// Kernels: a warp takes the next ticket = next global tile.
+// Fix-up: merge the words shared between tiles.  Word w belongs to the tile
+// holding its first bit; that tile's tail plus the heads of the following
+// tiles that start inside w (several, if tiles are tiny) are OR-ed once.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int find_chain(const ChainTab& ct, long long g) {  // chain of global tile g
+__device__ __forceinline__ int find_chain(const ChainTab& ct, long long g) {
   int lo = 0, hi = ct.nchains;
   while (hi - lo > 1) {
     int mid = (lo + hi) >> 1;
@@ -474,90 +646,6 @@ __device__ __forceinline__ int find_chain(const ChainTab& ct, long long g) {  //
   return lo;
 }
 
-__global__ void __launch_bounds__(128) k_entropy(const ImgDesc* __restrict__ descs, ChainTab ct) {
-  const int lane = threadIdx.x & 31;
-  for (;;) {
-    long long t = 0;
-    if (lane == 0) t = atomicAdd(ct.ticket, 1);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    if (t >= ct.ntiles) return;
-    // round-robin over chains: all chains advance together, every wait is on an older ticket
-    int k = 0;
-    while (k + 1 < ct.nseg && ct.seg_t0[k + 1] <= t) k++;
-    const long long rel = t - ct.seg_t0[k];
-    const int act = ct.seg_active[k];
-    const long long tin = ct.seg_r0[k] + rel / act;
-    const int chain = ct.rr_chain[rel % act];
-    const long long g = ct.tile_base[chain] + tin;
-    const ImgDesc& d = descs[ct.img[chain]];
-    const int kind = ct.kind[chain];
-    if (kind == 0) {
-      const long long tpc = (d.nblocks + 31) / 32;
-      const int ci = (int)(tin / tpc);
-      const long long bi = (tin % tpc) * 32 + lane;
-      DctBlock blk;
-      blk.base = ci == 0 ? 0 : 3;
-      blk.z = nullptr;
-      blk.prev_dc = 0;
-      if (bi < d.nblocks) {
-        blk.z = d.zz + ((long long)ci * d.nblocks + bi) * 64;
-        blk.prev_dc = bi > 0 ? d.zz[((long long)ci * d.nblocks + bi - 1) * 64] : 0;
-      }
-      run_tile<6>(ct, chain, tin, g, blk, d.status);
-    } else {
-      const int y = (int)tin;
-      const uint8_t* src = kind == 1 ? d.e_plane : d.res_planes + (long long)(kind - 2) * d.n;
-      PlaneRow pr;
-      pr.cur = src + (long long)y * d.w;
-      pr.prev = y > 0 ? src + (long long)(y - 1) * d.w : nullptr;
-      pr.w = d.w;
-      const int P = (d.w + 31) / 32;
-      pr.x0 = min(d.w, lane * P);
-      pr.x1 = min(d.w, pr.x0 + P);
-      // slice transition functions for the 3 entry states, composed across lanes
-      int T = slice_transition(pr, kFree) | (slice_transition(pr, kForced) << 2) |
-              (slice_transition(pr, kInRun) << 4);
-      int comp = T;  // inclusive composition (apply lower lanes first)
-#pragma unroll
-      for (int dd = 1; dd < 32; dd <<= 1) {
-        int o = __shfl_up_sync(0xffffffffu, comp, dd);
-        if (lane >= dd) {
-          int r = 0;
-          for (int s = 0; s < 3; s++) r |= ((comp >> (2 * ((o >> (2 * s)) & 3))) & 3) << (2 * s);
-          comp = r;
-        }
-      }
-      int excl = __shfl_up_sync(0xffffffffu, comp, 1);
-      pr.entry = lane == 0 ? kFree : (excl & 3);  // prefix applied to kFree
-      // leading run continuation: lead = E-ones from the slice start, pass = whole slice
-      long long lead = 0;
-      for (int x = pr.x0; x < pr.x1 && pr.ebit(x); x++) lead++;
-      bool pass = lead == pr.x1 - pr.x0;
-      long long val = lead;
-      bool fl = pass;
-#pragma unroll
-      for (int dd = 1; dd < 32; dd <<= 1) {
-        long long ov = __shfl_down_sync(0xffffffffu, val, dd);
-        bool of = __shfl_down_sync(0xffffffffu, fl, dd);
-        if (lane + dd < 32) {
-          if (fl) {
-            val += ov;
-            fl = of;
-          }
-        } else {
-          fl = false;
-        }
-      }
-      long long nx = __shfl_down_sync(0xffffffffu, val, 1);
-      pr.cont_next = lane == 31 ? 0 : nx;
-      run_tile<5>(ct, chain, tin, g, pr, d.status);
-    }
-  }
-}
-
-// Merge the words shared between tiles.  Word w belongs to the tile holding
-// its first bit; that tile's tail plus the heads of the following tiles that
-// start inside w (several, if tiles are tiny) are OR-ed and stored once.
 __global__ void __launch_bounds__(256) k_entropy_fixup(ChainTab ct) {
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= ct.ntiles) return;
@@ -580,16 +668,53 @@ __global__ void __launch_bounds__(256) k_entropy_fixup(ChainTab ct) {
   if (w < ct.cap[chain] / 4) words[w] = __byte_perm(v, 0, 0x0123);
 }
 
-void launch_entropy_fixup(const ChainTab& ct, cudaStream_t st) {
-  k_entropy_fixup<<<(unsigned)((ct.ntiles + 255) / 256), 256, 0, st>>>(ct);
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
 }
 
-void launch_entropy(const ImgDesc* d_descs, const ChainTab& ct, cudaStream_t st) {
-  int warps_per_block = 4;
-  long long blocks = (ct.ntiles + warps_per_block - 1) / warps_per_block;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  if (blocks < 1) blocks = 1;
-  k_entropy<<<(unsigned)blocks, 32 * warps_per_block, 0, st>>>(d_descs, ct);
+void launch_entropy_dct(const ImgDesc* d_descs, const ChainTab& ct, cudaStream_t st) {
+  if (ct.ntiles <= 0) return;
+  const size_t smem = sizeof(uint32_t) * 4 * 32 * kDctLaneCap;
+  cudaFuncSetAttribute(k_entropy_dct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_entropy_dct, 128, smem);
+  long long blocks = (long long)num_sms() * (per_sm > 0 ? per_sm : 1);
+  long long need = (ct.ntiles + 3) / 4;
+  if (blocks > need) blocks = need;
+  k_entropy_dct<<<(unsigned)blocks, 128, smem, st>>>(d_descs, ct);
+}
+
+void launch_entropy_plane(const ImgDesc* d_descs, const ChainTab& ct, int max_w, cudaStream_t st) {
+  if (ct.ntiles <= 0) return;
+  const int P = (max_w + 31) / 32;
+  const int lane_cap = 2 * P + max_w / 255 + 4;
+  const int row_bytes = (max_w + 16) / 16 * 16;
+  size_t per_warp = 2 * (size_t)row_bytes + 32 * (size_t)lane_cap * sizeof(uint16_t);
+  int warps = (int)std::min<size_t>(4, (200 * 1024) / per_warp);
+  if (warps < 1) warps = 1;
+  size_t smem = per_warp * warps;
+  cudaFuncSetAttribute(k_entropy_plane, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_entropy_plane, 32 * warps, smem);
+  long long blocks = (long long)num_sms() * (per_sm > 0 ? per_sm : 1);
+  long long need = (ct.ntiles + warps - 1) / warps;
+  if (blocks > need) blocks = need;
+  k_entropy_plane<<<(unsigned)blocks, 32 * warps, smem, st>>>(d_descs, ct, row_bytes, lane_cap);
+}
+
+void launch_entropy_fixup(const ChainTab& ct, cudaStream_t st) {
+  if (ct.ntiles <= 0) return;
+  k_entropy_fixup<<<(unsigned)((ct.ntiles + 255) / 256), 256, 0, st>>>(ct);
 }
 
 }  // namespace hdll
