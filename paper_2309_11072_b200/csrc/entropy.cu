@@ -83,7 +83,6 @@ __device__ __forceinline__ int wait_state(const ChainTab& ct, long long g, int w
 }
 
 __device__ __forceinline__ void publish(const ChainTab& ct, long long g, int which, int state) {
-  __threadfence();
   st_release(ct.flags + g * 4 + which, (ct.epoch << 2) | state);
 }
 
@@ -161,15 +160,22 @@ struct LaneBits {
 };
 
 // ---------------------------------------------------------------------------
-// Symbol formats in shared memory
-//   plane: u16 = ctx << 8 | value
-//   dct  : u32 = xb << 14 | xl << 9 | lctx << 7 | value   (value <= 64, xl <= 17)
+// Symbol formats in shared memory (k is filled in by the length pass)
+//   plane: u16 = k << 11 | ctx << 8 | value
+//   dct  : u32 = xb << 17 | k << 13 | xl << 9 | lctx << 7 | value
+//          (value <= 64, raw bits xl <= 13: |DC diff| <= 4080 and |AC| <= 2040
+//           for an orthonormal 8x8 DCT of 8-bit samples)
 // ---------------------------------------------------------------------------
 struct PlaneSym {
   typedef uint16_t T;
-  static __device__ __forceinline__ void dec(T s, int& c, int& v, int& xl, uint32_t& xb) {
-    c = s >> 8;
+  static __device__ __forceinline__ void dec(T s, int& c, int& v) {
+    c = (s >> 8) & 7;
     v = s & 0xFF;
+  }
+  static __device__ __forceinline__ T with_k(T s, int k) { return (T)(s | (k << 11)); }
+  static __device__ __forceinline__ void dec_emit(T s, int& v, int& k, int& xl, uint32_t& xb) {
+    v = s & 0xFF;
+    k = s >> 11;
     xl = 0;
     xb = 0;
   }
@@ -177,14 +183,29 @@ struct PlaneSym {
 struct DctSym {
   typedef uint32_t T;
   static __device__ __forceinline__ T enc(int c, int v, int xl, uint32_t xb) {
-    return (xb << 14) | ((uint32_t)xl << 9) | ((uint32_t)c << 7) | (uint32_t)v;
+    return (xb << 17) | ((uint32_t)xl << 9) | ((uint32_t)c << 7) | (uint32_t)v;
   }
-  static __device__ __forceinline__ void dec(T s, int& c, int& v, int& xl, uint32_t& xb) {
+  static __device__ __forceinline__ void dec(T s, int& c, int& v) {
     v = s & 0x7F;
     c = (s >> 7) & 3;
-    xl = (s >> 9) & 31;
-    xb = s >> 14;
   }
+  static __device__ __forceinline__ T with_k(T s, int k) { return s | ((uint32_t)k << 13); }
+  static __device__ __forceinline__ void dec_emit(T s, int& v, int& k, int& xl, uint32_t& xb) {
+    v = s & 0x7F;
+    xl = (s >> 9) & 15;
+    k = (s >> 13) & 15;
+    xb = s >> 17;
+  }
+};
+
+// Per-lane context state lives in shared memory, [context][lane], so a symbol
+// touches only its own context (no per-context predication).
+struct LaneState {
+  long long* mc;  // map constant
+  int* ms;        // map shift (< 0: step map)
+  int* mt;        // step-map threshold
+  int* a;         // A
+  int* nn;        // N
 };
 
 // ---------------------------------------------------------------------------
@@ -194,7 +215,7 @@ struct DctSym {
 // ---------------------------------------------------------------------------
 template <int NL, int NC, class S>
 __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long g, int base,
-                         const typename S::T* syms, int nsym, const int* cnt_in, unsigned* status) {
+                         typename S::T* syms, int nsym, const int* cnt_in, const LaneState& ls, unsigned* status) {
   const int lane = threadIdx.x & 31;
   const bool chain_start = tin == 0;
 
@@ -233,34 +254,43 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
     for (int c = 0; c < NC; c++) cv[kMaxCtx + c] = incnt[c] + ((c >= base && c < base + NL) ? tot[c - base] : 0);
     publish(ct, g, 0, 2);
   }
-  long long idx[NL];
+  int n0[NL];  // N before this lane's first symbol of each context
 #pragma unroll
-  for (int c = 0; c < NL; c++) idx[c] = __shfl_sync(0xffffffffu, incnt[base + c], 0) + lbase[c];
+  for (int c = 0; c < NL; c++) n0[c] = n_before(__shfl_sync(0xffffffffu, incnt[base + c], 0) + lbase[c]);
 
-  // ---- 2. A-maps ----
-  AMap m[NL];
-  {
-    long long j[NL];
+  // ---- 2. A-maps (the reference's update_state as a map of the incoming A) ----
 #pragma unroll
-    for (int c = 0; c < NL; c++) {
-      m[c] = amap_identity();
-      j[c] = idx[c];
-    }
-    for (int i = 0; i < nsym; i++) {
-      int c, v, xl;
-      uint32_t xb;
-      S::dec(syms[i], c, v, xl, xb);
-#pragma unroll
-      for (int q = 0; q < NL; q++)
-        if (c == q) {
-          amap_push_fast(m[q], v, halves_after(j[q]));
-          j[q]++;
-        }
+  for (int c = 0; c < NL; c++) {
+    ls.mc[c * 32 + lane] = 0;
+    ls.ms[c * 32 + lane] = 0;
+    ls.mt[c * 32 + lane] = 0;
+    ls.nn[c * 32 + lane] = n0[c];
+  }
+  for (int i = 0; i < nsym; i++) {
+    int c, v;
+    S::dec(syms[i], c, v);
+    const int o = c * 32 + lane;
+    const int nb = ls.nn[o];
+    const int h = nb == kStateReset - 1;  // N reaches 64: A and N halve
+    ls.nn[o] = h ? kStateReset / 2 : nb + 1;
+    const int sft = ls.ms[o];
+    if (sft >= 0 && sft + h < kADomainBits) {
+      ls.mc[o] += (long long)v << sft;
+      ls.ms[o] = sft + h;
+    } else {
+      AMap m{ls.mc[o], sft, ls.mt[o]};
+      m = amap_push_slow(m, v, h);
+      ls.mc[o] = m.c;
+      ls.ms[o] = m.s;
+      ls.mt[o] = m.t;
     }
   }
   AMap pre[NL], agg[NL];
 #pragma unroll 1
-  for (int c = 0; c < NL; c++) pre[c] = warp_excl_amap_small(m[c], &agg[c]);
+  for (int c = 0; c < NL; c++) {
+    AMap m{ls.mc[c * 32 + lane], ls.ms[c * 32 + lane], ls.mt[c * 32 + lane]};
+    pre[c] = warp_excl_amap_small(m, &agg[c]);
+  }
   int ain[NC];
 #pragma unroll
   for (int c = 0; c < NC; c++) ain[c] = 4;  // AdaptiveRiceState: A = 4, N = 1
@@ -304,30 +334,34 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
       sv[c] = (c >= base && c < base + NL) ? (int)amap_apply(agg[c - base], ain[c]) : ain[c];
     publish(ct, g, 1, 2);
   }
-  int A[NL];
-#pragma unroll
-  for (int c = 0; c < NL; c++) A[c] = (int)amap_apply(pre[c], __shfl_sync(0xffffffffu, ain[base + c], 0));
 
-  // ---- 3. code lengths ----
+  // ---- 3. code lengths; k of every symbol is stored for the emit pass ----
+#pragma unroll
+  for (int c = 0; c < NL; c++) {
+    ls.a[c * 32 + lane] = (int)amap_apply(pre[c], __shfl_sync(0xffffffffu, ain[base + c], 0));
+    ls.nn[c * 32 + lane] = n0[c];
+  }
   long long nbits = 0;
-  {
-    int a2[NL];
-    long long j[NL];
-#pragma unroll
-    for (int c = 0; c < NL; c++) a2[c] = A[c], j[c] = idx[c];
-    for (int i = 0; i < nsym; i++) {
-      int c, v, xl;
-      uint32_t xb;
-      S::dec(syms[i], c, v, xl, xb);
-#pragma unroll
-      for (int q = 0; q < NL; q++)
-        if (c == q) {
-          int k = kfast(a2[q], n_before(j[q]));
-          nbits += rice_len(v, k) + xl;
-          a2[q] = (a2[q] + v) >> halves_after(j[q]);
-          j[q]++;
-        }
+  for (int i = 0; i < nsym; i++) {
+    typename S::T sy = syms[i];
+    int c, v;
+    S::dec(sy, c, v);
+    const int o = c * 32 + lane;
+    int a = ls.a[o], nb = ls.nn[o];
+    const int k = kfast(a, nb);
+    int xl, kk, vv;
+    uint32_t xb;
+    S::dec_emit(sy, vv, kk, xl, xb);
+    nbits += rice_len(v, k) + xl;
+    a += v;  // _update_state
+    nb += 1;
+    if (nb >= kStateReset) {
+      a >>= 1;
+      nb >>= 1;
     }
+    ls.a[o] = a;
+    ls.nn[o] = nb;
+    syms[i] = S::with_k(sy, k);
   }
   long long tbits;
   const long long loff = warp_excl_sum(nbits, &tbits);
@@ -365,25 +399,12 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
   sink.status = status;
   LaneBits lb;
   lb.init(toff + loff);
-  {
-    long long j[NL];
-#pragma unroll
-    for (int c = 0; c < NL; c++) j[c] = idx[c];
-    for (int i = 0; i < nsym; i++) {
-      int c, v, xl;
-      uint32_t xb;
-      S::dec(syms[i], c, v, xl, xb);
-      int k = 0;
-#pragma unroll
-      for (int q = 0; q < NL; q++)
-        if (c == q) {
-          k = kfast(A[q], n_before(j[q]));
-          A[q] = (A[q] + v) >> halves_after(j[q]);
-          j[q]++;
-        }
-      lb.put(sink, rice_bits(v, k), rice_len(v, k));
-      if (xl) lb.put(sink, xb, xl);
-    }
+  for (int i = 0; i < nsym; i++) {
+    int v, k, xl;
+    uint32_t xb;
+    S::dec_emit(syms[i], v, k, xl, xb);
+    lb.put(sink, rice_bits(v, k), rice_len(v, k));
+    if (xl) lb.put(sink, xb, xl);
   }
   // lane partial words: head (started mid-word, completed) and tail (bits left)
   const bool has_tail = lb.nacc > 0 && nbits > 0;
@@ -416,6 +437,19 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
   }
 }
 
+// shared-memory bytes of one warp's LaneState for NL contexts
+__host__ __device__ constexpr size_t lane_state_bytes(int nl) { return (size_t)nl * 32 * (8 + 4 + 4 + 4 + 4); }
+
+__device__ __forceinline__ LaneState carve_state(uint8_t* p, int nl) {
+  LaneState ls;
+  ls.mc = reinterpret_cast<long long*>(p);
+  ls.ms = reinterpret_cast<int*>(p + (size_t)nl * 32 * 8);
+  ls.mt = ls.ms + nl * 32;
+  ls.a = ls.mt + nl * 32;
+  ls.nn = ls.a + nl * 32;
+  return ls;
+}
+
 // ---------------------------------------------------------------------------
 // Plane coder: tile = one row (encode_plane, _kernels.py:169-216)
 // ---------------------------------------------------------------------------
@@ -432,28 +466,17 @@ struct RowView {
   }
 };
 
-__device__ __forceinline__ int slice_transition(const RowView& rv, int x0, int x1, int st) {
-  for (int x = x0; x < x1; x++) {
-    int a, b, c;
-    rv.abc(x, a, b, c);
-    bool E = rv.cur[x] == a;
-    if (st == kFree && a == b && b == c) st = kInRun;
-    if (st == kInRun && E) continue;
-    st = kFree;
-  }
-  return st;
-}
-
-// grid-persistent; dynamic smem per warp: 2 row copies + 32 lane symbol lists
+// grid-persistent; dynamic smem per warp: 2 row copies + context state + 32 lane symbol lists
 __global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict__ descs, ChainTab ct, int row_bytes,
                                                        int lane_cap) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const size_t per_warp = 2 * (size_t)row_bytes + 32 * (size_t)lane_cap * sizeof(uint16_t);
+  const size_t per_warp = 2 * (size_t)row_bytes + lane_state_bytes(5) + 32 * (size_t)lane_cap * sizeof(uint16_t);
   uint8_t* wbase = smem_raw + warp * per_warp;
   uint8_t* srow_prev = wbase;
   uint8_t* srow_cur = wbase + row_bytes;
-  uint16_t* ssym = reinterpret_cast<uint16_t*>(wbase + 2 * row_bytes) + lane * lane_cap;
+  const LaneState ls = carve_state(wbase + 2 * row_bytes, 5);
+  uint16_t* ssym = reinterpret_cast<uint16_t*>(wbase + 2 * row_bytes + lane_state_bytes(5)) + lane * lane_cap;
   int chain;
   long long tin, g;
   while (next_tile(ct, &chain, &tin, &g)) {
@@ -462,38 +485,49 @@ __global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict
     const int y = (int)tin, W = d.w;
     const uint8_t* src = kind == 1 ? d.e_plane : d.res_planes + (long long)(kind - 2) * d.n;
     const uint8_t* gcur = src + (long long)y * W;
-    for (int x = lane; x < W; x += 32) {
-      srow_cur[x] = gcur[x];
-      if (y > 0) srow_prev[x] = gcur[x - W];
+    // stage the row and the row above (16-byte vectors when aligned)
+    if (((reinterpret_cast<uintptr_t>(gcur) | (uintptr_t)W) & 15) == 0) {
+      const uint4* c4 = reinterpret_cast<const uint4*>(gcur);
+      for (int q = lane; q < W / 16; q += 32) {
+        reinterpret_cast<uint4*>(srow_cur)[q] = __ldg(c4 + q);
+        if (y > 0) reinterpret_cast<uint4*>(srow_prev)[q] = __ldg(c4 + q - W / 16);
+      }
+    } else {
+      for (int x = lane; x < W; x += 32) {
+        srow_cur[x] = gcur[x];
+        if (y > 0) srow_prev[x] = gcur[x - W];
+      }
     }
     __syncwarp();
-    RowView rv{srow_cur, y > 0 ? srow_prev : nullptr};
+    const RowView rv{srow_cur, y > 0 ? srow_prev : nullptr};
     const int P = (W + 31) / 32;
     const int x0 = min(W, lane * P), x1 = min(W, x0 + P);
-    // automaton state entering each slice: compose the 3-state transition maps
-    int T = slice_transition(rv, x0, x1, kFree) | (slice_transition(rv, x0, x1, kForced) << 2) |
-            (slice_transition(rv, x0, x1, kInRun) << 4);
-    int comp = T;
+    // one sweep: the slice's transition for the 3 entry states + its leading E-ones
+    int s0 = kFree, s1 = kForced, s2 = kInRun, lead = 0;
+    bool leading = true;
+    for (int x = x0; x < x1; x++) {
+      int a, b, c;
+      rv.abc(x, a, b, c);
+      const bool E = rv.cur[x] == a, F = a == b && b == c;
+      if (leading && E) lead++; else leading = false;
+      s0 = (s0 == kFree && F) || s0 == kInRun ? (E ? kInRun : kFree) : kFree;
+      s1 = (s1 == kFree && F) || s1 == kInRun ? (E ? kInRun : kFree) : kFree;
+      s2 = (s2 == kFree && F) || s2 == kInRun ? (E ? kInRun : kFree) : kFree;
+    }
+    int comp = s0 | (s1 << 2) | (s2 << 4);
 #pragma unroll
     for (int dd = 1; dd < 32; dd <<= 1) {
       int o = __shfl_up_sync(0xffffffffu, comp, dd);
       if (lane >= dd) {
         int r = 0;
 #pragma unroll
-        for (int s = 0; s < 3; s++) r |= ((comp >> (2 * ((o >> (2 * s)) & 3))) & 3) << (2 * s);
+        for (int q = 0; q < 3; q++) r |= ((comp >> (2 * ((o >> (2 * q)) & 3))) & 3) << (2 * q);
         comp = r;
       }
     }
     const int excl = __shfl_up_sync(0xffffffffu, comp, 1);
     int st = lane == 0 ? kFree : (excl & 3);
     // run continuation into the next slices: leading E-ones, passing whole slices
-    int lead = 0;
-    for (int x = x0; x < x1; x++) {
-      int a, b, c;
-      rv.abc(x, a, b, c);
-      if (rv.cur[x] != a) break;
-      lead++;
-    }
     int val = lead;
     bool fl = lead == x1 - x0;
 #pragma unroll
@@ -561,7 +595,7 @@ __global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict
       atomicOr(d.status, kErrCapacity);
       n = lane_cap;
     }
-    run_tile<5, 5, PlaneSym>(ct, chain, tin, g, 0, ssym, n, cnt, d.status);
+    run_tile<5, 5, PlaneSym>(ct, chain, tin, g, 0, ssym, n, cnt, ls, d.status);
     __syncwarp();
   }
 }
@@ -570,9 +604,12 @@ __global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict
 // DCT coder: tile = 32 blocks of one component, lane = block (encode_dct_component)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) k_entropy_dct(const ImgDesc* __restrict__ descs, ChainTab ct) {
-  extern __shared__ __align__(16) uint32_t sbuf[];  // per warp, per lane symbol list (<= 127 per block)
+  extern __shared__ __align__(16) uint8_t smem_dct[];  // per warp: context state + 32 lane symbol lists
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* ssym = sbuf + (warp * 32 + lane) * kDctLaneCap;
+  const size_t per_warp = lane_state_bytes(3) + sizeof(uint32_t) * 32 * kDctLaneCap;
+  uint8_t* wbase = smem_dct + warp * per_warp;
+  const LaneState ls = carve_state(wbase, 3);
+  uint32_t* ssym = reinterpret_cast<uint32_t*>(wbase + lane_state_bytes(3)) + lane * kDctLaneCap;
   int chain;
   long long tin, g;
   while (next_tile(ct, &chain, &tin, &g)) {
@@ -627,7 +664,7 @@ __global__ void __launch_bounds__(128) k_entropy_dct(const ImgDesc* __restrict__
         pos = nz + 1;
       }
     }
-    run_tile<3, 6, DctSym>(ct, chain, tin, g, ci == 0 ? 0 : 3, ssym, n, cnt, d.status);
+    run_tile<3, 6, DctSym>(ct, chain, tin, g, ci == 0 ? 0 : 3, ssym, n, cnt, ls, d.status);
     __syncwarp();
   }
 }
@@ -684,7 +721,7 @@ static int num_sms() {
 
 void launch_entropy_dct(const ImgDesc* d_descs, const ChainTab& ct, cudaStream_t st) {
   if (ct.ntiles <= 0) return;
-  const size_t smem = sizeof(uint32_t) * 4 * 32 * kDctLaneCap;
+  const size_t smem = 4 * (lane_state_bytes(3) + sizeof(uint32_t) * 32 * kDctLaneCap);
   cudaFuncSetAttribute(k_entropy_dct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_entropy_dct, 128, smem);
@@ -698,8 +735,8 @@ void launch_entropy_plane(const ImgDesc* d_descs, const ChainTab& ct, int max_w,
   if (ct.ntiles <= 0) return;
   const int P = (max_w + 31) / 32;
   const int lane_cap = 2 * P + max_w / 255 + 4;
-  const int row_bytes = (max_w + 16) / 16 * 16;
-  size_t per_warp = 2 * (size_t)row_bytes + 32 * (size_t)lane_cap * sizeof(uint16_t);
+  const int row_bytes = (max_w + 31) / 16 * 16;
+  size_t per_warp = 2 * (size_t)row_bytes + lane_state_bytes(5) + 32 * (size_t)lane_cap * sizeof(uint16_t);
   int warps = (int)std::min<size_t>(4, (200 * 1024) / per_warp);
   if (warps < 1) warps = 1;
   size_t smem = per_warp * warps;
