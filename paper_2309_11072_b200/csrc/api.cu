@@ -55,7 +55,7 @@ struct ImgLayout {
   size_t off_logv, off_tmnodes, off_scalars;
   size_t off_sdr, off_s, off_zz;
   size_t off_sstar, off_sstar_tmp, off_e, off_res, off_mstar;
-  size_t off_tile_hist, off_order, off_bin_start, off_seg_nodes, off_seg_level, off_seg_node_off, off_dot, off_a32,
+  size_t off_tile_hist, off_xs, off_ys, off_bin_start, off_seg_nodes, off_seg_level, off_seg_node_off, off_dot, off_a32,
       off_b32;
   size_t off_crc, off_crc_part;
   size_t off_chain[5];
@@ -166,7 +166,8 @@ ImgLayout plan(const hdll_b200_image& im, bool trace) {
   L.off_mstar = trace ? take(3 * n) : 0;
   const long long sort_tiles = (n + kSortTile - 1) / kSortTile;
   L.off_tile_hist = take(sizeof(unsigned) * 256 * sort_tiles);
-  L.off_order = take(sizeof(unsigned) * n);
+  L.off_xs = take(sizeof(double) * 3 * n);
+  L.off_ys = take(3 * n + 16);
   L.off_bin_start = take(sizeof(unsigned) * 257);
   L.off_seg_nodes = take(sizeof(double) * max_seg_nodes(n));
   L.off_seg_level = take(sizeof(int) * 768);
@@ -366,7 +367,7 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   const size_t t_ticket = stage(nullptr, 16);
 
   long long max_n = 0, max_sort_tiles = 0, max_nodes = 0, max_out = 0;
-  int max_w = 0, max_h = 0, max_radius = 0, max_level = 0, max_base_tiles = 0;
+  int max_w = 0, max_h = 0, max_radius = 0, max_level = 0, max_base_tiles = 0, max_chunks = 1;
   bool any_real = false, any_slrme = false;
   for (int i = 0; i < n; i++) {
     const auto& im = imgs[i];
@@ -428,7 +429,8 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
     d.mstar = d.want_trace ? B + L.off_mstar : nullptr;
     d.sort_tiles = (int)((d.n + kSortTile - 1) / kSortTile);
     d.tile_hist = (unsigned*)(B + L.off_tile_hist);
-    d.order = (unsigned*)(B + L.off_order);
+    d.xs = (double*)(B + L.off_xs);
+    d.ys = B + L.off_ys;
     d.bin_start = (unsigned*)(B + L.off_bin_start);
     d.seg_nodes = (double*)(B + L.off_seg_nodes);
     d.seg_level = (int*)(B + L.off_seg_level);
@@ -457,6 +459,7 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
     max_level = std::max(max_level, d.tm_level);
     max_sort_tiles = std::max(max_sort_tiles, (long long)d.sort_tiles);
     max_nodes = std::max(max_nodes, max_seg_nodes(d.n));
+    max_chunks = std::max(max_chunks, std::min(d.blas_threads, kMaxBlasThreads));
     int tiles_x = (d.nbx + 15) / 16;
     max_base_tiles = std::max(max_base_tiles, tiles_x * d.nby);
     if (mode == 0) max_out = std::max(max_out, d.out_cap);
@@ -516,7 +519,7 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   }
   mark(kStPrefilter);
   if (mode == 0 && any_slrme) {
-    launch_fit(dd, n, (int)max_sort_tiles, max_nodes, st);
+    launch_fit(dd, n, (int)max_sort_tiles, max_nodes, max_chunks, st);
     c->launches += 7;
   }
   mark(kStFit);

@@ -63,7 +63,8 @@ struct ImgDesc {
   // SLRME fit
   int sort_tiles;             // tiles of kSortTile pixels
   unsigned* tile_hist;        // [sort_tiles][256] (then tile offsets)
-  unsigned* order;            // n: pixel indices stable-sorted by E
+  double* xs;                 // [3][n]: S* samples stable-sorted by E (raster order inside a bin)
+  uint8_t* ys;                // [3][n]: M samples in the same order
   unsigned* bin_count;        // 256
   unsigned* bin_start;        // 257
   long long* sum_y;           // [3][256] exact integer sums of M per bin
@@ -149,7 +150,7 @@ void upload_crc_constants();
 void launch_tonemap_stats(const ImgDesc*, int nimg, long long max_n, int max_level, cudaStream_t);
 void launch_base_layer(const ImgDesc*, int nimg, int max_tiles, cudaStream_t);
 void launch_prefilter(const ImgDesc*, int nimg, int max_w, int max_h, int max_radius, cudaStream_t);
-void launch_fit(const ImgDesc*, int nimg, int max_sort_tiles, long long max_nodes, cudaStream_t);
+void launch_fit(const ImgDesc*, int nimg, int max_sort_tiles, long long max_nodes, int max_chunks, cudaStream_t);
 void launch_estimate(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
 void launch_crc(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
 void launch_entropy_dct(const ImgDesc*, const ChainTab&, cudaStream_t);

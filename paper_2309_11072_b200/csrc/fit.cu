@@ -9,7 +9,8 @@
 //   degenerate fallback (0, sy/n)           (:163-169), then float32 RNE (:205-214).
 // With sigma > 0 S* is real-valued and the float sums are order dependent, so
 // the GPU follows the reference's order exactly:
-//   1. stable counting sort of pixel indices by E (raster order inside a bin);
+//   1. stable counting sort of the (S*, M) samples by E (raster order inside a bin),
+//      written contiguously so the sums below stream them;
 //   2. pairwise tree for sx (pairwise.cuh) over each bin's sorted samples;
 //   3. the OpenBLAS kernel's lane structure for sxx/sxy: 32 (SKYLAKEX) or 16
 //      (HASWELL) sequential FMA chains, its fold order, its tail, and the
@@ -32,22 +33,33 @@ __global__ void __launch_bounds__(256) k_sort_hist(const ImgDesc* __restrict__ d
   const int tile = blockIdx.x;
   if (tile >= d.sort_tiles) return;
   __shared__ unsigned hist[256];
-  __shared__ unsigned long long sy[3][256];
+  __shared__ unsigned sy[3][256];  // per tile <= 4096 * 255 < 2^20
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
     hist[i] = 0;
     sy[0][i] = sy[1][i] = sy[2][i] = 0;
   }
   __syncthreads();
   const long long p0 = (long long)tile * kSortTile;
-  const long long p1 = min(d.n, p0 + kSortTile);
   const uint32_t* px = reinterpret_cast<const uint32_t*>(d.rgbe);
-  for (long long p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
-    uint32_t q = px[p];
-    unsigned e = q >> 24;
-    atomicAdd(&hist[e], 1u);
-    atomicAdd(&sy[0][e], (unsigned long long)(q & 0xFF));
-    atomicAdd(&sy[1][e], (unsigned long long)((q >> 8) & 0xFF));
-    atomicAdd(&sy[2][e], (unsigned long long)((q >> 16) & 0xFF));
+  const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
+  for (int k = threadIdx.x; k < kSortTile; k += blockDim.x) {
+    const long long p = p0 + k;
+    const bool valid = p < d.n;
+    const unsigned act = __ballot_sync(0xffffffffu, valid);
+    if (!valid) continue;
+    const uint32_t q = px[p];
+    const unsigned e = q >> 24;
+    // warp-aggregated: one shared atomic per distinct exponent in the warp
+    const unsigned peers = __match_any_sync(act, e);
+    const unsigned s0 = __reduce_add_sync(peers, q & 0xFF);
+    const unsigned s1 = __reduce_add_sync(peers, (q >> 8) & 0xFF);
+    const unsigned s2 = __reduce_add_sync(peers, (q >> 16) & 0xFF);
+    if ((peers & lt) == 0) {
+      atomicAdd(&hist[e], (unsigned)__popc(peers));
+      atomicAdd(&sy[0][e], s0);
+      atomicAdd(&sy[1][e], s1);
+      atomicAdd(&sy[2][e], s2);
+    }
   }
   __syncthreads();
   for (int e = threadIdx.x; e < 256; e += blockDim.x) {
@@ -55,7 +67,7 @@ __global__ void __launch_bounds__(256) k_sort_hist(const ImgDesc* __restrict__ d
     if (hist[e]) {
       atomicAdd(&d.bin_count[e], hist[e]);
       for (int c = 0; c < 3; c++)
-        atomicAdd(reinterpret_cast<unsigned long long*>(&d.sum_y[c * 256 + e]), sy[c][e]);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&d.sum_y[c * 256 + e]), (unsigned long long)sy[c][e]);
     }
   }
 }
@@ -119,16 +131,23 @@ __global__ void __launch_bounds__(256) k_sort_scatter(const ImgDesc* __restrict_
     }
   }
   __syncthreads();
+  const bool real = d.sigma_milli != 0;
   for (int step = 0; step < kSortTile / 8 / 32; step++) {
     long long p = base + step * 32 + lane;
     bool valid = p < d.n;
     unsigned act = __ballot_sync(0xffffffffu, valid);
-    unsigned e = 0, peers = 0, pos = 0;
+    unsigned e = 0, peers = 0;
     if (valid) {
-      e = px[p] >> 24;
+      const uint32_t q = px[p];
+      e = q >> 24;
       peers = __match_any_sync(act, e);
-      pos = wcnt[w][e] + __popc(peers & lt);
-      d.order[pos] = (unsigned)p;
+      // global_regression fits whole planes in raster order: identity placement
+      const long long pos = d.global_regression ? p : (long long)wcnt[w][e] + __popc(peers & lt);
+#pragma unroll
+      for (int c = 0; c < 3; c++) {
+        d.xs[(long long)c * d.n + pos] = real ? d.sstar[(long long)c * d.n + p] : (double)d.s_planes[(long long)c * d.n + p];
+        d.ys[(long long)c * d.n + pos] = (uint8_t)((q >> (8 * c)) & 0xFF);
+      }
     }
     __syncwarp();
     if (valid && (peers & lt) == 0) wcnt[w][e] += __popc(peers);
@@ -159,23 +178,13 @@ __device__ __forceinline__ SegView seg_view(const ImgDesc& d, int s) {
   return v;
 }
 
-struct XAcc {  // x[i] = S*_c at the i-th sorted sample of a segment
-  const double* sf;
-  const uint8_t* s8;
-  const unsigned* ord;
-  __device__ double operator()(long long i) const {
-    long long p = ord ? (long long)ord[i] : i;
-    return sf ? sf[p] : (double)s8[p];
-  }
+struct XAcc {  // x[i] = S*_c of the i-th sample of a segment (contiguous after the sort)
+  const double* p;
+  __device__ __forceinline__ double operator()(long long i) const { return p[i]; }
 };
 
 __device__ __forceinline__ XAcc x_acc(const ImgDesc& d, int c, const SegView& v) {
-  XAcc a;
-  bool real = d.sigma_milli != 0;
-  a.sf = real ? d.sstar + (long long)c * d.n : nullptr;
-  a.s8 = real ? nullptr : d.s_planes + (long long)c * d.n;
-  a.ord = v.identity ? nullptr : d.order + v.off;
-  return a;
+  return XAcc{d.xs + (long long)c * d.n + v.off};
 }
 
 __global__ void k_seg_setup(const ImgDesc* __restrict__ descs) {
@@ -213,14 +222,9 @@ __global__ void __launch_bounds__(128) k_seg_nodes(const ImgDesc* __restrict__ d
 // 3. OpenBLAS ddot models (oracle/hdll_oracle.c ddot_compute), one warp per
 //    (segment, thread-chunk); both dots (x.x and x.y) in one sweep.
 // ---------------------------------------------------------------------------
-struct MAcc {  // y[i] = M_c (mantissa byte c of the RGBE quad) at the i-th sorted sample
-  const uint8_t* px;
-  const unsigned* ord;
-  int c;
-  __device__ double operator()(long long i) const {
-    long long p = ord ? (long long)ord[i] : i;
-    return (double)px[p * 4 + c];
-  }
+struct MAcc {  // y[i] = M_c of the i-th sample of a segment
+  const uint8_t* p;
+  __device__ __forceinline__ double operator()(long long i) const { return (double)p[i]; }
 };
 
 template <class XA, class YA>
@@ -317,8 +321,8 @@ __device__ void warp_ddot2(const XA& X, const YA& Y, long long start, long long 
   *out_xy = dxy;
 }
 
-// grid: (kSegs, nimg), blockDim = 32 * warps; warp j handles thread-chunk j
-__global__ void __launch_bounds__(256) k_seg_dot(const ImgDesc* __restrict__ descs) {
+// grid: (kSegs, nimg, max chunks); one warp per (segment, OpenBLAS thread-chunk)
+__global__ void __launch_bounds__(32) k_seg_dot(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
   if (!d.slrme) return;
   const int s = blockIdx.x;
@@ -326,10 +330,9 @@ __global__ void __launch_bounds__(256) k_seg_dot(const ImgDesc* __restrict__ des
   if (v.n == 0) return;
   const int c = s >> 8;
   const XAcc X = x_acc(d, c, v);
-  const MAcc M{d.rgbe, X.ord, c};
+  const MAcc M{d.ys + (long long)c * d.n + v.off};
   const int T = (v.n > 10000 && d.blas_threads > 1) ? min(d.blas_threads, kMaxBlasThreads) : 1;
-  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int j = warp; j < T; j += nw) {
+  for (int j = blockIdx.z; j < T; j += gridDim.z) {
     // chunk j of OpenBLAS's level-1 split: width = ceil(rem / (T - used))
     long long start = 0, rem = v.n, width = 0;
     for (int u = 0; u <= j; u++) {
@@ -402,13 +405,14 @@ __global__ void __launch_bounds__(256) k_seg_reduce_coef(const ImgDesc* __restri
   if (!isfinite(a32) || !isfinite(b32)) atomicOr(d.status, kErrNonFinite);
 }
 
-void launch_fit(const ImgDesc* d_descs, int nimg, int max_sort_tiles, long long max_nodes, cudaStream_t st) {
+void launch_fit(const ImgDesc* d_descs, int nimg, int max_sort_tiles, long long max_nodes, int max_chunks,
+                cudaStream_t st) {
   k_sort_hist<<<dim3(max_sort_tiles, nimg), 256, 0, st>>>(d_descs);
   k_sort_scan<<<nimg, 256, 0, st>>>(d_descs);
   k_sort_scatter<<<dim3(max_sort_tiles, nimg), 256, 0, st>>>(d_descs);
   k_seg_setup<<<nimg, 32, 0, st>>>(d_descs);
   k_seg_nodes<<<dim3((unsigned)((max_nodes + 127) / 128), nimg), 128, 0, st>>>(d_descs);
-  k_seg_dot<<<dim3(kSegs, nimg), 256, 0, st>>>(d_descs);
+  k_seg_dot<<<dim3(kSegs, nimg, max_chunks), 32, 0, st>>>(d_descs);
   k_seg_reduce_coef<<<dim3(kSegs, nimg), 256, 0, st>>>(d_descs);
 }
 

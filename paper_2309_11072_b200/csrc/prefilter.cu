@@ -64,7 +64,60 @@ __global__ void __launch_bounds__(256) k_prefilter_h(const ImgDesc* __restrict__
   d.sstar[(long long)c * d.n + (long long)y * d.w + x] = o;
 }
 
+// Fused single pass for radius <= kFusedMaxR: one CTA = kTH x kTW outputs of one
+// channel; the u8 input tile with its reflected halo and the vertical-pass
+// rows stay in shared memory; only S* is written.
+constexpr int kTH = 32, kTW = 64, kFusedMaxR = 16;
+
+__global__ void __launch_bounds__(256) k_prefilter_fused(const ImgDesc* __restrict__ descs) {
+  const ImgDesc& d = descs[blockIdx.z / 3];
+  const int c = blockIdx.z % 3;
+  if (!d.slrme || d.sigma_milli == 0 || d.radius > kFusedMaxR) return;
+  const int tiles_x = (d.w + kTW - 1) / kTW;
+  const int ty = blockIdx.x / tiles_x, tx = blockIdx.x % tiles_x;
+  const int y0 = ty * kTH, x0 = tx * kTW;
+  if (y0 >= d.h) return;
+  const int r = d.radius;
+  const int IW = kTW + 2 * r, IH = kTH + 2 * r;
+  __shared__ uint8_t in[(kTH + 2 * kFusedMaxR) * (kTW + 2 * kFusedMaxR)];
+  __shared__ double tmp[kTH * (kTW + 2 * kFusedMaxR)];
+  __shared__ double fw_s[2 * kFusedMaxR + 1];
+  const uint8_t* S = d.s_planes + (long long)c * d.n;
+  for (int i = threadIdx.x; i < 2 * r + 1; i += blockDim.x) fw_s[i] = d.taps[i];
+  for (int i = threadIdx.x; i < IH * IW; i += blockDim.x) {
+    const int ry = i / IW, rx = i % IW;
+    const int gy = reflect_idx((long long)y0 - r + ry, d.h), gx = reflect_idx((long long)x0 - r + rx, d.w);
+    in[i] = S[(long long)gy * d.w + gx];
+  }
+  __syncthreads();
+  const double* fw = fw_s + r;
+  // vertical pass (axis 0) for every staged column
+  for (int i = threadIdx.x; i < kTH * IW; i += blockDim.x) {
+    const int oy = i / IW, col = i % IW;
+    const uint8_t* cp = in + (oy + r) * IW + col;
+    double o = (double)cp[0] * fw[0];
+    for (int jj = -r; jj < 0; jj++) o += ((double)cp[jj * IW] + (double)cp[-jj * IW]) * fw[jj];
+    tmp[oy * IW + col] = o;
+  }
+  __syncthreads();
+  // horizontal pass (axis 1)
+  for (int i = threadIdx.x; i < kTH * kTW; i += blockDim.x) {
+    const int oy = i / kTW, ox = i % kTW;
+    const int y = y0 + oy, x = x0 + ox;
+    if (y >= d.h || x >= d.w) continue;
+    const double* rp = tmp + oy * IW + ox + r;
+    double o = rp[0] * fw[0];
+    for (int jj = -r; jj < 0; jj++) o += (rp[jj] + rp[-jj]) * fw[jj];
+    d.sstar[(long long)c * d.n + (long long)y * d.w + x] = o;
+  }
+}
+
 void launch_prefilter(const ImgDesc* d_descs, int nimg, int max_w, int max_h, int max_radius, cudaStream_t st) {
+  if (max_radius <= kFusedMaxR) {
+    const int tiles = ((max_w + kTW - 1) / kTW) * ((max_h + kTH - 1) / kTH);
+    k_prefilter_fused<<<dim3(tiles, 1, nimg * 3), 256, 0, st>>>(d_descs);
+    return;
+  }
   k_prefilter_v<<<dim3((max_w + 127) / 128, max_h, nimg * 3), 128, 0, st>>>(d_descs);
   size_t smem = sizeof(double) * (256 + 2 * (size_t)max_radius);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_prefilter_h, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
