@@ -69,7 +69,7 @@ enum { kStTonemap, kStBase, kStPrefilter, kStFit, kStEstimate, kStCrc, kStEntrop
 
 constexpr size_t kEstatPerTile = 16 + 16 * kMaxCtx + sizeof(AMap) * kMaxCtx + 4 * kMaxCtx + 16 + 8;
 
-constexpr size_t kZeroBytes = 8 /*maxlw*/ + 8 /*status*/ + 1024 /*bin_count*/ + 8 * 768 /*sum_y*/;
+constexpr size_t kZeroBytes = 8 /*maxlw*/ + 8 /*status, amb*/ + 1024 /*bin_count*/ + 8 * 768 /*sum_y*/;
 
 struct Ctx {
   int device = 0;
@@ -413,6 +413,7 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
     d.crc_mask = mode == 0 ? 0x1F : (mode == 1 ? 0x2 : 0x1);
     d.maxlw = (unsigned long long*)(B + L.off_zero);
     d.status = (unsigned*)(B + L.off_zero + 8);
+    d.amb = (unsigned*)(B + L.off_zero + 12);
     d.bin_count = (unsigned*)(B + L.off_zero + 16);
     d.sum_y = (long long*)(B + L.off_zero + 16 + 1024);
     d.logv = (double*)(B + L.off_logv);

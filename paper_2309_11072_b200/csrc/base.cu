@@ -31,9 +31,33 @@ __device__ __forceinline__ double rgbe_scale_b(unsigned e) {
   return __longlong_as_double((long long)((int)e - 136 + 1023) << 52);
 }
 
+// srgb_quantize(pow(m, g)) = round_half_away(255 * clip(m^g, 0, 1)) for m >= 0.
+// The quantised byte only depends on which side of k + 0.5 the product lies,
+// so it is first evaluated in fp32 (log2f 1 ulp, exp2f 2 ulp: |err(255 m^g)|
+// < 2e-4 for g <= 50) and accepted when 255 m^g + 0.5 is more than kAmb away
+// from an integer; otherwise the fp64 pow decides (as numpy's does; numpy's
+// own power is SVML, not correctly rounded).
+constexpr float kAmb = 2e-3f;
+
+__device__ __noinline__ uint8_t quantize_pow_exact(double m, double g) {
+  double v = pow(m, g);
+  return (uint8_t)rha(255.0 * clampd(v, 0.0, 1.0));
+}
+
+__device__ __forceinline__ uint8_t quantize_pow(double m, double g, float g32, unsigned* amb) {
+  if (m >= 1.0) return 255;  // m^g >= 1 clips to 1
+  if (m <= 0.0) return 0;
+  const float y = 255.0f * exp2f(g32 * log2f(__double2float_rn(m)));
+  const float yf = y + 0.5f;
+  const float fl = floorf(yf), fr = yf - fl;
+  if (fr > kAmb && fr < 1.0f - kAmb) return (uint8_t)fl;
+  (*amb)++;
+  return quantize_pow_exact(m, g);
+}
+
 // tone_map pass B for one pixel -> 3 SDR bytes
 __device__ __forceinline__ void sdr_pixel(const ImgDesc& d, uint32_t q, double log_avg, double white, bool allzero,
-                                          uint8_t* out3) {
+                                          uint8_t* out3, unsigned* amb) {
   if (allzero || q == 0u) {
     out3[0] = out3[1] = out3[2] = 0;
     return;
@@ -47,13 +71,9 @@ __device__ __forceinline__ void sdr_pixel(const ImgDesc& d, uint32_t q, double l
   double scaled = d.key * lw / log_avg;
   double disp = scaled * (1.0 + scaled / (white * white)) / (1.0 + scaled);
   double ratio = lw > 0 ? disp / lw : 0.0;
+  const float g32 = (float)d.inv_gamma;
 #pragma unroll
-  for (int c = 0; c < 3; c++) {
-    double mapped = f[c] * ratio;
-    double v = pow(fmax(mapped, 0.0), d.inv_gamma);
-    double x = 255.0 * clampd(v, 0.0, 1.0);
-    out3[c] = (uint8_t)rha(x);
-  }
+  for (int c = 0; c < 3; c++) out3[c] = quantize_pow(fmax(f[c] * ratio, 0.0), d.inv_gamma, g32, amb);
 }
 
 __global__ void __launch_bounds__(128) k_base_layer(const ImgDesc* __restrict__ descs) {
@@ -74,6 +94,7 @@ __global__ void __launch_bounds__(128) k_base_layer(const ImgDesc* __restrict__ 
   const bool allzero = d.sdr_in ? false : d.scalars[3] != 0.0;
 
   // 1. SDR (tone-map pass B) and YCC for every padded pixel of the tile
+  unsigned amb = 0;  // samples the fp32 pow could not certify
   for (int p = t; p < 8 * kTileCols; p += blockDim.x) {
     int ry = p / kTileCols, rx = p % kTileCols;
     if (rx >= nblk * 8) continue;
@@ -85,7 +106,7 @@ __global__ void __launch_bounds__(128) k_base_layer(const ImgDesc* __restrict__ 
       s3[0] = sp[0], s3[1] = sp[1], s3[2] = sp[2];
     } else {
       uint32_t q = reinterpret_cast<const uint32_t*>(d.rgbe)[(long long)sy * d.w + sx];
-      sdr_pixel(d, q, log_avg, white, allzero, s3);
+      sdr_pixel(d, q, log_avg, white, allzero, s3, &amb);
     }
     if (d.want_trace && y < d.h && x < d.w) {
       uint8_t* o = d.sdr + ((long long)y * d.w + x) * 3;
@@ -101,6 +122,7 @@ __global__ void __launch_bounds__(128) k_base_layer(const ImgDesc* __restrict__ 
     bufA[(1 * 8 + ry) * kRowStride + rx] = clampd(rha(cb), -128.0, 127.0);
     bufA[(2 * 8 + ry) * kRowStride + rx] = clampd(rha(cr), -128.0, 127.0);
   }
+  if (amb) atomicAdd(d.amb, amb);
   __syncthreads();
 
   // task t: block b = t / 8, line l = t % 8, for each of the 3 components

@@ -94,6 +94,7 @@ struct ImgDesc {
   const uint8_t* hdr_post;    // u32 length + header text block
   int hdr_post_len;
   unsigned* status;           // error bits
+  unsigned* amb;              // tone-map samples decided by the fp64 pow (diagnostic)
 };
 
 constexpr int kMaxBlasThreads = 64;

@@ -406,34 +406,43 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
     lb.put(sink, rice_bits(v, k), rice_len(v, k));
     if (xl) lb.put(sink, xb, xl);
   }
-  // lane partial words: head (started mid-word, completed) and tail (bits left)
+  // Lane partial words.  A lane that starts mid-word owes its first word to the
+  // carry of the lanes before it; a lane whose bits sit inside one word
+  // ("single") passes the carry on OR-ed with its bits.  The carry is a
+  // composition of maps x -> x | m (single / empty lanes) and x -> t (lanes
+  // ending mid-word), scanned in log2(32) steps.
   const bool has_tail = lb.nacc > 0 && nbits > 0;
   const uint32_t tail = has_tail ? (uint32_t)(lb.acc << (32 - lb.nacc)) : 0u;
-  const long long tail_word = lb.wpos;
-  const bool single = has_tail && tail_word == lb.first && lb.head_partial;
-  long long cw = -1;
-  uint32_t cb = 0;
-#pragma unroll 1
-  for (int l = 0; l < 32; l++) {
-    long long ncw = cw;
-    uint32_t ncb = cb;
-    if (lane == l && nbits > 0) {
-      if (single) {
-        ncw = lb.first;
-        ncb = (cw == lb.first ? cb : 0u) | tail;
-      } else {
-        if (lb.have_head) sink.write(lb.first, (cw == lb.first ? cb : 0u) | lb.head);
-        ncw = has_tail ? tail_word : -1;
-        ncb = has_tail ? tail : 0u;
-      }
+  const bool single = has_tail && lb.wpos == lb.first && lb.head_partial;
+  // f_l: constant (word, bits) for lanes ending mid-word / aligned (word -1),
+  // or x -> x | bits into word `fw` for single lanes, identity (word -2) if empty
+  bool c_const = nbits > 0 && !single;
+  uint32_t c_val = has_tail ? tail : 0u;
+  long long c_word = nbits == 0 ? -2 : (single ? lb.first : (has_tail ? lb.wpos : -1));
+#pragma unroll
+  for (int dd = 1; dd < 32; dd <<= 1) {
+    const bool o_const = __shfl_up_sync(0xffffffffu, c_const, dd);
+    const uint32_t o_val = __shfl_up_sync(0xffffffffu, c_val, dd);
+    const long long o_word = __shfl_up_sync(0xffffffffu, c_word, dd);
+    if (lane >= dd && !c_const) {  // compose: earlier (o) then this (c)
+      c_val |= o_val;
+      c_const = o_const;
+      if (c_word == -2) c_word = o_word;
     }
-    cw = __shfl_sync(0xffffffffu, ncw, l);
-    cb = __shfl_sync(0xffffffffu, ncb, l);
   }
+  if (c_word == -2) c_word = -1;  // applied to "no carry"
+  // exclusive carry entering this lane
+  uint32_t in_val = __shfl_up_sync(0xffffffffu, c_val, 1);
+  long long in_word = __shfl_up_sync(0xffffffffu, c_word, 1);
+  if (lane == 0) in_val = 0u, in_word = -1;
+  if (nbits > 0 && !single && lb.have_head)
+    sink.write(lb.first, (in_word == lb.first ? in_val : 0u) | lb.head);
   // the tile's last partial word: parked for the fix-up pass (a later tile may add bits)
-  if (lane == 0 && cw >= 0) {
-    if (cw == sink.tile_first_word && sink.tile_start_partial) sink.edge[0] = cb;
-    else sink.edge[1] = cb;
+  const uint32_t out_val = __shfl_sync(0xffffffffu, c_val, 31);
+  const long long out_word = __shfl_sync(0xffffffffu, c_word, 31);
+  if (lane == 0 && out_word >= 0) {
+    if (out_word == sink.tile_first_word && sink.tile_start_partial) sink.edge[0] = out_val;
+    else sink.edge[1] = out_val;
   }
 }
 

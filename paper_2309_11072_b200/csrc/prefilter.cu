@@ -69,6 +69,61 @@ __global__ void __launch_bounds__(256) k_prefilter_h(const ImgDesc* __restrict__
 // rows stay in shared memory; only S* is written.
 constexpr int kTH = 32, kTW = 64, kFusedMaxR = 16;
 
+struct PfSmem {
+  uint8_t in[(kTH + 2 * kFusedMaxR) * (kTW + 2 * kFusedMaxR)];
+  double tmp[kTH * (kTW + 2 * kFusedMaxR)];
+  double fw_s[2 * kFusedMaxR + 1];
+  int gys[kTH + 2 * kFusedMaxR], gxs[kTW + 2 * kFusedMaxR];
+};
+
+template <int R>  // R > 0: compile-time radius; R == 0: runtime d.radius
+__device__ __forceinline__ void prefilter_tile(const ImgDesc& d, int c, int y0, int x0, PfSmem& sm) {
+  const int r = R > 0 ? R : d.radius;
+  const int IW = kTW + 2 * r, IH = kTH + 2 * r;
+  uint8_t* in = sm.in;
+  double* tmp = sm.tmp;
+  double* fw_s = sm.fw_s;
+  int* gys = sm.gys;
+  int* gxs = sm.gxs;
+  const uint8_t* S = d.s_planes + (long long)c * d.n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  for (int i = threadIdx.x; i < 2 * r + 1; i += blockDim.x) fw_s[i] = d.taps[i];
+  for (int i = threadIdx.x; i < IH; i += blockDim.x) gys[i] = reflect_idx((long long)y0 - r + i, d.h);
+  for (int i = threadIdx.x; i < IW; i += blockDim.x) gxs[i] = reflect_idx((long long)x0 - r + i, d.w);
+  __syncthreads();
+  for (int ry = warp; ry < IH; ry += nwarp) {
+    const uint8_t* srow = S + (long long)gys[ry] * d.w;
+    for (int rx = lane; rx < IW; rx += 32) in[ry * IW + rx] = srow[gxs[rx]];
+  }
+  __syncthreads();
+  const double* fw = fw_s + r;
+  // vertical pass (axis 0) for every staged column
+  for (int oy = warp; oy < kTH; oy += nwarp) {
+    for (int col = lane; col < IW; col += 32) {
+      const uint8_t* cp = in + (oy + r) * IW + col;
+      double o = (double)cp[0] * fw[0];
+#pragma unroll
+      for (int jj = -r; jj < 0; jj++) o += ((double)cp[jj * IW] + (double)cp[-jj * IW]) * fw[jj];
+      tmp[oy * IW + col] = o;
+    }
+  }
+  __syncthreads();
+  // horizontal pass (axis 1)
+  for (int oy = warp; oy < kTH; oy += nwarp) {
+    const int y = y0 + oy;
+    if (y >= d.h) break;
+    for (int ox = lane; ox < kTW; ox += 32) {
+      const int x = x0 + ox;
+      if (x >= d.w) break;
+      const double* rp = tmp + oy * IW + ox + r;
+      double o = rp[0] * fw[0];
+#pragma unroll
+      for (int jj = -r; jj < 0; jj++) o += (rp[jj] + rp[-jj]) * fw[jj];
+      d.sstar[(long long)c * d.n + (long long)y * d.w + x] = o;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_prefilter_fused(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.z / 3];
   const int c = blockIdx.z % 3;
@@ -77,39 +132,9 @@ __global__ void __launch_bounds__(256) k_prefilter_fused(const ImgDesc* __restri
   const int ty = blockIdx.x / tiles_x, tx = blockIdx.x % tiles_x;
   const int y0 = ty * kTH, x0 = tx * kTW;
   if (y0 >= d.h) return;
-  const int r = d.radius;
-  const int IW = kTW + 2 * r, IH = kTH + 2 * r;
-  __shared__ uint8_t in[(kTH + 2 * kFusedMaxR) * (kTW + 2 * kFusedMaxR)];
-  __shared__ double tmp[kTH * (kTW + 2 * kFusedMaxR)];
-  __shared__ double fw_s[2 * kFusedMaxR + 1];
-  const uint8_t* S = d.s_planes + (long long)c * d.n;
-  for (int i = threadIdx.x; i < 2 * r + 1; i += blockDim.x) fw_s[i] = d.taps[i];
-  for (int i = threadIdx.x; i < IH * IW; i += blockDim.x) {
-    const int ry = i / IW, rx = i % IW;
-    const int gy = reflect_idx((long long)y0 - r + ry, d.h), gx = reflect_idx((long long)x0 - r + rx, d.w);
-    in[i] = S[(long long)gy * d.w + gx];
-  }
-  __syncthreads();
-  const double* fw = fw_s + r;
-  // vertical pass (axis 0) for every staged column
-  for (int i = threadIdx.x; i < kTH * IW; i += blockDim.x) {
-    const int oy = i / IW, col = i % IW;
-    const uint8_t* cp = in + (oy + r) * IW + col;
-    double o = (double)cp[0] * fw[0];
-    for (int jj = -r; jj < 0; jj++) o += ((double)cp[jj * IW] + (double)cp[-jj * IW]) * fw[jj];
-    tmp[oy * IW + col] = o;
-  }
-  __syncthreads();
-  // horizontal pass (axis 1)
-  for (int i = threadIdx.x; i < kTH * kTW; i += blockDim.x) {
-    const int oy = i / kTW, ox = i % kTW;
-    const int y = y0 + oy, x = x0 + ox;
-    if (y >= d.h || x >= d.w) continue;
-    const double* rp = tmp + oy * IW + ox + r;
-    double o = rp[0] * fw[0];
-    for (int jj = -r; jj < 0; jj++) o += (rp[jj] + rp[-jj]) * fw[jj];
-    d.sstar[(long long)c * d.n + (long long)y * d.w + x] = o;
-  }
+  __shared__ PfSmem sm;
+  if (d.radius == 3) prefilter_tile<3>(d, c, y0, x0, sm);  // sigma 1.0 (the default)
+  else prefilter_tile<0>(d, c, y0, x0, sm);
 }
 
 void launch_prefilter(const ImgDesc* d_descs, int nimg, int max_w, int max_h, int max_radius, cudaStream_t st) {
