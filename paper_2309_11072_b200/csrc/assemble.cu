@@ -65,8 +65,38 @@ __global__ void __launch_bounds__(256) k_assemble(const ImgDesc* __restrict__ de
   }
   __syncthreads();
   const long long total = min(L.total, d.out_cap);
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
+  // payload bit streams: the bulk, copied 16 bytes at a time (funnel shifts
+  // re-align the 4-byte aligned source to the byte offset in the stream)
+  const long long nthreads = (long long)gridDim.x * blockDim.x;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int k = 0; k < 5; k++) {
+    const uint8_t* src = k == 0 ? at.dct_out[img] : at.plane_out[img * 4 + k - 1];
+    const long long dst0 = L.pay[k] + 17, len = L.body_len[k] - 8;
+    // head bytes up to a 16-byte aligned destination, then aligned 16-byte chunks
+    const long long head = min(len, (16 - ((long long)(reinterpret_cast<uintptr_t>(d.out) + dst0) & 15)) & 15);
+    for (long long i = tid; i < head; i += nthreads)
+      if (dst0 + i < total) d.out[dst0 + i] = src[i];
+    const long long nvec = (len - head) / 16;
+    for (long long v = tid; v < nvec; v += nthreads) {
+      const long long so = head + v * 16;  // source byte offset
+      const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src + (so & ~3LL));
+      const int sh = (int)(so & 3);
+      uint32_t w[5];
+#pragma unroll
+      for (int q = 0; q < 5; q++) w[q] = (q < 4 || sh) ? s4[q] : 0u;
+      uint4 o;
+      // little-endian byte stream: byte b of the output = source byte so + b
+      o.x = __funnelshift_r(w[0], w[1], 8 * sh);
+      o.y = __funnelshift_r(w[1], w[2], 8 * sh);
+      o.z = __funnelshift_r(w[2], w[3], 8 * sh);
+      o.w = __funnelshift_r(w[3], w[4], 8 * sh);
+      if (dst0 + so + 16 <= total) *reinterpret_cast<uint4*>(d.out + dst0 + so) = o;
+    }
+    for (long long i = head + nvec * 16 + tid; i < len; i += nthreads)
+      if (dst0 + i < total) d.out[dst0 + i] = src[i];
+  }
+  // everything else (headers, table, frames): byte by byte
+  for (long long i = tid; i < total; i += nthreads) {
     uint8_t v;
     if (i < L.tab) {
       v = d.hdr_pre[i];
@@ -105,8 +135,12 @@ __global__ void __launch_bounds__(256) k_assemble(const ImgDesc* __restrict__ de
       int k = 4;
       while (i < L.pay[k]) k--;
       long long r = i - L.pay[k];
-      if (r < 17) v = frame[k][r];
-      else v = (k == 0 ? at.dct_out[img] : at.plane_out[img * 4 + k - 1])[r - 17];
+      if (r >= 17) {  // bit-stream bytes were written above
+        long long skip = L.pay[k] + 9 + L.body_len[k] - i;  // jump to the next frame
+        i += skip - 1 - ((skip - 1) % nthreads);
+        continue;
+      }
+      v = frame[k][r];
     }
     d.out[i] = v;
   }

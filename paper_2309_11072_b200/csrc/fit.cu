@@ -33,11 +33,7 @@ __global__ void __launch_bounds__(256) k_sort_hist(const ImgDesc* __restrict__ d
   const int tile = blockIdx.x;
   if (tile >= d.sort_tiles) return;
   __shared__ unsigned hist[256];
-  __shared__ unsigned sy[3][256];  // per tile <= 4096 * 255 < 2^20
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-    hist[i] = 0;
-    sy[0][i] = sy[1][i] = sy[2][i] = 0;
-  }
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
   __syncthreads();
   const long long p0 = (long long)tile * kSortTile;
   const uint32_t* px = reinterpret_cast<const uint32_t*>(d.rgbe);
@@ -47,28 +43,15 @@ __global__ void __launch_bounds__(256) k_sort_hist(const ImgDesc* __restrict__ d
     const bool valid = p < d.n;
     const unsigned act = __ballot_sync(0xffffffffu, valid);
     if (!valid) continue;
-    const uint32_t q = px[p];
-    const unsigned e = q >> 24;
+    const unsigned e = px[p] >> 24;
     // warp-aggregated: one shared atomic per distinct exponent in the warp
     const unsigned peers = __match_any_sync(act, e);
-    const unsigned s0 = __reduce_add_sync(peers, q & 0xFF);
-    const unsigned s1 = __reduce_add_sync(peers, (q >> 8) & 0xFF);
-    const unsigned s2 = __reduce_add_sync(peers, (q >> 16) & 0xFF);
-    if ((peers & lt) == 0) {
-      atomicAdd(&hist[e], (unsigned)__popc(peers));
-      atomicAdd(&sy[0][e], s0);
-      atomicAdd(&sy[1][e], s1);
-      atomicAdd(&sy[2][e], s2);
-    }
+    if ((peers & lt) == 0) atomicAdd(&hist[e], (unsigned)__popc(peers));
   }
   __syncthreads();
   for (int e = threadIdx.x; e < 256; e += blockDim.x) {
     d.tile_hist[(long long)tile * 256 + e] = hist[e];
-    if (hist[e]) {
-      atomicAdd(&d.bin_count[e], hist[e]);
-      for (int c = 0; c < 3; c++)
-        atomicAdd(reinterpret_cast<unsigned long long*>(&d.sum_y[c * 256 + e]), (unsigned long long)sy[c][e]);
-    }
+    if (hist[e]) atomicAdd(&d.bin_count[e], hist[e]);
   }
 }
 
@@ -345,9 +328,15 @@ __global__ void __launch_bounds__(32) k_seg_dot(const ImgDesc* __restrict__ desc
     }
     double xx, xy;
     warp_ddot2(X, M, start, width, d.blas_kernel, &xx, &xy);
+    // y.sum() is an exact integer sum (estimator.py:160): any order
+    unsigned long long sy = 0;
+    for (long long i = start + (threadIdx.x & 31); i < start + width; i += 32) sy += M.p[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sy += __shfl_xor_sync(0xffffffffu, sy, o);
     if ((threadIdx.x & 31) == 0) {
       d.dot_part[((long long)s * kMaxBlasThreads + j) * 2 + 0] = xx;
       d.dot_part[((long long)s * kMaxBlasThreads + j) * 2 + 1] = xy;
+      atomicAdd(reinterpret_cast<unsigned long long*>(&d.sum_y[s]), sy);
     }
   }
 }
@@ -366,12 +355,7 @@ __global__ void __launch_bounds__(256) k_seg_reduce_coef(const ImgDesc* __restri
   if (threadIdx.x != 0) return;
   sx = 0.0 + sx;
   const int c = s >> 8;
-  long long sy_i = 0;
-  if (d.global_regression) {
-    for (int e = 0; e < 256; e++) sy_i += d.sum_y[c * 256 + e];
-  } else {
-    sy_i = d.sum_y[s];
-  }
+  const long long sy_i = d.sum_y[s];  // global_regression: the (c, 0) segment spans the whole plane
   const double sy = (double)sy_i;
   const int T = (v.n > 10000 && d.blas_threads > 1) ? min(d.blas_threads, kMaxBlasThreads) : 1;
   double sxx = 0.0, sxy = 0.0;
