@@ -160,42 +160,63 @@ struct LaneBits {
 };
 
 // ---------------------------------------------------------------------------
-// Symbol formats in shared memory (k is filled in by the length pass)
-//   plane: u16 = k << 11 | ctx << 8 | value
-//   dct  : u32 = xb << 17 | k << 13 | xl << 9 | lctx << 7 | value
-//          (value <= 64, raw bits xl <= 13: |DC diff| <= 4080 and |AC| <= 2040
-//           for an orthonormal 8x8 DCT of 8-bit samples)
+// Symbol sources.  A generator enumerates a lane's symbols in coder order as
+// f(index, ctx, value, raw_len, raw_bits).  The plane coder keeps its symbols
+// in shared memory (u16: k << 11 | ctx << 8 | value) and records k there in the
+// length pass; the DCT coder re-derives them from the block each pass and the
+// emit pass re-runs the context state to recover k.
 // ---------------------------------------------------------------------------
-struct PlaneSym {
-  typedef uint16_t T;
-  static __device__ __forceinline__ void dec(T s, int& c, int& v) {
-    c = (s >> 8) & 7;
-    v = s & 0xFF;
+struct PlaneList {
+  static constexpr bool kStoresK = true;
+  uint16_t* syms;
+  int n;
+  template <class F>
+  __device__ __forceinline__ void for_each(F&& f) const {
+    for (int i = 0; i < n; i++) {
+      const uint16_t s = syms[i];
+      f(i, (s >> 8) & 7, s & 0xFF, 0, 0u);
+    }
   }
-  static __device__ __forceinline__ T with_k(T s, int k) { return (T)(s | (k << 11)); }
-  static __device__ __forceinline__ void dec_emit(T s, int& v, int& k, int& xl, uint32_t& xb) {
-    v = s & 0xFF;
-    k = s >> 11;
-    xl = 0;
-    xb = 0;
+  __device__ __forceinline__ void set_k(int i, int k) const { syms[i] = (uint16_t)(syms[i] | (k << 11)); }
+  template <class F>
+  __device__ __forceinline__ void for_each_k(F&& f) const {  // f(value, k, raw_len, raw_bits)
+    for (int i = 0; i < n; i++) {
+      const uint16_t s = syms[i];
+      f(s & 0xFF, s >> 11, 0, 0u);
+    }
   }
 };
-struct DctSym {
-  typedef uint32_t T;
-  static __device__ __forceinline__ T enc(int c, int v, int xl, uint32_t xb) {
-    return (xb << 17) | ((uint32_t)xl << 9) | ((uint32_t)c << 7) | (uint32_t)v;
+
+// One 8x8 block of zigzag coefficients (encode_dct_component, _kernels.py:280-324):
+// DC size (ctx 0) + raw bits, then per nonzero AC (zero run ctx 1, size ctx 2 +
+// raw bits), EOB = run 64 unless position 63 is coded.
+struct DctBlockGen {
+  static constexpr bool kStoresK = false;
+  const int16_t* z;  // nullptr: idle lane
+  unsigned long long nzm;
+  unsigned dcu;      // interleaved DC difference
+  template <class F>
+  __device__ __forceinline__ void for_each(F&& f) const {
+    if (!z) return;
+    int s = dcu ? 32 - __clz(dcu) : 0;
+    f(0, 0, s, s, dcu);
+    int pos = 1, i = 1;
+    while (pos < 64) {
+      const unsigned long long rest = nzm >> pos;
+      if (rest == 0) {
+        f(i, 1, kEOB, 0, 0u);
+        break;
+      }
+      const int nz = pos + __ffsll((long long)rest) - 1;
+      f(i++, 1, nz - pos, 0, 0u);
+      const int zv = z[nz];
+      const unsigned u = zv >= 0 ? 2u * zv : (unsigned)(-2 * zv - 1);
+      s = 32 - __clz(u);
+      f(i++, 2, s, s, u);
+      pos = nz + 1;
+    }
   }
-  static __device__ __forceinline__ void dec(T s, int& c, int& v) {
-    v = s & 0x7F;
-    c = (s >> 7) & 3;
-  }
-  static __device__ __forceinline__ T with_k(T s, int k) { return s | ((uint32_t)k << 13); }
-  static __device__ __forceinline__ void dec_emit(T s, int& v, int& k, int& xl, uint32_t& xb) {
-    v = s & 0x7F;
-    xl = (s >> 9) & 15;
-    k = (s >> 13) & 15;
-    xb = s >> 17;
-  }
+  __device__ __forceinline__ void set_k(int, int) const {}
 };
 
 // Per-lane context state lives in shared memory, [context][lane], so a symbol
@@ -213,9 +234,9 @@ struct LaneState {
 //   NL local contexts used by the tile, mapped to chain contexts base..base+NL-1,
 //   NC contexts carried by the chain.
 // ---------------------------------------------------------------------------
-template <int NL, int NC, class S>
-__device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long g, int base,
-                         typename S::T* syms, int nsym, const int* cnt_in, const LaneState& ls, unsigned* status) {
+template <int NL, int NC, class Gen>
+__device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long g, int base, const Gen& gen,
+                         const int* cnt_in, const LaneState& ls, unsigned* status) {
   const int lane = threadIdx.x & 31;
   const bool chain_start = tin == 0;
 
@@ -266,9 +287,7 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
     ls.mt[c * 32 + lane] = 0;
     ls.nn[c * 32 + lane] = n0[c];
   }
-  for (int i = 0; i < nsym; i++) {
-    int c, v;
-    S::dec(syms[i], c, v);
+  gen.for_each([&](int, int c, int v, int, uint32_t) {
     const int o = c * 32 + lane;
     const int nb = ls.nn[o];
     const int h = nb == kStateReset - 1;  // N reaches 64: A and N halve
@@ -284,7 +303,7 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
       ls.ms[o] = m.s;
       ls.mt[o] = m.t;
     }
-  }
+  });
   AMap pre[NL], agg[NL];
 #pragma unroll 1
   for (int c = 0; c < NL; c++) {
@@ -335,23 +354,19 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
     publish(ct, g, 1, 2);
   }
 
-  // ---- 3. code lengths; k of every symbol is stored for the emit pass ----
+  // ---- 3. code lengths (k of every symbol is kept for the emit pass when the generator can) ----
+  int a_start[NL];
 #pragma unroll
   for (int c = 0; c < NL; c++) {
-    ls.a[c * 32 + lane] = (int)amap_apply(pre[c], __shfl_sync(0xffffffffu, ain[base + c], 0));
+    a_start[c] = (int)amap_apply(pre[c], __shfl_sync(0xffffffffu, ain[base + c], 0));
+    ls.a[c * 32 + lane] = a_start[c];
     ls.nn[c * 32 + lane] = n0[c];
   }
   long long nbits = 0;
-  for (int i = 0; i < nsym; i++) {
-    typename S::T sy = syms[i];
-    int c, v;
-    S::dec(sy, c, v);
+  gen.for_each([&](int i, int c, int v, int xl, uint32_t) {
     const int o = c * 32 + lane;
     int a = ls.a[o], nb = ls.nn[o];
     const int k = kfast(a, nb);
-    int xl, kk, vv;
-    uint32_t xb;
-    S::dec_emit(sy, vv, kk, xl, xb);
     nbits += rice_len(v, k) + xl;
     a += v;  // _update_state
     nb += 1;
@@ -361,8 +376,8 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
     }
     ls.a[o] = a;
     ls.nn[o] = nb;
-    syms[i] = S::with_k(sy, k);
-  }
+    gen.set_k(i, k);
+  });
   long long tbits;
   const long long loff = warp_excl_sum(nbits, &tbits);
   long long toff = 0;
@@ -399,12 +414,32 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
   sink.status = status;
   LaneBits lb;
   lb.init(toff + loff);
-  for (int i = 0; i < nsym; i++) {
-    int v, k, xl;
-    uint32_t xb;
-    S::dec_emit(syms[i], v, k, xl, xb);
-    lb.put(sink, rice_bits(v, k), rice_len(v, k));
-    if (xl) lb.put(sink, xb, xl);
+  if constexpr (Gen::kStoresK) {
+    gen.for_each_k([&](int v, int k, int xl, uint32_t xb) {
+      lb.put(sink, rice_bits(v, k), rice_len(v, k));
+      if (xl) lb.put(sink, xb, xl);
+    });
+  } else {
+#pragma unroll
+    for (int c = 0; c < NL; c++) {
+      ls.a[c * 32 + lane] = a_start[c];
+      ls.nn[c * 32 + lane] = n0[c];
+    }
+    gen.for_each([&](int, int c, int v, int xl, uint32_t xb) {
+      const int o = c * 32 + lane;
+      int a = ls.a[o], nb = ls.nn[o];
+      const int k = kfast(a, nb);
+      a += v;
+      nb += 1;
+      if (nb >= kStateReset) {
+        a >>= 1;
+        nb >>= 1;
+      }
+      ls.a[o] = a;
+      ls.nn[o] = nb;
+      lb.put(sink, rice_bits(v, k), rice_len(v, k));
+      if (xl) lb.put(sink, xb, xl);
+    });
   }
   // Lane partial words.  A lane that starts mid-word owes its first word to the
   // carry of the lanes before it; a lane whose bits sit inside one word
@@ -475,7 +510,7 @@ struct RowView {
   }
 };
 
-// grid-persistent; dynamic smem per warp: 2 row copies + context state + 32 lane symbol lists
+// grid-persistent; dynamic smem per warp: context state + 32 lane symbol lists
 __global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict__ descs, ChainTab ct, int row_bytes,
                                                        int lane_cap) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -604,21 +639,18 @@ __global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict
       atomicOr(d.status, kErrCapacity);
       n = lane_cap;
     }
-    run_tile<5, 5, PlaneSym>(ct, chain, tin, g, 0, ssym, n, cnt, ls, d.status);
+    run_tile<5, 5>(ct, chain, tin, g, 0, PlaneList{ssym, n}, cnt, ls, d.status);
     __syncwarp();
   }
 }
 
 // ---------------------------------------------------------------------------
-// DCT coder: tile = 32 blocks of one component, lane = block (encode_dct_component)
+// DCT coder: tile = 32 blocks of one component, lane = block
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) k_entropy_dct(const ImgDesc* __restrict__ descs, ChainTab ct) {
-  extern __shared__ __align__(16) uint8_t smem_dct[];  // per warp: context state + 32 lane symbol lists
+  __shared__ __align__(16) uint8_t smem_dct[4 * lane_state_bytes(3)];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const size_t per_warp = lane_state_bytes(3) + sizeof(uint32_t) * 32 * kDctLaneCap;
-  uint8_t* wbase = smem_dct + warp * per_warp;
-  const LaneState ls = carve_state(wbase, 3);
-  uint32_t* ssym = reinterpret_cast<uint32_t*>(wbase + lane_state_bytes(3)) + lane * kDctLaneCap;
+  const LaneState ls = carve_state(smem_dct + warp * lane_state_bytes(3), 3);
   int chain;
   long long tin, g;
   while (next_tile(ct, &chain, &tin, &g)) {
@@ -626,7 +658,7 @@ __global__ void __launch_bounds__(128) k_entropy_dct(const ImgDesc* __restrict__
     const long long tpc = (d.nblocks + 31) / 32;
     const int ci = (int)(tin / tpc);
     const long long bi = (tin % tpc) * 32 + lane;
-    int n = 0;
+    DctBlockGen gen{nullptr, 0ULL, 0u};
     int cnt[3] = {0, 0, 0};
     if (bi < d.nblocks) {
       const int16_t* z = d.zz + ((long long)ci * d.nblocks + bi) * 64;
@@ -647,33 +679,16 @@ __global__ void __launch_bounds__(128) k_entropy_dct(const ImgDesc* __restrict__
       }
       nzm &= ~1ULL;
       const int prev_dc = bi > 0 ? d.zz[((long long)ci * d.nblocks + bi - 1) * 64] : 0;
-      // DC: size s of the interleaved difference (ctx 0) + s raw bits
-      int dv = dc - prev_dc;
-      unsigned u = dv >= 0 ? 2u * dv : (unsigned)(-2 * dv - 1);
-      int s = u ? 32 - __clz(u) : 0;
-      ssym[n++] = DctSym::enc(0, s, s, u);
-      cnt[0]++;
-      // AC: (zero run ctx 1, size ctx 2 + raw bits), EOB = run 64 unless position 63 is coded
-      int pos = 1;
-      while (pos < 64) {
-        unsigned long long rest = nzm >> pos;
-        if (rest == 0) {
-          ssym[n++] = DctSym::enc(1, kEOB, 0, 0u);
-          cnt[1]++;
-          break;
-        }
-        int nz = pos + __ffsll((long long)rest) - 1;
-        ssym[n++] = DctSym::enc(1, nz - pos, 0, 0u);
-        cnt[1]++;
-        int zv = z[nz];
-        u = zv >= 0 ? 2u * zv : (unsigned)(-2 * zv - 1);
-        s = 32 - __clz(u);
-        ssym[n++] = DctSym::enc(2, s, s, u);
-        cnt[2]++;
-        pos = nz + 1;
-      }
+      const int dv = dc - prev_dc;
+      gen.z = z;
+      gen.nzm = nzm;
+      gen.dcu = dv >= 0 ? 2u * dv : (unsigned)(-2 * dv - 1);
+      const int nnz = __popcll(nzm);
+      cnt[0] = 1;
+      cnt[1] = nnz + ((nzm >> 63) ? 0 : 1);  // runs + EOB (absent when position 63 is coded)
+      cnt[2] = nnz;
     }
-    run_tile<3, 6, DctSym>(ct, chain, tin, g, ci == 0 ? 0 : 3, ssym, n, cnt, ls, d.status);
+    run_tile<3, 6>(ct, chain, tin, g, ci == 0 ? 0 : 3, gen, cnt, ls, d.status);
     __syncwarp();
   }
 }
@@ -730,14 +745,12 @@ static int num_sms() {
 
 void launch_entropy_dct(const ImgDesc* d_descs, const ChainTab& ct, cudaStream_t st) {
   if (ct.ntiles <= 0) return;
-  const size_t smem = 4 * (lane_state_bytes(3) + sizeof(uint32_t) * 32 * kDctLaneCap);
-  cudaFuncSetAttribute(k_entropy_dct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_entropy_dct, 128, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_entropy_dct, 128, 0);
   long long blocks = (long long)num_sms() * (per_sm > 0 ? per_sm : 1);
   long long need = (ct.ntiles + 3) / 4;
   if (blocks > need) blocks = need;
-  k_entropy_dct<<<(unsigned)blocks, 128, smem, st>>>(d_descs, ct);
+  k_entropy_dct<<<(unsigned)blocks, 128, 0, st>>>(d_descs, ct);
 }
 
 void launch_entropy_plane(const ImgDesc* d_descs, const ChainTab& ct, int max_w, cudaStream_t st) {
