@@ -153,8 +153,10 @@ def main() -> int:
         sigma=0.0)
 
     np.savez_compressed(HERE / "inputs.npz", **inputs)
+    from hdll.rgbe import float_to_rgbe
+    f2r = sha(float_to_rgbe(synth.config1_scene(1000, 135, 240)))  # pins synth.float_to_rgbe
     out = {"generator": "tests/golden/make_golden.py", "reference": "/root/reference/pkg (hdll 0.1.0)",
-           "numpy": np.__version__, "blas": blas, "cases": cases}
+           "numpy": np.__version__, "blas": blas, "cases": cases, "float_to_rgbe_sha256": f2r}
     (HERE / "golden.json").write_text(json.dumps(out, indent=1) + "\n")
     shutil.rmtree(scratch, ignore_errors=True)
     print(f"wrote {len(cases)} cases, {len(inputs)} stored inputs")
