@@ -148,7 +148,7 @@ ImgLayout plan(const hdll_b200_image& im, bool trace) {
     return r;
   };
   L.off_zero = take(kZeroBytes);
-  L.off_qt = take(128 * sizeof(double));
+  L.off_qt = take(256 * sizeof(double));
   L.off_taps = take(sizeof(double) * (2 * (size_t)std::max(0, im.params.radius) + 1));
   L.off_pre = take(im.hdr_pre_len + 1);
   L.off_post = take(im.hdr_post_len + 1);
@@ -325,7 +325,7 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   std::vector<ImgDesc> ds(n);
   size_t stage_bytes = (size_t)n * 4 * kAlign;  // per-image alignment padding of the 4 staged blocks
   for (int i = 0; i < n; i++)
-    stage_bytes += 128 * 8 + 8 * (2 * (size_t)std::max(0, imgs[i].params.radius) + 1) + imgs[i].hdr_pre_len +
+    stage_bytes += 256 * 8 + 8 * (2 * (size_t)std::max(0, imgs[i].params.radius) + 1) + imgs[i].hdr_pre_len +
                    imgs[i].hdr_post_len;
   // sequential-coder chains: the DCT stream of every image (kind 0) and its 4
   // plane streams (kinds 1..4), each family driven by its own kernel
@@ -396,8 +396,9 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
     d.white_point = p.tmo_white_point;
     d.inv_gamma = p.tmo_inv_gamma;
     d.epsilon = p.tmo_epsilon;
-    double qt[128];
+    double qt[256];  // luma, chroma, then their reciprocals (for the certified quantiser)
     quant_tables(p.quality, qt);
+    for (int k = 0; k < 128; k++) qt[128 + k] = 1.0 / qt[k];
     size_t s_qt = stage(qt, sizeof(qt));
     size_t s_taps = stage(p.taps, (p.slrme && p.sigma_milli) ? 8 * (2 * (size_t)p.radius + 1) : 0);
     size_t s_pre = stage(im.hdr_pre, im.hdr_pre_len);

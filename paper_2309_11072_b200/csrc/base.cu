@@ -55,28 +55,32 @@ __device__ __forceinline__ uint8_t quantize_pow(double m, double g, float g32, u
   return quantize_pow_exact(m, g);
 }
 
-// tone_map pass B for one pixel -> 3 SDR bytes
-__device__ __forceinline__ void sdr_pixel(const ImgDesc& d, uint32_t q, double log_avg, double white, bool allzero,
-                                          uint8_t* out3, unsigned* amb) {
+// tone_map pass B for one pixel -> 3 SDR bytes (fp64 chain of the reference,
+// tonemap.py:102-110; the gamma step through quantize_pow)
+struct TmoConst {
+  float g32;  // 1 / gamma
+};
+
+__device__ __forceinline__ void sdr_pixel(const ImgDesc& d, uint32_t q, double log_avg, double white,
+                                          const TmoConst& tc, bool allzero, uint8_t* out3, unsigned* amb) {
   if (allzero || q == 0u) {
     out3[0] = out3[1] = out3[2] = 0;
     return;
   }
-  double sc = rgbe_scale_b(q >> 24);
+  const double sc = rgbe_scale_b(q >> 24);
   double f[3];
   f[0] = ((double)(q & 0xFF) + 0.5) * sc;
   f[1] = ((double)((q >> 8) & 0xFF) + 0.5) * sc;
   f[2] = ((double)((q >> 16) & 0xFF) + 0.5) * sc;
-  double lw = 0.2126 * f[0] + 0.7152 * f[1] + 0.0722 * f[2];
-  double scaled = d.key * lw / log_avg;
-  double disp = scaled * (1.0 + scaled / (white * white)) / (1.0 + scaled);
-  double ratio = lw > 0 ? disp / lw : 0.0;
-  const float g32 = (float)d.inv_gamma;
+  const double lw = 0.2126 * f[0] + 0.7152 * f[1] + 0.0722 * f[2];
+  const double scaled = d.key * lw / log_avg;
+  const double disp = scaled * (1.0 + scaled / (white * white)) / (1.0 + scaled);
+  const double ratio = lw > 0 ? disp / lw : 0.0;
 #pragma unroll
-  for (int c = 0; c < 3; c++) out3[c] = quantize_pow(fmax(f[c] * ratio, 0.0), d.inv_gamma, g32, amb);
+  for (int c = 0; c < 3; c++) out3[c] = quantize_pow(fmax(f[c] * ratio, 0.0), d.inv_gamma, tc.g32, amb);
 }
 
-__global__ void __launch_bounds__(128) k_base_layer(const ImgDesc* __restrict__ descs) {
+__global__ void __launch_bounds__(128, 4) k_base_layer(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
   const int tiles_x = (d.nbx + kTileBlocks - 1) / kTileBlocks;
   const int tile = blockIdx.x;
@@ -90,8 +94,10 @@ __global__ void __launch_bounds__(128) k_base_layer(const ImgDesc* __restrict__ 
   double* bufB = smem + 3 * 8 * kRowStride;  // [3][8][kRowStride]
   const int t = threadIdx.x;
 
-  const double log_avg = d.sdr_in ? 0.0 : d.scalars[1], white = d.sdr_in ? 0.0 : d.scalars[2];
+  const double log_avg = d.sdr_in ? 1.0 : d.scalars[1], white = d.sdr_in ? 1.0 : d.scalars[2];
   const bool allzero = d.sdr_in ? false : d.scalars[3] != 0.0;
+  TmoConst tc;
+  tc.g32 = (float)d.inv_gamma;
 
   // 1. SDR (tone-map pass B) and YCC for every padded pixel of the tile
   unsigned amb = 0;  // samples the fp32 pow could not certify
@@ -106,7 +112,7 @@ __global__ void __launch_bounds__(128) k_base_layer(const ImgDesc* __restrict__ 
       s3[0] = sp[0], s3[1] = sp[1], s3[2] = sp[2];
     } else {
       uint32_t q = reinterpret_cast<const uint32_t*>(d.rgbe)[(long long)sy * d.w + sx];
-      sdr_pixel(d, q, log_avg, white, allzero, s3, &amb);
+      sdr_pixel(d, q, log_avg, white, tc, allzero, s3, &amb);
     }
     if (d.want_trace && y < d.h && x < d.w) {
       uint8_t* o = d.sdr + ((long long)y * d.w + x) * 3;
@@ -132,7 +138,7 @@ __global__ void __launch_bounds__(128) k_base_layer(const ImgDesc* __restrict__ 
 
   // 2. forward pass 1 (dct_blocks first loop): tmp[u][x] = sum_t C[u][t] * blk[t][x], x = l
   if (live) {
-#pragma unroll
+#pragma unroll 1
     for (int ci = 0; ci < 3; ci++) {
       double in[8];
 #pragma unroll
@@ -151,7 +157,7 @@ __global__ void __launch_bounds__(128) k_base_layer(const ImgDesc* __restrict__ 
   // 3. forward pass 2: out[u][v] = sum_t tmp[u][t] * C[v][t], u = l; quantise, zigzag, dequantise
   const long long bi = (long long)by * d.nbx + bx0 + b;
   if (live) {
-#pragma unroll
+#pragma unroll 1
     for (int ci = 0; ci < 3; ci++) {
       const double* qt = d.qt + (ci == 0 ? 0 : 64);
       double in[8];
@@ -163,8 +169,8 @@ __global__ void __launch_bounds__(128) k_base_layer(const ImgDesc* __restrict__ 
         double s = 0.0;
 #pragma unroll
         for (int tt = 0; tt < 8; tt++) s += in[tt] * c_dct[v * 8 + tt];
-        double qv = qt[l * 8 + v];
-        double qz = rha(s / qv);
+        const double qv = qt[l * 8 + v];
+        const double qz = rha(s / qv);  // B200 fp64 division is cheaper than a certified reciprocal
         zz[c_zigzag[l * 8 + v]] = (int16_t)qz;
         bufA[(ci * 8 + l) * kRowStride + col0 + v] = qz * qv;  // dequantised coefficient
       }
@@ -174,7 +180,7 @@ __global__ void __launch_bounds__(128) k_base_layer(const ImgDesc* __restrict__ 
 
   // 4. inverse pass 1 (idct_blocks first loop): tmp[x][v] = sum_t C[t][x] * coef[t][v], v = l
   if (live) {
-#pragma unroll
+#pragma unroll 1
     for (int ci = 0; ci < 3; ci++) {
       double in[8];
 #pragma unroll
@@ -192,7 +198,7 @@ __global__ void __launch_bounds__(128) k_base_layer(const ImgDesc* __restrict__ 
 
   // 5. inverse pass 2: out[x][y] = sum_t tmp[x][t] * C[t][y], x = l
   if (live) {
-#pragma unroll
+#pragma unroll 1
     for (int ci = 0; ci < 3; ci++) {
       double in[8];
 #pragma unroll

@@ -34,7 +34,7 @@ struct ImgDesc {
   int want_trace;
   double key, white_point /* <=0: auto */, inv_gamma, epsilon;
   const double* taps;   // 2*radius+1 taps computed on the host with numpy (estimator.py:120-127)
-  const double* qt;     // 128 doubles: luma[64] then chroma[64], natural order
+  const double* qt;     // 256 doubles: luma[64], chroma[64] (natural order), then their reciprocals
 
   // input
   const uint8_t* rgbe;  // (h, w, 4), 16-byte aligned
@@ -98,7 +98,7 @@ struct ImgDesc {
 };
 
 constexpr int kMaxBlasThreads = 64;
-constexpr int kSortTile = 4096;
+constexpr int kSortTile = 2048;
 constexpr int kCrcChunk = 1024;       // bytes per CRC partial
 constexpr int kNodeTarget = 1024;     // pairwise-sum level-L node size target
 

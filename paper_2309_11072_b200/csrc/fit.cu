@@ -81,60 +81,112 @@ __global__ void __launch_bounds__(256) k_sort_scan(const ImgDesc* __restrict__ d
   }
 }
 
+// Stable placement: within a tile the samples are first ranked and staged in
+// shared memory in bin order, then written out so that consecutive threads
+// store consecutive positions of a bin (coalesced).
+struct ScatterSmem {
+  unsigned wcnt[8][256];
+  unsigned loc_off[257];
+  unsigned g_off[256];
+  double xs[3][kSortTile];
+  uint8_t ys[3][kSortTile];
+  uint8_t es[kSortTile];
+};
+
 __global__ void __launch_bounds__(256) k_sort_scatter(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
   if (!d.slrme) return;
   const int tile = blockIdx.x;
   if (tile >= d.sort_tiles) return;
-  __shared__ unsigned wcnt[8][256];
+  extern __shared__ __align__(16) uint8_t sm_raw[];
+  ScatterSmem& sm = *reinterpret_cast<ScatterSmem*>(sm_raw);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&wcnt[0][0])[i] = 0;
-  __syncthreads();
-  const long long base = (long long)tile * kSortTile + (long long)w * (kSortTile / 8);
+  const long long t0 = (long long)tile * kSortTile;
+  const int tn = (int)min((long long)kSortTile, d.n - t0);
   const uint32_t* px = reinterpret_cast<const uint32_t*>(d.rgbe);
+  const bool real = d.sigma_milli != 0;
+  if (d.global_regression) {  // whole planes in raster order: identity placement
+    for (int k = threadIdx.x; k < tn; k += blockDim.x) {
+      const long long p = t0 + k;
+      const uint32_t q = px[p];
+#pragma unroll
+      for (int c = 0; c < 3; c++) {
+        d.xs[(long long)c * d.n + p] = real ? d.sstar[(long long)c * d.n + p] : (double)d.s_planes[(long long)c * d.n + p];
+        d.ys[(long long)c * d.n + p] = (uint8_t)((q >> (8 * c)) & 0xFF);
+      }
+    }
+    return;
+  }
+  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&sm.wcnt[0][0])[i] = 0;
+  __syncthreads();
+  constexpr int kPerWarp = kSortTile / 8;
+  const int wb = w * kPerWarp;
   const unsigned lt = (1u << lane) - 1u;
-  for (int step = 0; step < kSortTile / 8 / 32; step++) {
-    long long p = base + step * 32 + lane;
-    bool valid = p < d.n;
-    unsigned act = __ballot_sync(0xffffffffu, valid);
+  for (int step = 0; step < kPerWarp / 32; step++) {
+    const int k = wb + step * 32 + lane;
+    const bool valid = k < tn;
+    const unsigned act = __ballot_sync(0xffffffffu, valid);
     if (valid) {
-      unsigned e = px[p] >> 24;
-      unsigned peers = __match_any_sync(act, e);
-      if ((peers & lt) == 0) wcnt[w][e] += __popc(peers);
+      const unsigned e = px[t0 + k] >> 24;
+      const unsigned peers = __match_any_sync(act, e);
+      if ((peers & lt) == 0) sm.wcnt[w][e] += __popc(peers);
     }
   }
   __syncthreads();
-  {
+  {  // bin offsets inside the tile, per-warp bases, absolute bin offsets of the tile
     const int e = threadIdx.x;
-    unsigned run = d.tile_hist[(long long)tile * 256 + e];
+    unsigned tot = 0;
+    for (int k = 0; k < 8; k++) tot += sm.wcnt[k][e];
+    unsigned wtot;
+    unsigned ex = warp_excl_sum(tot, &wtot);
+    __shared__ unsigned wsum[8];
+    if (lane == 31) wsum[w] = ex + tot;
+    __syncthreads();
+    unsigned pre = 0;
+    for (int k = 0; k < w; k++) pre += wsum[k];
+    const unsigned off = pre + ex;
+    sm.loc_off[e] = off;
+    if (e == 255) sm.loc_off[256] = off + tot;
+    sm.g_off[e] = d.tile_hist[(long long)tile * 256 + e];
+    unsigned run = off;
     for (int k = 0; k < 8; k++) {
-      unsigned c = wcnt[k][e];
-      wcnt[k][e] = run;
+      unsigned c = sm.wcnt[k][e];
+      sm.wcnt[k][e] = run;
       run += c;
     }
   }
   __syncthreads();
-  const bool real = d.sigma_milli != 0;
-  for (int step = 0; step < kSortTile / 8 / 32; step++) {
-    long long p = base + step * 32 + lane;
-    bool valid = p < d.n;
-    unsigned act = __ballot_sync(0xffffffffu, valid);
+  for (int step = 0; step < kPerWarp / 32; step++) {
+    const int k = wb + step * 32 + lane;
+    const bool valid = k < tn;
+    const unsigned act = __ballot_sync(0xffffffffu, valid);
     unsigned e = 0, peers = 0;
     if (valid) {
+      const long long p = t0 + k;
       const uint32_t q = px[p];
       e = q >> 24;
       peers = __match_any_sync(act, e);
-      // global_regression fits whole planes in raster order: identity placement
-      const long long pos = d.global_regression ? p : (long long)wcnt[w][e] + __popc(peers & lt);
+      const unsigned slot = sm.wcnt[w][e] + __popc(peers & lt);
 #pragma unroll
       for (int c = 0; c < 3; c++) {
-        d.xs[(long long)c * d.n + pos] = real ? d.sstar[(long long)c * d.n + p] : (double)d.s_planes[(long long)c * d.n + p];
-        d.ys[(long long)c * d.n + pos] = (uint8_t)((q >> (8 * c)) & 0xFF);
+        sm.xs[c][slot] = real ? d.sstar[(long long)c * d.n + p] : (double)d.s_planes[(long long)c * d.n + p];
+        sm.ys[c][slot] = (uint8_t)((q >> (8 * c)) & 0xFF);
       }
+      sm.es[slot] = (uint8_t)e;
     }
     __syncwarp();
-    if (valid && (peers & lt) == 0) wcnt[w][e] += __popc(peers);
+    if (valid && (peers & lt) == 0) sm.wcnt[w][e] += __popc(peers);
     __syncwarp();
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < tn; q += blockDim.x) {
+    const unsigned e = sm.es[q];
+    const long long gpos = (long long)sm.g_off[e] + (q - sm.loc_off[e]);
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      d.xs[(long long)c * d.n + gpos] = sm.xs[c][q];
+      d.ys[(long long)c * d.n + gpos] = sm.ys[c][q];
+    }
   }
 }
 
@@ -184,10 +236,13 @@ __global__ void k_seg_setup(const ImgDesc* __restrict__ descs) {
   d.seg_node_off[kSegs] = off;
 }
 
+// one warp per depth-L node of a segment's pairwise tree
 __global__ void __launch_bounds__(128) k_seg_nodes(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
   if (!d.slrme) return;
-  long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ double leaves[4][kMaxLeaves];
+  const int warp = threadIdx.x >> 5;
+  const long long g = (long long)blockIdx.x * 4 + warp;
   if (g >= d.seg_node_off[kSegs]) return;
   int lo = 0, hi = kSegs;  // find s with off[s] <= g < off[s+1]
   while (hi - lo > 1) {
@@ -198,7 +253,8 @@ __global__ void __launch_bounds__(128) k_seg_nodes(const ImgDesc* __restrict__ d
   SegView v = seg_view(d, s);
   long long off, sz;
   pairwise_node(v.n, d.seg_level[s], g - d.seg_node_off[s], &off, &sz);
-  d.seg_nodes[g] = pairwise_seq(x_acc(d, s >> 8, v), off, sz);
+  const double r = warp_pairwise(x_acc(d, s >> 8, v), off, sz, leaves[warp]);
+  if ((threadIdx.x & 31) == 0) d.seg_nodes[g] = r;
 }
 
 // ---------------------------------------------------------------------------
@@ -393,9 +449,10 @@ void launch_fit(const ImgDesc* d_descs, int nimg, int max_sort_tiles, long long 
                 cudaStream_t st) {
   k_sort_hist<<<dim3(max_sort_tiles, nimg), 256, 0, st>>>(d_descs);
   k_sort_scan<<<nimg, 256, 0, st>>>(d_descs);
-  k_sort_scatter<<<dim3(max_sort_tiles, nimg), 256, 0, st>>>(d_descs);
+  cudaFuncSetAttribute(k_sort_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ScatterSmem));
+  k_sort_scatter<<<dim3(max_sort_tiles, nimg), 256, sizeof(ScatterSmem), st>>>(d_descs);
   k_seg_setup<<<nimg, 32, 0, st>>>(d_descs);
-  k_seg_nodes<<<dim3((unsigned)((max_nodes + 127) / 128), nimg), 128, 0, st>>>(d_descs);
+  k_seg_nodes<<<dim3((unsigned)((max_nodes + 3) / 4), nimg), 128, 0, st>>>(d_descs);
   k_seg_dot<<<dim3(kSegs, nimg, max_chunks), 32, 0, st>>>(d_descs);
   k_seg_reduce_coef<<<dim3(kSegs, nimg), 256, 0, st>>>(d_descs);
 }

@@ -69,6 +69,85 @@ __device__ double pairwise_seq(const Acc& a, long long off, long long n) {
   }
 }
 
+// One warp sums one pairwise subtree [off, off + n) exactly as pairwise_seq:
+// the leaves (n <= 128) are found by the same recursion and summed four at a
+// time by groups of 8 lanes -- lane j of a group is numpy's accumulator r[j],
+// so every addition happens in numpy's order -- then lane 0 combines the leaf
+// sums along the recursion tree.  Result in every lane.
+constexpr int kMaxLeaves = 160;  // n <= 8192
+
+static __device__ __noinline__ double pairwise_combine(const double* leaf, int* li, long long m) {
+  if (m <= 128) return leaf[(*li)++];
+  long long n2 = m / 2;
+  n2 -= n2 % 8;
+  double left = pairwise_combine(leaf, li, n2);
+  return left + pairwise_combine(leaf, li, m - n2);
+}
+
+template <class Acc>
+__device__ double warp_pairwise(const Acc& a, long long off, long long n, double* leaf_buf /* kMaxLeaves */) {
+  const int lane = threadIdx.x & 31, grp = lane >> 3, j = lane & 7;
+  long long st_off[24], st_n[24];
+  int sp = 0, nleaf = 0, nb = 0;
+  long long boff[4], bn[4];
+  st_off[0] = off;
+  st_n[0] = n;
+  sp = 1;
+  auto flush = [&]() {
+    const bool mine = grp < nb;
+    const long long lo = mine ? boff[grp] : 0, ln = mine ? bn[grp] : 0;
+    const long long lim = ln - (ln % 8);
+    double r = 0.0;
+    if (mine && ln >= 8) {
+      r = a(lo + j);
+      for (long long i = 8; i < lim; i += 8) r += a(lo + i + j);
+    }
+    const double p2 = r + __shfl_down_sync(0xffffffffu, r, 1);    // r0+r1, r2+r3, ...
+    const double q4 = p2 + __shfl_down_sync(0xffffffffu, p2, 2);  // (r0+r1)+(r2+r3), ...
+    const double s8 = q4 + __shfl_down_sync(0xffffffffu, q4, 4);  // ((..)+(..))+((..)+(..))
+    if (mine && j == 0) {
+      double res;
+      if (ln < 8) {
+        res = 0.0;
+        for (long long i = 0; i < ln; i++) res += a(lo + i);
+      } else {
+        res = s8;
+        for (long long i = lim; i < ln; i++) res += a(lo + i);
+      }
+      leaf_buf[nleaf - nb + grp] = res;
+    }
+    nb = 0;
+  };
+  while (sp > 0) {  // depth first, left to right: leaves come out in order
+    sp--;
+    const long long o = st_off[sp], m = st_n[sp];
+    if (m <= 128) {
+      boff[nb] = o;
+      bn[nb] = m;
+      nb++;
+      nleaf++;
+      if (nb == 4) flush();
+    } else {
+      long long n2 = m / 2;
+      n2 -= n2 % 8;
+      st_off[sp] = o + n2;
+      st_n[sp] = m - n2;
+      sp++;
+      st_off[sp] = o;
+      st_n[sp] = n2;
+      sp++;
+    }
+  }
+  if (nb) flush();
+  __syncwarp();
+  double out = 0.0;
+  if (lane == 0) {
+    int li = 0;
+    out = pairwise_combine(leaf_buf, &li, n);
+  }
+  return __shfl_sync(0xffffffffu, out, 0);
+}
+
 // Perfect-binary-tree sum of vals[0 .. 2^L) by one CTA (blockDim.x = 256).
 // Returns the result in thread 0.
 __device__ __forceinline__ double tree_reduce_block(const double* vals, int L, double* smem /*256*/) {
