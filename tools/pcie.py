@@ -1,0 +1,21 @@
+"""Measure pinned H2D / D2H bandwidth and their overlap on this box."""
+import time, torch
+dev = torch.device('cuda', 0)
+n = 512 << 20
+h = torch.empty(n, dtype=torch.uint8).pin_memory()
+h2 = torch.empty(n, dtype=torch.uint8).pin_memory()
+d = torch.empty(n, dtype=torch.uint8, device=dev)
+d2 = torch.empty(n, dtype=torch.uint8, device=dev)
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+for _ in range(2):
+    d.copy_(h, non_blocking=True); h2.copy_(d2, non_blocking=True)
+torch.cuda.synchronize()
+def t(f):
+    torch.cuda.synchronize(); t0 = time.perf_counter(); f(); torch.cuda.synchronize(); return time.perf_counter() - t0
+a = t(lambda: d.copy_(h, non_blocking=True))
+b = t(lambda: h2.copy_(d2, non_blocking=True))
+def both():
+    with torch.cuda.stream(s1): d.copy_(h, non_blocking=True)
+    with torch.cuda.stream(s2): h2.copy_(d2, non_blocking=True)
+c = t(both)
+print(f"H2D {n/a/1e9:.1f} GB/s  D2H {n/b/1e9:.1f} GB/s  both {2*n/c/1e9:.1f} GB/s total")
