@@ -86,6 +86,55 @@ __device__ __forceinline__ void publish(const ChainTab& ct, long long g, int whi
   st_release(ct.flags + g * 4 + which, (ct.epoch << 2) | state);
 }
 
+// Warp-parallel look-back: lane l probes predecessor tile j0 - l (>= jmin).
+// Waits until every valid tile of the window has published phase `which`;
+// returns the lowest lane holding an inclusive prefix (32 if none) and the
+// lane's own state (0 outside the chain, 1 aggregate, 2 inclusive).
+__device__ __forceinline__ int probe_window(const ChainTab& ct, long long j0, long long jmin, int which,
+                                            unsigned* status, int* my_state) {
+  const int lane = threadIdx.x & 31;
+  const long long j = j0 - lane;
+  const bool valid = j >= jmin;
+  const int* f = ct.flags + (valid ? j : 0) * 4 + which;
+  int st = 0;
+  for (long long it = 0;; it++) {
+    if (valid && st == 0) {
+      const int v = ld_acquire(f);
+      if ((v >> 2) == ct.epoch && (v & 3)) st = v & 3;
+    }
+    if (__all_sync(0xffffffffu, !valid || st != 0)) break;
+    if (it > kSpinLimit) {
+      if (lane == 0) atomicOr(status, kErrLookback);
+      if (valid && st == 0) st = 2;  // give up: treat as a (garbage) prefix, never hang
+      break;
+    }
+    __nanosleep(20);
+  }
+  *my_state = valid ? st : 0;
+  const unsigned incl = __ballot_sync(0xffffffffu, valid && st == 2);
+  return incl ? __ffs(incl) - 1 : 32;
+}
+
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// composition of the lanes' maps, oldest (highest lane) first; result in every lane
+__device__ __forceinline__ AMap warp_compose_down(AMap x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (int d = 1; d < 32; d <<= 1) {
+    AMap y;
+    y.c = __shfl_down_sync(0xffffffffu, x.c, d);
+    y.s = __shfl_down_sync(0xffffffffu, x.s, d);
+    y.t = __shfl_down_sync(0xffffffffu, x.t, d);
+    if (lane + d < 32) x = amap_then_slow(y, x);
+  }
+  return shfl_amap(x, 0);
+}
+
 // ticket -> (chain, tile-in-chain, global tile) through the round-robin schedule
 __device__ __forceinline__ bool next_tile(const ChainTab& ct, int* chain, long long* tin, long long* g) {
   const int lane = threadIdx.x & 31;
@@ -251,33 +300,38 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
   long long incnt[NC];
 #pragma unroll
   for (int c = 0; c < NC; c++) incnt[c] = 0;
-  if (lane == 0) {
-    long long* cv = ct.cnt + g * 2 * kMaxCtx;
-    if (!chain_start) {
+  if (!chain_start) {
+    if (lane == 0) {
+      long long* cv = ct.cnt + g * 2 * kMaxCtx;
 #pragma unroll
       for (int c = 0; c < NC; c++) cv[c] = (c >= base && c < base + NL) ? tot[c - base] : 0;
       publish(ct, g, 0, 1);
-      const long long jmin = g - tin;
-      for (long long j = g - 1;; j--) {
-        int st = wait_state(ct, j, 0, status);
-        volatile const long long* pv = ct.cnt + j * 2 * kMaxCtx;
-        if (st == 2) {
-#pragma unroll
-          for (int c = 0; c < NC; c++) incnt[c] += pv[kMaxCtx + c];
-          break;
-        }
-#pragma unroll
-        for (int c = 0; c < NC; c++) incnt[c] += pv[c];
-        if (st == 0 || j == jmin) break;
-      }
     }
+    const long long jmin = g - tin;
+    for (long long j0 = g - 1;; j0 -= 32) {
+      int st;
+      const int k = probe_window(ct, j0, jmin, 0, status, &st);
+      const long long j = j0 - lane;
+      volatile const long long* pv = ct.cnt + (st ? j : 0) * 2 * kMaxCtx;
+#pragma unroll
+      for (int c = 0; c < NC; c++) {
+        long long v = 0;
+        if (st && lane < k) v = pv[c];
+        else if (st && lane == k) v = pv[kMaxCtx + c];
+        incnt[c] += warp_sum_ll(v);
+      }
+      if (k < 32) break;
+    }
+  }
+  if (lane == 0) {
+    long long* cv = ct.cnt + g * 2 * kMaxCtx;
 #pragma unroll
     for (int c = 0; c < NC; c++) cv[kMaxCtx + c] = incnt[c] + ((c >= base && c < base + NL) ? tot[c - base] : 0);
     publish(ct, g, 0, 2);
   }
   int n0[NL];  // N before this lane's first symbol of each context
 #pragma unroll
-  for (int c = 0; c < NL; c++) n0[c] = n_before(__shfl_sync(0xffffffffu, incnt[base + c], 0) + lbase[c]);
+  for (int c = 0; c < NL; c++) n0[c] = n_before(incnt[base + c] + lbase[c]);
 
   // ---- 2. A-maps (the reference's update_state as a map of the incoming A) ----
 #pragma unroll
@@ -313,40 +367,38 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
   int ain[NC];
 #pragma unroll
   for (int c = 0; c < NC; c++) ain[c] = 4;  // AdaptiveRiceState: A = 4, N = 1
-  if (lane == 0) {
-    if (!chain_start) {
+  if (!chain_start) {
+    if (lane == 0) {
       AMap* mv = ct.maps + g * kMaxCtx;
 #pragma unroll
       for (int c = 0; c < NC; c++) mv[c] = (c >= base && c < base + NL) ? agg[c - base] : amap_identity();
       publish(ct, g, 1, 1);
-      AMap acc[NC];
-#pragma unroll
-      for (int c = 0; c < NC; c++) acc[c] = amap_identity();
-      const long long jmin = g - tin;
-      for (long long j = g - 1;; j--) {
-        int st = wait_state(ct, j, 1, status);
-        if (st == 2) {
-          volatile const int* ps = ct.states + j * kMaxCtx;
-#pragma unroll
-          for (int c = 0; c < NC; c++) ain[c] = (int)amap_apply(acc[c], ps[c]);
-          break;
-        }
-        volatile const AMap* pm = ct.maps + j * kMaxCtx;
-#pragma unroll 1
-        for (int c = 0; c < NC; c++) {
-          AMap a;
-          a.c = pm[c].c;
-          a.s = pm[c].s;
-          a.t = pm[c].t;
-          acc[c] = amap_then_slow(a, acc[c]);
-        }
-        if (st == 0 || j == jmin) {
-#pragma unroll
-          for (int c = 0; c < NC; c++) ain[c] = (int)amap_apply(acc[c], 4);
-          break;
-        }
-      }
     }
+    AMap acc[NC];  // composition of the tiles already passed (newer than the window)
+#pragma unroll
+    for (int c = 0; c < NC; c++) acc[c] = amap_identity();
+    const long long jmin = g - tin;
+    for (long long j0 = g - 1;; j0 -= 32) {
+      int st;
+      const int k = probe_window(ct, j0, jmin, 1, status, &st);
+      const long long j = j0 - lane;
+      volatile const AMap* pm = ct.maps + (st ? j : 0) * kMaxCtx;
+      volatile const int* ps = ct.states + (st ? j : 0) * kMaxCtx;
+#pragma unroll 1
+      for (int c = 0; c < NC; c++) {
+        AMap m = amap_identity();
+        if (st && lane < k) {
+          m.c = pm[c].c;
+          m.s = pm[c].s;
+          m.t = pm[c].t;
+        }
+        acc[c] = amap_then_slow(warp_compose_down(m), acc[c]);
+        if (k < 32) ain[c] = (int)amap_apply(acc[c], __shfl_sync(0xffffffffu, st ? ps[c] : 0, k));
+      }
+      if (k < 32) break;
+    }
+  }
+  if (lane == 0) {
     int* sv = ct.states + g * kMaxCtx;
 #pragma unroll
     for (int c = 0; c < NC; c++)
@@ -358,7 +410,7 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
   int a_start[NL];
 #pragma unroll
   for (int c = 0; c < NL; c++) {
-    a_start[c] = (int)amap_apply(pre[c], __shfl_sync(0xffffffffu, ain[base + c], 0));
+    a_start[c] = (int)amap_apply(pre[c], ain[base + c]);
     ls.a[c * 32 + lane] = a_start[c];
     ls.nn[c * 32 + lane] = n0[c];
   }
@@ -382,27 +434,28 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
   const long long loff = warp_excl_sum(nbits, &tbits);
   long long toff = 0;
   if (lane == 0) {
-    unsigned long long* bv = ct.bitv + g * 2;
-    bv[0] = (unsigned long long)tbits;
-    if (!chain_start) {
-      publish(ct, g, 2, 1);
-      const long long jmin = g - tin;
-      for (long long j = g - 1;; j--) {
-        int st = wait_state(ct, j, 2, status);
-        volatile const unsigned long long* pv = ct.bitv + j * 2;
-        if (st == 2) {
-          toff += (long long)pv[1];
-          break;
-        }
-        toff += (long long)pv[0];
-        if (st == 0 || j == jmin) break;
-      }
+    ct.bitv[g * 2 + 0] = (unsigned long long)tbits;
+    if (!chain_start) publish(ct, g, 2, 1);
+  }
+  if (!chain_start) {
+    const long long jmin = g - tin;
+    for (long long j0 = g - 1;; j0 -= 32) {
+      int st;
+      const int k = probe_window(ct, j0, jmin, 2, status, &st);
+      const long long j = j0 - lane;
+      volatile const unsigned long long* pv = ct.bitv + (st ? j : 0) * 2;
+      long long v = 0;
+      if (st && lane < k) v = (long long)pv[0];
+      else if (st && lane == k) v = (long long)pv[1];
+      toff += warp_sum_ll(v);
+      if (k < 32) break;
     }
-    bv[1] = (unsigned long long)(toff + tbits);
+  }
+  if (lane == 0) {
+    ct.bitv[g * 2 + 1] = (unsigned long long)(toff + tbits);
     publish(ct, g, 2, 2);
     if (tin == ct.tile_base[chain + 1] - ct.tile_base[chain] - 1) ct.bits[chain] = (unsigned long long)(toff + tbits);
   }
-  toff = __shfl_sync(0xffffffffu, toff, 0);
 
   // ---- 4. emit ----
   WordSink sink;

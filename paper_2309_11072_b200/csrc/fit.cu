@@ -275,7 +275,23 @@ __device__ void warp_ddot2(const XA& X, const YA& Y, long long start, long long 
   if (kernel == 0) {  // SKYLAKEX
     long long n32 = n1 & ~31LL;
     double axx = 0.0, axy = 0.0;
-    for (long long i = lane; i < n32; i += 32) {
+    long long i = lane;
+    // the lane's chain is sequential; keep kPF loads in flight ahead of it
+    constexpr int kPF = 16;
+    for (; i + 32LL * (kPF - 1) < n32; i += 32LL * kPF) {
+      double xv[kPF], yv[kPF];
+#pragma unroll
+      for (int u = 0; u < kPF; u++) {
+        xv[u] = X(start + i + 32LL * u);
+        yv[u] = Y(start + i + 32LL * u);
+      }
+#pragma unroll
+      for (int u = 0; u < kPF; u++) {
+        axx = __fma_rn(xv[u], xv[u], axx);
+        axy = __fma_rn(xv[u], yv[u], axy);
+      }
+    }
+    for (; i < n32; i += 32) {
       double x = X(start + i), y = Y(start + i);
       axx = __fma_rn(x, x, axx);
       axy = __fma_rn(x, y, axy);
@@ -317,12 +333,28 @@ __device__ void warp_ddot2(const XA& X, const YA& Y, long long start, long long 
       }
   } else {  // HASWELL: 16 lanes, lane 4k+l = acc[k][l]
     double axx = 0.0, axy = 0.0;
-    if (lane < 16)
-      for (long long i = lane; i < n1; i += 16) {
+    if (lane < 16) {
+      long long i = lane;
+      constexpr int kPF = 16;
+      for (; i + 16LL * (kPF - 1) < n1; i += 16LL * kPF) {
+        double xv[kPF], yv[kPF];
+#pragma unroll
+        for (int u = 0; u < kPF; u++) {
+          xv[u] = X(start + i + 16LL * u);
+          yv[u] = Y(start + i + 16LL * u);
+        }
+#pragma unroll
+        for (int u = 0; u < kPF; u++) {
+          axx = __fma_rn(xv[u], xv[u], axx);
+          axy = __fma_rn(xv[u], yv[u], axy);
+        }
+      }
+      for (; i < n1; i += 16) {
         double x = X(start + i), y = Y(start + i);
         axx = __fma_rn(x, x, axx);
         axy = __fma_rn(x, y, axy);
       }
+    }
     double a[16], b[16];
 #pragma unroll
     for (int j = 0; j < 16; j++) {
@@ -360,6 +392,18 @@ __device__ void warp_ddot2(const XA& X, const YA& Y, long long start, long long 
   *out_xy = dxy;
 }
 
+// The ddot lanes are sequential FMA chains (the reference's order), so the
+// samples are streamed through shared memory with bulk async copies
+// (cp.async.bulk + mbarrier, kStages deep) and each lane's chain only waits on
+// FMA latency.  Blocks hold kBlk samples; the bulk region is [0, nmain) with
+// nmain = n32 (SKYLAKEX, 32 lanes) or n1 (HASWELL, 16 lanes).
+constexpr int kBlk = 2048, kStages = 4;
+struct DotSmem {
+  uint64_t bar[kStages];
+  double x[kStages][kBlk + 2];
+  uint8_t y[kStages][kBlk + 32];
+};
+
 // grid: (kSegs, nimg, max chunks); one warp per (segment, OpenBLAS thread-chunk)
 __global__ void __launch_bounds__(32) k_seg_dot(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
@@ -367,10 +411,18 @@ __global__ void __launch_bounds__(32) k_seg_dot(const ImgDesc* __restrict__ desc
   const int s = blockIdx.x;
   SegView v = seg_view(d, s);
   if (v.n == 0) return;
+  extern __shared__ __align__(16) uint8_t dot_raw[];
+  DotSmem& sm = *reinterpret_cast<DotSmem*>(dot_raw);
+  const int lane = threadIdx.x & 31;
   const int c = s >> 8;
   const XAcc X = x_acc(d, c, v);
   const MAcc M{d.ys + (long long)c * d.n + v.off};
   const int T = (v.n > 10000 && d.blas_threads > 1) ? min(d.blas_threads, kMaxBlasThreads) : 1;
+  if (lane == 0)
+    for (int k = 0; k < kStages; k++) mbar_init(&sm.bar[k], 1);
+  fence_mbar_init();
+  __syncwarp();
+  unsigned phase_bits = 0;  // parity of every stage's barrier, flipped at each consumed block
   for (int j = blockIdx.z; j < T; j += gridDim.z) {
     // chunk j of OpenBLAS's level-1 split: width = ceil(rem / (T - used))
     long long start = 0, rem = v.n, width = 0;
@@ -382,16 +434,127 @@ __global__ void __launch_bounds__(32) k_seg_dot(const ImgDesc* __restrict__ desc
         rem -= width;
       }
     }
-    double xx, xy;
-    warp_ddot2(X, M, start, width, d.blas_kernel, &xx, &xy);
-    // y.sum() is an exact integer sum (estimator.py:160): any order
+    const int kernel = d.blas_kernel;
+    const long long n1 = width & ~15LL;
+    const long long nmain = kernel == 0 ? (n1 & ~31LL) : n1;
+    const int nl = kernel == 0 ? 32 : 16;  // lanes of the main loop
+    const long long nblk = (nmain + kBlk - 1) / kBlk;
+    auto issue = [&](long long b) {
+      const int st = (int)(b % kStages);
+      const long long e0 = b * kBlk, len = min((long long)kBlk, nmain - e0);
+      const char* xa = reinterpret_cast<const char*>(X.p + start + e0);
+      const char* xa0 = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(xa) & ~uintptr_t(15));
+      const unsigned xbytes = (unsigned)(((xa - xa0) + len * 8 + 15) & ~15LL);
+      const char* ya = reinterpret_cast<const char*>(M.p + start + e0);
+      const char* ya0 = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(ya) & ~uintptr_t(15));
+      const unsigned ybytes = (unsigned)(((ya - ya0) + len + 15) & ~15LL);
+      fence_proxy_async_smem();
+      mbar_expect_tx(&sm.bar[st], xbytes + ybytes);
+      bulk_g2s(&sm.x[st][0], xa0, xbytes, &sm.bar[st]);
+      bulk_g2s(&sm.y[st][0], ya0, ybytes, &sm.bar[st]);
+    };
+    if (lane == 0)
+      for (long long b = 0; b < min((long long)kStages - 1, nblk); b++) issue(b);
+    __syncwarp();
+    double axx = 0.0, axy = 0.0;
     unsigned long long sy = 0;
-    for (long long i = start + (threadIdx.x & 31); i < start + width; i += 32) sy += M.p[i];
+    for (long long b = 0; b < nblk; b++) {
+      if (lane == 0 && b + kStages - 1 < nblk) issue(b + kStages - 1);
+      const int st = (int)(b % kStages);
+      mbar_wait(&sm.bar[st], (phase_bits >> st) & 1u);
+      phase_bits ^= 1u << st;
+      const long long e0 = b * kBlk, len = min((long long)kBlk, nmain - e0);
+      const int mx = (int)((reinterpret_cast<uintptr_t>(X.p + start + e0) & 15) >> 3);
+      const int my = (int)(reinterpret_cast<uintptr_t>(M.p + start + e0) & 15);
+      const double* xs = &sm.x[st][mx];
+      const uint8_t* ys = &sm.y[st][my];
+      if (lane < nl) {
+#pragma unroll 8
+        for (long long k = lane; k < len; k += nl) {
+          const double x = xs[k], y = (double)ys[k];
+          axx = __fma_rn(x, x, axx);
+          axy = __fma_rn(x, y, axy);
+          sy += ys[k];
+        }
+      }
+      __syncwarp();
+    }
+    // fold and tails (oracle/hdll_oracle.c ddot_compute)
+    double dxx = 0.0, dxy = 0.0;
+    if (kernel == 0) {
+      double fxx = axx + __shfl_down_sync(0xffffffffu, axx, 4);  // 512 -> 256 fold
+      double fxy = axy + __shfl_down_sync(0xffffffffu, axy, 4);
+      if ((lane & 7) < 4) {
+        const int k = lane >> 3, l = lane & 7;
+        for (long long i = nmain; i < n1; i += 16) {
+          const double x = X(start + i + 4 * k + l), y = M(start + i + 4 * k + l);
+          fxx = __fma_rn(x, x, fxx);
+          fxy = __fma_rn(x, y, fxy);
+        }
+      }
+      double sxx4[4], sxy4[4];
+#pragma unroll
+      for (int l = 0; l < 4; l++) {
+        double v0 = __shfl_sync(0xffffffffu, fxx, l), v1 = __shfl_sync(0xffffffffu, fxx, 8 + l);
+        double v2 = __shfl_sync(0xffffffffu, fxx, 16 + l), v3 = __shfl_sync(0xffffffffu, fxx, 24 + l);
+        sxx4[l] = ((v0 + v1) + v2) + v3;
+        v0 = __shfl_sync(0xffffffffu, fxy, l);
+        v1 = __shfl_sync(0xffffffffu, fxy, 8 + l);
+        v2 = __shfl_sync(0xffffffffu, fxy, 16 + l);
+        v3 = __shfl_sync(0xffffffffu, fxy, 24 + l);
+        sxy4[l] = ((v0 + v1) + v2) + v3;
+      }
+      if (n1) {
+        dxx = (sxx4[0] + sxx4[2]) + (sxx4[1] + sxx4[3]);
+        dxy = (sxy4[0] + sxy4[2]) + (sxy4[1] + sxy4[3]);
+      }
+      if (lane == 0)
+        for (long long i = n1; i < width; i++) {
+          const double x = X(start + i), y = M(start + i);
+          dxx = __fma_rn(x, x, dxx);
+          dxy = __fma_rn(y, x, dxy);
+        }
+    } else {
+      double a[16], bb[16];
+#pragma unroll
+      for (int q = 0; q < 16; q++) {
+        a[q] = __shfl_sync(0xffffffffu, axx, q);
+        bb[q] = __shfl_sync(0xffffffffu, axy, q);
+      }
+      if (n1) {
+        double t0[4], t1[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          t0[k] = a[4 * k + 0] + a[4 * k + 2];
+          t1[k] = a[4 * k + 1] + a[4 * k + 3];
+        }
+        double u0 = t0[0] + t0[1], u1 = t1[0] + t1[1], v0 = t0[2] + t0[3], v1 = t1[2] + t1[3];
+        dxx = (u0 + v0) + (u1 + v1);
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          t0[k] = bb[4 * k + 0] + bb[4 * k + 2];
+          t1[k] = bb[4 * k + 1] + bb[4 * k + 3];
+        }
+        u0 = t0[0] + t0[1];
+        u1 = t1[0] + t1[1];
+        v0 = t0[2] + t0[3];
+        v1 = t1[2] + t1[3];
+        dxy = (u0 + v0) + (u1 + v1);
+      }
+      if (lane == 0)
+        for (long long i = n1; i < width; i++) {
+          const double x = X(start + i), y = M(start + i);
+          dxx = dxx + x * x;
+          dxy = dxy + y * x;
+        }
+    }
+    // y.sum() is an exact integer sum (estimator.py:160): any order
+    for (long long i = nmain + lane; i < width; i += 32) sy += M.p[start + i];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sy += __shfl_xor_sync(0xffffffffu, sy, o);
-    if ((threadIdx.x & 31) == 0) {
-      d.dot_part[((long long)s * kMaxBlasThreads + j) * 2 + 0] = xx;
-      d.dot_part[((long long)s * kMaxBlasThreads + j) * 2 + 1] = xy;
+    if (lane == 0) {
+      d.dot_part[((long long)s * kMaxBlasThreads + j) * 2 + 0] = dxx;
+      d.dot_part[((long long)s * kMaxBlasThreads + j) * 2 + 1] = dxy;
       atomicAdd(reinterpret_cast<unsigned long long*>(&d.sum_y[s]), sy);
     }
   }
@@ -453,7 +616,8 @@ void launch_fit(const ImgDesc* d_descs, int nimg, int max_sort_tiles, long long 
   k_sort_scatter<<<dim3(max_sort_tiles, nimg), 256, sizeof(ScatterSmem), st>>>(d_descs);
   k_seg_setup<<<nimg, 32, 0, st>>>(d_descs);
   k_seg_nodes<<<dim3((unsigned)((max_nodes + 3) / 4), nimg), 128, 0, st>>>(d_descs);
-  k_seg_dot<<<dim3(kSegs, nimg, max_chunks), 32, 0, st>>>(d_descs);
+  cudaFuncSetAttribute(k_seg_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DotSmem));
+  k_seg_dot<<<dim3(kSegs, nimg, max_chunks), 32, sizeof(DotSmem), st>>>(d_descs);
   k_seg_reduce_coef<<<dim3(kSegs, nimg), 256, 0, st>>>(d_descs);
 }
 
