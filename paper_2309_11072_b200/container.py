@@ -548,12 +548,15 @@ def encode_device(preps, rgbe_ptrs, out_ptrs, out_caps, lens_ptr: int, stream_ha
 class HostPipeline:
     """Host-to-host batched encode with transfers overlapped with compute.
 
-    The batch is cut into chunks; chunk i's host->device copy, chunk i-1's
-    encode and chunk i-2's device->host copy of its streams run concurrently
-    on separate CUDA streams (two device contexts alternate so workspaces never
-    collide).  Inputs must be pinned host tensors; streams land in pinned host
-    buffers.  This is the `e2e` path of bench.py.
+    The batch is cut into chunks encoded back to back on one compute stream;
+    chunk i+1's host->device copy and chunk i-1's device->host copy of its
+    streams run on two copy streams meanwhile.  Three rotating buffer slots keep
+    a slot from being refilled before its streams have been read back.  Inputs
+    are pinned host tensors; streams land in pinned host buffers.  This is the
+    `e2e` path of bench.py.
     """
+
+    NSLOT = 3
 
     def __init__(self, preps, device: int = 0, chunk: int = 8):
         import torch
@@ -564,19 +567,20 @@ class HostPipeline:
         self.preps = preps
         self.chunk = max(1, chunk)
         self.chunks = [list(range(i, min(len(preps), i + self.chunk))) for i in range(0, len(preps), self.chunk)]
-        self.ctx = [_native.Context(device), _native.Context(device)]
-        self.s_comp = [torch.cuda.Stream(self.dev), torch.cuda.Stream(self.dev)]
+        self.ctx = _native.Context(device)
+        self.s_comp = torch.cuda.Stream(self.dev)
         self.s_h2d = torch.cuda.Stream(self.dev)
         self.s_d2h = torch.cuda.Stream(self.dev)
         mx = max(len(c) for c in self.chunks)
-        in_bytes = [max(p.pixels.nbytes for p in preps)] * mx
+        in_mx = max(p.pixels.nbytes for p in preps)
         self.caps = [stream_capacity(p) for p in preps]
         cap_mx = max(self.caps)
-        self.d_in = [[torch.empty(b, dtype=torch.uint8, device=self.dev) for b in in_bytes] for _ in range(2)]
-        self.d_out = [[torch.empty(cap_mx, dtype=torch.uint8, device=self.dev) for _ in range(mx)] for _ in range(2)]
-        self.d_len = [torch.zeros(mx, dtype=torch.int64, device=self.dev) for _ in range(2)]
-        self.h_len = [torch.zeros(mx, dtype=torch.int64).pin_memory() for _ in range(2)]
-        self.slot_free = [torch.cuda.Event(), torch.cuda.Event()]
+        n = self.NSLOT
+        self.d_in = [[torch.empty(in_mx, dtype=torch.uint8, device=self.dev) for _ in range(mx)] for _ in range(n)]
+        self.d_out = [[torch.empty(cap_mx, dtype=torch.uint8, device=self.dev) for _ in range(mx)] for _ in range(n)]
+        self.d_len = [torch.zeros(mx, dtype=torch.int64, device=self.dev) for _ in range(n)]
+        self.h_len = [torch.zeros(mx, dtype=torch.int64).pin_memory() for _ in range(n)]
+        self.slot_free = [torch.cuda.Event() for _ in range(n)]
         for e in self.slot_free:
             e.record(torch.cuda.current_stream(self.dev))
 
@@ -585,43 +589,49 @@ class HostPipeline:
         uint8 tensor of capacity >= stream_capacity.  Returns the stream lengths."""
         torch = self.torch
         lens = [0] * len(self.preps)
-        pending = []  # (chunk index, slot, done event)
-        for ci, idx in enumerate(self.chunks):
-            s = ci % 2
-            # H2D into slot s once the slot's previous D2H has drained
+        pending = []
+        ns = self.NSLOT
+
+        def upload(ci):
+            s = ci % ns
             self.s_h2d.wait_event(self.slot_free[s])
             with torch.cuda.stream(self.s_h2d):
-                for k, i in enumerate(idx):
-                    n = self.preps[i].pixels.nbytes
-                    self.d_in[s][k][:n].copy_(h_in[i][:n], non_blocking=True)
-            h2d_done = torch.cuda.Event()
-            h2d_done.record(self.s_h2d)
-            self.s_comp[s].wait_event(h2d_done)
+                for k, i in enumerate(self.chunks[ci]):
+                    nb = self.preps[i].pixels.nbytes
+                    self.d_in[s][k][:nb].copy_(h_in[i][:nb], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self.s_h2d)
+            return ev
+
+        up = {0: upload(0)}
+        for ci, idx in enumerate(self.chunks):
+            s = ci % ns
+            if ci + 1 < len(self.chunks):
+                up[ci + 1] = upload(ci + 1)  # next chunk's upload overlaps this chunk's encode
+            self.s_comp.wait_event(up.pop(ci))
             encode_device([self.preps[i] for i in idx], [self.d_in[s][k].data_ptr() for k in range(len(idx))],
                           [self.d_out[s][k].data_ptr() for k in range(len(idx))], [self.caps[i] for i in idx],
-                          self.d_len[s].data_ptr(), self.s_comp[s].cuda_stream, self.device, self.ctx[s])
-            with torch.cuda.stream(self.s_comp[s]):
+                          self.d_len[s].data_ptr(), self.s_comp.cuda_stream, self.device, self.ctx)
+            with torch.cuda.stream(self.s_comp):
                 self.h_len[s][: len(idx)].copy_(self.d_len[s][: len(idx)], non_blocking=True)
             done = torch.cuda.Event()
-            done.record(self.s_comp[s])
+            done.record(self.s_comp)
             pending.append((ci, s, done))
-            if len(pending) == 2:  # drain the older chunk while this one computes
+            if len(pending) == 2:  # read back the previous chunk while this one computes
                 self._drain(pending.pop(0), h_out, lens)
         while pending:
             self._drain(pending.pop(0), h_out, lens)
         self.s_d2h.synchronize()
-        for c in self.ctx:
-            _native.check(_native.lib().hdll_b200_sync(c.handle), "pipeline")
+        _native.check(_native.lib().hdll_b200_sync(self.ctx.handle), "pipeline")
         return lens
 
     def _drain(self, item, h_out, lens):
         torch = self.torch
         ci, s, done = item
-        done.synchronize()  # lengths of this chunk are on the host now
-        idx = self.chunks[ci]
+        done.synchronize()  # the chunk's lengths are on the host now
         self.s_d2h.wait_event(done)
         with torch.cuda.stream(self.s_d2h):
-            for k, i in enumerate(idx):
+            for k, i in enumerate(self.chunks[ci]):
                 n = int(self.h_len[s][k])
                 lens[i] = n
                 h_out[i][:n].copy_(self.d_out[s][k][:n], non_blocking=True)
