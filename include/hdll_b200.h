@@ -104,8 +104,9 @@ int hdll_b200_lossy_encode(hdll_b200_ctx *ctx, const uint8_t *h_rgb, uint32_t wi
 /* Number of kernel launches issued by the last encode call. */
 int hdll_b200_last_launch_count(hdll_b200_ctx *ctx);
 
-/* Device time (ms) of the 8 stages of the last batch, in order: tonemap stats,
- * base layer, prefilter, fit, estimate, crc, entropy coders, assemble. */
+/* Device time (ms) of the 9 stages of the last batch, in order: tonemap stats,
+ * base layer, prefilter, fit, estimate, crc, DCT entropy coder, plane entropy
+ * coders, assemble. */
 int hdll_b200_stage_times(hdll_b200_ctx *ctx, float *ms, int n);
 
 const char *hdll_b200_status_string(int status);

@@ -39,7 +39,7 @@ MAGIC = b"HDLL"
 VERSION = 1
 _ENTRY_FMT = "<BBffI"
 _ENTRY_SIZE = struct.calcsize(_ENTRY_FMT)  # 14 bytes (container.py:60-61)
-STAGES = ("tonemap", "base", "prefilter", "fit", "estimate", "crc", "entropy", "assemble")
+STAGES = ("tonemap", "base", "prefilter", "fit", "estimate", "crc", "entropy_dct", "entropy_plane", "assemble")
 
 
 # --------------------------------------------------------------------------

@@ -65,7 +65,8 @@ struct ImgLayout {
 };
 
 // stage boundaries recorded with CUDA events (hdll_b200_stage_times)
-enum { kStTonemap, kStBase, kStPrefilter, kStFit, kStEstimate, kStCrc, kStEntropy, kStAssemble, kStages };
+enum { kStTonemap, kStBase, kStPrefilter, kStFit, kStEstimate, kStCrc, kStEntropyDct, kStEntropyPlane, kStAssemble,
+       kStages };
 
 constexpr size_t kEstatPerTile = 16 + 16 * kMaxCtx + sizeof(AMap) * kMaxCtx + 4 * kMaxCtx + 16 + 8;
 
@@ -538,12 +539,13 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
     launch_entropy_fixup(ct_dct, st);
     c->launches += 2;
   }
+  mark(kStEntropyDct);
   if (ct_pln.ntiles > 0) {
     launch_entropy_plane(dd, ct_pln, max_w, st);
     launch_entropy_fixup(ct_pln, st);
     c->launches += 2;
   }
-  mark(kStEntropy);
+  mark(kStEntropyPlane);
   if (mode == 0) {
     AsmTab at;
     at.dct_out = ct_dct.out;
