@@ -44,7 +44,18 @@ __device__ __forceinline__ int kfast(int a, int n) {
 }
 
 __device__ __noinline__ AMap amap_push_slow(AMap m, int u, int h) { return amap_push(m, u, h); }
-__device__ __noinline__ AMap amap_then_slow(AMap f, AMap g) { return amap_then(f, g); }
+__device__ __noinline__ AMap amap_then_call(AMap f, AMap g) { return amap_then(f, g); }
+// exact o exact with a small total shift is the common case: inline it
+__device__ __forceinline__ AMap amap_then_slow(const AMap& f, const AMap& g) {
+  if (f.s >= 0 && g.s >= 0 && f.s + g.s < kADomainBits && f.s < 20) {
+    AMap r;
+    r.c = f.c + (g.c << f.s);
+    r.s = f.s + g.s;
+    r.t = 0;
+    return r;
+  }
+  return amap_then_call(f, g);
+}
 
 __device__ __forceinline__ void amap_push_fast(AMap& m, int u, int h) {
   if (m.s >= 0 && m.s + h < kADomainBits) {
@@ -552,51 +563,31 @@ __device__ __forceinline__ LaneState carve_state(uint8_t* p, int nl) {
 // ---------------------------------------------------------------------------
 enum { kFree = 0, kForced = 1, kInRun = 2 };
 
+// Rows are staged with one pad byte on the left: cur[-1] is the left
+// neighbour of x = 0 (the sample above, or 128 on row 0) and prev[-1] = prev[0],
+// so _neighbors (_kernels.py:131-143) is branch-free: a = cur[x-1], and
+// b = prev[x], c = prev[x-1] below row 0 (b = c = a on row 0).
+template <bool kHasPrev>
 struct RowView {
   const uint8_t* cur;
-  const uint8_t* prev;  // nullptr on row 0
-  // _neighbors, _kernels.py:131-143
+  const uint8_t* prev;
   __device__ __forceinline__ void abc(int x, int& a, int& b, int& c) const {
-    a = x > 0 ? cur[x - 1] : (prev ? prev[x] : 128);
-    b = prev ? prev[x] : a;
-    c = (x > 0 && prev) ? prev[x - 1] : b;
+    a = cur[x - 1];
+    if (kHasPrev) {
+      b = prev[x];
+      c = prev[x - 1];
+    } else {
+      b = a;
+      c = a;
+    }
   }
 };
 
-// grid-persistent; dynamic smem per warp: context state + 32 lane symbol lists
-__global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict__ descs, ChainTab ct, int row_bytes,
-                                                       int lane_cap) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const size_t per_warp = 2 * (size_t)row_bytes + lane_state_bytes(5) + 32 * (size_t)lane_cap * sizeof(uint16_t);
-  uint8_t* wbase = smem_raw + warp * per_warp;
-  uint8_t* srow_prev = wbase;
-  uint8_t* srow_cur = wbase + row_bytes;
-  const LaneState ls = carve_state(wbase + 2 * row_bytes, 5);
-  uint16_t* ssym = reinterpret_cast<uint16_t*>(wbase + 2 * row_bytes + lane_state_bytes(5)) + lane * lane_cap;
-  int chain;
-  long long tin, g;
-  while (next_tile(ct, &chain, &tin, &g)) {
-    const ImgDesc& d = descs[ct.img[chain]];
-    const int kind = ct.kind[chain];
-    const int y = (int)tin, W = d.w;
-    const uint8_t* src = kind == 1 ? d.e_plane : d.res_planes + (long long)(kind - 2) * d.n;
-    const uint8_t* gcur = src + (long long)y * W;
-    // stage the row and the row above (16-byte vectors when aligned)
-    if (((reinterpret_cast<uintptr_t>(gcur) | (uintptr_t)W) & 15) == 0) {
-      const uint4* c4 = reinterpret_cast<const uint4*>(gcur);
-      for (int q = lane; q < W / 16; q += 32) {
-        reinterpret_cast<uint4*>(srow_cur)[q] = __ldg(c4 + q);
-        if (y > 0) reinterpret_cast<uint4*>(srow_prev)[q] = __ldg(c4 + q - W / 16);
-      }
-    } else {
-      for (int x = lane; x < W; x += 32) {
-        srow_cur[x] = gcur[x];
-        if (y > 0) srow_prev[x] = gcur[x - W];
-      }
-    }
-    __syncwarp();
-    const RowView rv{srow_cur, y > 0 ? srow_prev : nullptr};
+// The lane's slice of one row -> its symbols in coder order (encode_plane's
+// automaton, _kernels.py:183-215).  Returns the count; per-context counts in cnt.
+template <bool kHasPrev>
+__device__ __forceinline__ int plane_row_symbols(const RowView<kHasPrev> rv, int W, int lane, uint16_t* ssym,
+                                                 int lane_cap, int* cnt) {
     const int P = (W + 31) / 32;
     const int x0 = min(W, lane * P), x1 = min(W, x0 + P);
     // one sweep: the slice's transition for the 3 entry states + its leading E-ones
@@ -642,9 +633,9 @@ __global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict
     }
     const int nx = __shfl_down_sync(0xffffffffu, val, 1);
     const int cont_next = lane == 31 ? 0 : nx;
-    // generate the lane's symbols
+    // generate the lane's symbols; per-context counts packed 12 bits apiece
     int n = 0;
-    int cnt[5] = {0, 0, 0, 0, 0};
+    unsigned long long cntp = 0;
     for (int x = x0; x < x1; x++) {
       int a, b, c;
       rv.abc(x, a, b, c);
@@ -664,7 +655,7 @@ __global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict
           int ch = L >= 255 ? 255 : L;
           if (n < lane_cap) ssym[n] = (uint16_t)((kRunCtx << 8) | ch);
           n++;
-          cnt[kRunCtx]++;
+          cntp += 1ULL << (12 * kRunCtx);
           L -= ch;
           if (ch < 255) break;
         }
@@ -684,10 +675,56 @@ __global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict
       const int u = r >= 0 ? 2 * r : -2 * r - 1;
       if (n < lane_cap) ssym[n] = (uint16_t)((ctx << 8) | u);
       n++;
-#pragma unroll
-      for (int q = 0; q < 4; q++) cnt[q] += ctx == q;
+      cntp += 1ULL << (12 * ctx);
       st = kFree;
     }
+#pragma unroll
+    for (int q = 0; q < 5; q++) cnt[q] = (int)((cntp >> (12 * q)) & 0xFFF);
+    return n;
+}
+
+// grid-persistent; dynamic smem per warp: context state + 32 lane symbol lists
+__global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict__ descs, ChainTab ct, int row_bytes,
+                                                       int lane_cap) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const size_t per_warp = 2 * (size_t)row_bytes + lane_state_bytes(5) + 32 * (size_t)lane_cap * sizeof(uint16_t);
+  uint8_t* wbase = smem_raw + warp * per_warp;
+  uint8_t* srow_prev = wbase + 16;  // 16 bytes of left pad keep the rows 16-byte aligned
+  uint8_t* srow_cur = wbase + row_bytes + 16;
+  const LaneState ls = carve_state(wbase + 2 * row_bytes, 5);
+  uint16_t* ssym = reinterpret_cast<uint16_t*>(wbase + 2 * row_bytes + lane_state_bytes(5)) + lane * lane_cap;
+  int chain;
+  long long tin, g;
+  while (next_tile(ct, &chain, &tin, &g)) {
+    const ImgDesc& d = descs[ct.img[chain]];
+    const int kind = ct.kind[chain];
+    const int y = (int)tin, W = d.w;
+    const uint8_t* src = kind == 1 ? d.e_plane : d.res_planes + (long long)(kind - 2) * d.n;
+    const uint8_t* gcur = src + (long long)y * W;
+    // stage the row and the row above (16-byte vectors when aligned)
+    if (((reinterpret_cast<uintptr_t>(gcur) | (uintptr_t)W) & 15) == 0) {
+      const uint4* c4 = reinterpret_cast<const uint4*>(gcur);
+      for (int q = lane; q < W / 16; q += 32) {
+        reinterpret_cast<uint4*>(srow_cur)[q] = __ldg(c4 + q);
+        if (y > 0) reinterpret_cast<uint4*>(srow_prev)[q] = __ldg(c4 + q - W / 16);
+      }
+    } else {
+      for (int x = lane; x < W; x += 32) {
+        srow_cur[x] = gcur[x];
+        if (y > 0) srow_prev[x] = gcur[x - W];
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      srow_cur[-1] = y > 0 ? srow_prev[0] : 128;
+      srow_prev[-1] = srow_prev[0];
+    }
+    __syncwarp();
+    int cnt[5];
+    int n;
+    if (y > 0) n = plane_row_symbols(RowView<true>{srow_cur, srow_prev}, W, lane, ssym, lane_cap, cnt);
+    else n = plane_row_symbols(RowView<false>{srow_cur, srow_prev}, W, lane, ssym, lane_cap, cnt);
     if (n > lane_cap) {
       atomicOr(d.status, kErrCapacity);
       n = lane_cap;
@@ -810,7 +847,7 @@ void launch_entropy_plane(const ImgDesc* d_descs, const ChainTab& ct, int max_w,
   if (ct.ntiles <= 0) return;
   const int P = (max_w + 31) / 32;
   const int lane_cap = 2 * P + max_w / 255 + 4;
-  const int row_bytes = (max_w + 31) / 16 * 16;
+  const int row_bytes = (max_w + 16 + 31) / 16 * 16;
   size_t per_warp = 2 * (size_t)row_bytes + lane_state_bytes(5) + 32 * (size_t)lane_cap * sizeof(uint16_t);
   int warps = (int)std::min<size_t>(4, (200 * 1024) / per_warp);
   if (warps < 1) warps = 1;
