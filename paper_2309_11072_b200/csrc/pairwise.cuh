@@ -99,8 +99,14 @@ __device__ double warp_pairwise(const Acc& a, long long off, long long n, double
     const long long lim = ln - (ln % 8);
     double r = 0.0;
     if (mine && ln >= 8) {
-      r = a(lo + j);
-      for (long long i = 8; i < lim; i += 8) r += a(lo + i + j);
+      // a leaf holds <= 128 samples: issue all 16 loads of the lane before the adds
+      double v[16];
+#pragma unroll
+      for (int q = 0; q < 16; q++) v[q] = (8 * q < lim) ? a(lo + 8 * q + j) : 0.0;
+      r = v[0];
+#pragma unroll
+      for (int q = 1; q < 16; q++)
+        if (8 * q < lim) r += v[q];
     }
     const double p2 = r + __shfl_down_sync(0xffffffffu, r, 1);    // r0+r1, r2+r3, ...
     const double q4 = p2 + __shfl_down_sync(0xffffffffu, p2, 2);  // (r0+r1)+(r2+r3), ...
