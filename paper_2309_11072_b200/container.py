@@ -584,19 +584,22 @@ class HostPipeline:
         for e in self.slot_free:
             e.record(torch.cuda.current_stream(self.dev))
 
-    def run(self, h_in, h_out):
+    def run(self, h_in, h_out, repeats: int = 1):
         """h_in[i]: pinned uint8 tensor of image i's RGBE bytes; h_out[i]: pinned
-        uint8 tensor of capacity >= stream_capacity.  Returns the stream lengths."""
+        uint8 tensor of capacity >= stream_capacity.  Returns the stream lengths.
+        `repeats` > 1 streams the batch that many times back to back (one
+        continuous pipeline, as for a stream of images)."""
         torch = self.torch
         lens = [0] * len(self.preps)
         pending = []
         ns = self.NSLOT
+        chunks = self.chunks * max(1, repeats)
 
         def upload(ci):
             s = ci % ns
             self.s_h2d.wait_event(self.slot_free[s])
             with torch.cuda.stream(self.s_h2d):
-                for k, i in enumerate(self.chunks[ci]):
+                for k, i in enumerate(chunks[ci]):
                     nb = self.preps[i].pixels.nbytes
                     self.d_in[s][k][:nb].copy_(h_in[i][:nb], non_blocking=True)
             ev = torch.cuda.Event()
@@ -604,9 +607,9 @@ class HostPipeline:
             return ev
 
         up = {0: upload(0)}
-        for ci, idx in enumerate(self.chunks):
+        for ci, idx in enumerate(chunks):
             s = ci % ns
-            if ci + 1 < len(self.chunks):
+            if ci + 1 < len(chunks):
                 up[ci + 1] = upload(ci + 1)  # next chunk's upload overlaps this chunk's encode
             self.s_comp.wait_event(up.pop(ci))
             encode_device([self.preps[i] for i in idx], [self.d_in[s][k].data_ptr() for k in range(len(idx))],
@@ -616,7 +619,7 @@ class HostPipeline:
                 self.h_len[s][: len(idx)].copy_(self.d_len[s][: len(idx)], non_blocking=True)
             done = torch.cuda.Event()
             done.record(self.s_comp)
-            pending.append((ci, s, done))
+            pending.append((idx, s, done))
             if len(pending) == 2:  # read back the previous chunk while this one computes
                 self._drain(pending.pop(0), h_out, lens)
         while pending:
@@ -627,11 +630,11 @@ class HostPipeline:
 
     def _drain(self, item, h_out, lens):
         torch = self.torch
-        ci, s, done = item
+        idx, s, done = item
         done.synchronize()  # the chunk's lengths are on the host now
         self.s_d2h.wait_event(done)
         with torch.cuda.stream(self.s_d2h):
-            for k, i in enumerate(self.chunks[ci]):
+            for k, i in enumerate(idx):
                 n = int(self.h_len[s][k])
                 lens[i] = n
                 h_out[i][:n].copy_(self.d_out[s][k][:n], non_blocking=True)
