@@ -6,6 +6,8 @@
 // Parallel form: every 1 KiB chunk is CRC'd independently (slice-by-4 tables
 // in shared memory), then chunks are merged with zlib's crc32_combine
 // algebra: crc(A||B) = x^(8|B|) * crc(A) + crc(B) over GF(2) mod P.
+#include <cstring>
+
 #include "encoder.cuh"
 
 namespace hdll {
@@ -29,6 +31,8 @@ __device__ __forceinline__ uint32_t crc_combine(uint32_t a, uint32_t b, unsigned
 
 // job j of an image: 0 = decoded RGB interleaved (from S planes), 1 = E, 2..4 = residuals
 __device__ __forceinline__ long long crc_job_len(const ImgDesc& d, int j) { return j == 0 ? 3 * d.n : d.n; }
+// chunk bytes: whole pixels for the interleaved job (340 px), 1 KiB for planes
+__host__ __device__ __forceinline__ long long crc_chunk_bytes(int j) { return j == 0 ? 1020 : kCrcChunk; }
 
 __global__ void __launch_bounds__(256) k_crc_chunks(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
@@ -38,22 +42,38 @@ __global__ void __launch_bounds__(256) k_crc_chunks(const ImgDesc* __restrict__ 
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) (&tab[0][0])[i] = (&c_crc_tab[0][0])[i];
   __syncthreads();
   const long long len = crc_job_len(d, job);
+  const long long csz = crc_chunk_bytes(job);
   const long long chunk = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long b0 = chunk * kCrcChunk;
+  const long long b0 = chunk * csz;
   if (b0 >= len) return;
-  const long long b1 = min(len, b0 + kCrcChunk);
+  const long long b1 = min(len, b0 + csz);
   uint32_t c = 0xFFFFFFFFu;
   if (job == 0) {
-    const uint8_t* S = d.s_planes;
+    // decoded RGB interleaved from the 3 S planes, 4 pixels (12 bytes) per step
+    const uint8_t* R = d.s_planes;
+    const uint8_t* G = d.s_planes + d.n;
+    const uint8_t* B = d.s_planes + 2 * d.n;
     long long p = b0 / 3;
-    int ch = (int)(b0 % 3);
-    for (long long i = b0; i < b1; i++) {
-      uint8_t byte = S[(long long)ch * d.n + p];
-      c = tab[0][(c ^ byte) & 0xFF] ^ (c >> 8);
-      if (++ch == 3) {
-        ch = 0;
-        p++;
-      }
+    const long long p1 = b1 / 3;  // chunks are whole pixels
+    auto slice4 = [&](uint32_t w) {
+      w ^= c;
+      c = tab[3][w & 0xFF] ^ tab[2][(w >> 8) & 0xFF] ^ tab[1][(w >> 16) & 0xFF] ^ tab[0][w >> 24];
+    };
+    for (; p + 4 <= p1; p += 4) {
+      uint32_t r4, g4, b4;
+      memcpy(&r4, R + p, 4);
+      memcpy(&g4, G + p, 4);
+      memcpy(&b4, B + p, 4);
+      // little-endian words of the byte stream r0 g0 b0 r1 | g1 b1 r2 g2 | b2 r3 g3 b3
+      slice4((r4 & 0xFF) | ((g4 & 0xFF) << 8) | ((b4 & 0xFF) << 16) | (((r4 >> 8) & 0xFF) << 24));
+      slice4(((g4 >> 8) & 0xFF) | (((b4 >> 8) & 0xFF) << 8) | (((r4 >> 16) & 0xFF) << 16) |
+             (((g4 >> 16) & 0xFF) << 24));
+      slice4(((b4 >> 16) & 0xFF) | ((r4 >> 24) << 8) | ((g4 >> 24) << 16) | ((b4 >> 24) << 24));
+    }
+    for (; p < p1; p++) {
+      c = tab[0][(c ^ R[p]) & 0xFF] ^ (c >> 8);
+      c = tab[0][(c ^ G[p]) & 0xFF] ^ (c >> 8);
+      c = tab[0][(c ^ B[p]) & 0xFF] ^ (c >> 8);
     }
   } else {
     const uint8_t* src = job == 1 ? d.e_plane : d.res_planes + (long long)(job - 2) * d.n;
@@ -75,7 +95,8 @@ __global__ void __launch_bounds__(1024) k_crc_combine(const ImgDesc* __restrict_
   const int job = blockIdx.x;
   if (!((d.crc_mask >> job) & 1)) return;
   const long long len = crc_job_len(d, job);
-  const long long nch = (len + kCrcChunk - 1) / kCrcChunk;
+  const long long csz = crc_chunk_bytes(job);
+  const long long nch = (len + csz - 1) / csz;
   const uint32_t* part = d.crc_part + d.crc_part_off[job];
   const int nt = blockDim.x, t = threadIdx.x;
   __shared__ uint32_t scrc[1024];
@@ -85,12 +106,12 @@ __global__ void __launch_bounds__(1024) k_crc_combine(const ImgDesc* __restrict_
   uint32_t acc = 0;
   unsigned long long alen = 0;
   if (c0 < c1) {
-    const uint32_t xfull = x2nmodp((unsigned long long)kCrcChunk, 3);
+    const uint32_t xfull = x2nmodp((unsigned long long)csz, 3);
     acc = part[c0];
-    alen = (unsigned long long)min((long long)kCrcChunk, len - c0 * kCrcChunk);
+    alen = (unsigned long long)min(csz, len - c0 * csz);
     for (long long k = c0 + 1; k < c1; k++) {
-      unsigned long long l = (unsigned long long)min((long long)kCrcChunk, len - k * kCrcChunk);
-      uint32_t xp = (l == (unsigned long long)kCrcChunk) ? xfull : x2nmodp(l, 3);
+      unsigned long long l = (unsigned long long)min(csz, len - k * csz);
+      uint32_t xp = (l == (unsigned long long)csz) ? xfull : x2nmodp(l, 3);
       acc = crc_multmodp(xp, acc) ^ part[k];
       alen += l;
     }
@@ -126,7 +147,7 @@ void upload_crc_constants() {
 }
 
 void launch_crc(const ImgDesc* d_descs, int nimg, long long max_n, cudaStream_t st) {
-  long long max_chunks = (3 * max_n + kCrcChunk - 1) / kCrcChunk;
+  long long max_chunks = (3 * max_n + crc_chunk_bytes(0) - 1) / crc_chunk_bytes(0);
   k_crc_chunks<<<dim3((unsigned)((max_chunks + 255) / 256), nimg, 5), 256, 0, st>>>(d_descs);
   k_crc_combine<<<dim3(5, nimg), 1024, 0, st>>>(d_descs);
 }
