@@ -44,8 +44,13 @@ def _stale(out: Path, deps) -> bool:
     return any(Path(d).stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    BUILD.mkdir(exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines=(), lib: Path | None = None,
+          objdir: Path | None = None) -> Path:
+    """defines / lib / objdir: experiment builds (never the shipped library)."""
+    global BUILD, LIB
+    if objdir is not None:
+        BUILD, LIB = Path(objdir), Path(lib)
+    BUILD.mkdir(parents=True, exist_ok=True)
     sources = sorted(CSRC.glob("*.cu"))
     headers = sorted(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "hdll_b200.h"]
     cc = nvcc()
@@ -53,7 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     def compile_one(src: Path) -> Path:
         obj = BUILD / (src.stem + ".o")
         if force or _stale(obj, [src, *headers, Path(__file__)]):
-            cmd = [cc, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+            cmd = [cc, *NVCC_FLAGS, *[f"-D{x}" for x in defines], "-c", str(src), "-o", str(obj)]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if r.returncode != 0:
                 raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stdout}\n{r.stderr}")

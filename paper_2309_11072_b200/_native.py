@@ -7,11 +7,12 @@ CUDA device is present, `lib()` / `context()` raise immediately.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libhdll_b200.so"
+LIB_PATH = Path(os.environ["HDLL_B200_LIB"]) if os.environ.get("HDLL_B200_LIB") else _PKG / "libhdll_b200.so"
 
 OK, E_ARG, E_EMPTY, E_NONFINITE, E_CUDA, E_INTERNAL, E_CAPACITY = range(7)
 

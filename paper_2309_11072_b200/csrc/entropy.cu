@@ -298,7 +298,11 @@ template <int NL, int NC, class Gen>
 __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long g, int base, const Gen& gen,
                          const int* cnt_in, const LaneState& ls, unsigned* status) {
   const int lane = threadIdx.x & 31;
+#ifdef HDLL_EXP_NO_LB  // timing experiment only: no look-backs (wrong output)
+  const bool chain_start = true;
+#else
   const bool chain_start = tin == 0;
+#endif
 
   // ---- 1. counts -> global symbol index of this lane's first symbol per context ----
   long long lbase[NL], tot[NL];
@@ -352,6 +356,7 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
     ls.mt[c * 32 + lane] = 0;
     ls.nn[c * 32 + lane] = n0[c];
   }
+#ifndef HDLL_EXP_NO_MAPS
   gen.for_each([&](int, int c, int v, int, uint32_t) {
     const int o = c * 32 + lane;
     const int nb = ls.nn[o];
@@ -369,6 +374,7 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
       ls.mt[o] = m.t;
     }
   });
+#endif
   AMap pre[NL], agg[NL];
 #pragma unroll 1
   for (int c = 0; c < NL; c++) {
@@ -478,7 +484,12 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
   sink.status = status;
   LaneBits lb;
   lb.init(toff + loff);
+#ifdef HDLL_EXP_NO_EMIT
+  if constexpr (false) {
+  } else if constexpr (false) {
+#else
   if constexpr (Gen::kStoresK) {
+#endif
     gen.for_each_k([&](int v, int k, int xl, uint32_t xb) {
       lb.put(sink, rice_bits(v, k), rice_len(v, k));
       if (xl) lb.put(sink, xb, xl);
