@@ -195,18 +195,30 @@ int map_status(unsigned bits) {
 // Host side of a ChainTab: chains, their tiles and the round-robin ticket schedule.
 struct HostChains {
   std::vector<long long> tile_base{0};
-  std::vector<int> img, kind;
+  std::vector<int> img, kind, comp;
+  std::vector<long long> first, units;
   std::vector<uint8_t*> out;
   std::vector<long long> cap;
+  std::vector<long long> in_cnt;  // [chain][kMaxCtx]
+  std::vector<int> in_a;          // [chain][kMaxCtx]
   std::vector<int> rr_chain;
   std::vector<long long> seg_r0, seg_t0;
   std::vector<int> seg_active;
 
-  void add(int i, int k, long long tiles, uint8_t* o, long long c) {
+  // chain of image i, kind k over `units` blocks / rows from `first`, DCT component cp (-1: all three)
+  void add(int i, int k, int cp, long long fst, long long nunits, uint8_t* o, long long c) {
     img.push_back(i);
     kind.push_back(k);
+    comp.push_back(cp);
+    first.push_back(fst);
+    units.push_back(nunits);
     out.push_back(o);
     cap.push_back(c);
+    for (int q = 0; q < kMaxCtx; q++) {
+      in_cnt.push_back(0);
+      in_a.push_back(4);  // AdaptiveRiceState: A = 4 (_kernels.py:114-128)
+    }
+    const long long tiles = k == 0 ? (cp < 0 ? 3 : 1) * ((nunits + 31) / 32) : nunits;
     tile_base.push_back(tile_base.back() + tiles);
   }
   int nchains() const { return (int)img.size(); }
@@ -236,25 +248,34 @@ struct HostChains {
       seg_active.push_back(1);
     }
     if (rr_chain.empty()) rr_chain.push_back(0);
-    if (img.empty()) add(0, 0, 0, nullptr, 0);  // keep device arrays non-empty
+    if (img.empty()) add(0, 1, -1, 0, 0, nullptr, 0);  // keep device arrays non-empty
   }
   size_t staged_bytes() const {
     size_t nc = img.size() + 2;
-    return 10 * kAlign + 8 * (nc + 1) + 4 * nc * 2 + 8 * nc * 3 + 8 * 2 * seg_r0.size() + 4 * seg_active.size() +
-           4 * rr_chain.size();
+    return 16 * kAlign + 8 * (nc + 1) + 4 * nc * 3 + 8 * nc * 5 + (8 + 4 + 8 + sizeof(AMap)) * kMaxCtx * nc +
+           8 * 2 * seg_r0.size() + 4 * seg_active.size() + 4 * rr_chain.size();
   }
   struct Staged {
-    size_t tile_base, img, kind, out, cap, bits, seg_r0, seg_t0, seg_active, rr_chain;
+    size_t tile_base, img, kind, comp, first, units, out, cap, bits, in_cnt, in_a, out_cnt, out_map, seg_r0, seg_t0,
+        seg_active, rr_chain;
   };
   template <class F>
   Staged stage(F& st) const {
     Staged s;
+    const size_t nc = img.size();
     s.tile_base = st(tile_base.data(), 8 * tile_base.size());
-    s.img = st(img.data(), 4 * img.size());
-    s.kind = st(kind.data(), 4 * kind.size());
-    s.out = st(out.data(), 8 * out.size());
-    s.cap = st(cap.data(), 8 * cap.size());
-    s.bits = st(nullptr, 8 * img.size());
+    s.img = st(img.data(), 4 * nc);
+    s.kind = st(kind.data(), 4 * nc);
+    s.comp = st(comp.data(), 4 * nc);
+    s.first = st(first.data(), 8 * nc);
+    s.units = st(units.data(), 8 * nc);
+    s.out = st(out.data(), 8 * nc);
+    s.cap = st(cap.data(), 8 * nc);
+    s.bits = st(nullptr, 8 * nc);
+    s.in_cnt = st(in_cnt.data(), 8 * in_cnt.size());
+    s.in_a = st(in_a.data(), 4 * in_a.size());
+    s.out_cnt = st(nullptr, 8 * kMaxCtx * nc);
+    s.out_map = st(nullptr, sizeof(AMap) * kMaxCtx * nc);
     s.seg_r0 = st(seg_r0.data(), 8 * seg_r0.size());
     s.seg_t0 = st(seg_t0.data(), 8 * seg_t0.size());
     s.seg_active = st(seg_active.data(), 4 * seg_active.size());
@@ -262,16 +283,24 @@ struct HostChains {
     return s;
   }
   // status arrays live in the shared entropy arena at tile offset `t0`
-  ChainTab table(const Staged& s, uint8_t* D, uint8_t* E, long long cap_t, long long t0, int* ticket,
-                 int epoch) const {
+  ChainTab table(const Staged& s, uint8_t* D, uint8_t* E, long long cap_t, long long t0, int* ticket, int epoch,
+                 int mode = 0) const {
     ChainTab ct;
     ct.nchains = nchains();
     ct.tile_base = (const long long*)(D + s.tile_base);
     ct.img = (const int*)(D + s.img);
     ct.kind = (const int*)(D + s.kind);
+    ct.comp = (const int*)(D + s.comp);
+    ct.first = (const long long*)(D + s.first);
+    ct.units = (const long long*)(D + s.units);
     ct.out = (uint8_t* const*)(D + s.out);
     ct.cap = (const long long*)(D + s.cap);
     ct.bits = (unsigned long long*)(D + s.bits);
+    ct.in_cnt = (const long long*)(D + s.in_cnt);
+    ct.in_a = (const int*)(D + s.in_a);
+    ct.out_cnt = (long long*)(D + s.out_cnt);
+    ct.out_map = (AMap*)(D + s.out_map);
+    ct.mode = mode;
     size_t o = 0;
     ct.flags = (int*)(E + o) + t0 * 4;
     o += cap_t * 16;
@@ -336,8 +365,8 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
     const long long nb = ((w + 7) / 8) * ((h + 7) / 8);
     for (int k = 0; k < 5; k++) {
       bool active = (mode == 0) || (mode == 1 && k == 1) || (mode == 2 && k == 0);
-      long long tiles = active ? ((k == 0) ? 3 * ((nb + 31) / 32) : h) : 0;
-      (k == 0 ? hc_dct : hc_pln).add(i, k, tiles, A + base[i] + lays[i].off_chain[k], lays[i].chain_cap[k]);
+      (k == 0 ? hc_dct : hc_pln).add(i, k, -1, 0, active ? (k == 0 ? nb : h) : 0, A + base[i] + lays[i].off_chain[k],
+                                     lays[i].chain_cap[k]);
     }
   }
   hc_dct.schedule();
@@ -418,6 +447,17 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
     d.amb = (unsigned*)(B + L.off_zero + 12);
     d.bin_count = (unsigned*)(B + L.off_zero + 16);
     d.sum_y = (long long*)(B + L.off_zero + 16 + 1024);
+    d.full_n = d.n;
+    d.pix_base = 0;
+    d.px0 = 0;
+    d.px1 = d.n;
+    d.node0 = 0;
+    d.node1 = 1LL << pairwise_level(d.n);
+    d.fit_p0 = 0;
+    d.fit_m = d.n;
+    d.fit_owner = 0;
+    d.crc_p0 = 0;
+    d.crc_np = d.n;
     d.logv = (double*)(B + L.off_logv);
     d.tm_nodes = (double*)(B + L.off_tmnodes);
     d.tm_level = pairwise_level(d.n);

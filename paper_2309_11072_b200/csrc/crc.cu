@@ -30,7 +30,8 @@ __device__ __forceinline__ uint32_t crc_combine(uint32_t a, uint32_t b, unsigned
 }
 
 // job j of an image: 0 = decoded RGB interleaved (from S planes), 1 = E, 2..4 = residuals
-__device__ __forceinline__ long long crc_job_len(const ImgDesc& d, int j) { return j == 0 ? 3 * d.n : d.n; }
+// (over desc pixels [crc_p0, crc_p0 + crc_np): the whole image, or a row band's own rows)
+__device__ __forceinline__ long long crc_job_len(const ImgDesc& d, int j) { return j == 0 ? 3 * d.crc_np : d.crc_np; }
 // chunk bytes: whole pixels for the interleaved job (340 px), 1 KiB for planes
 __host__ __device__ __forceinline__ long long crc_chunk_bytes(int j) { return j == 0 ? 1020 : kCrcChunk; }
 
@@ -50,9 +51,9 @@ __global__ void __launch_bounds__(256) k_crc_chunks(const ImgDesc* __restrict__ 
   uint32_t c = 0xFFFFFFFFu;
   if (job == 0) {
     // decoded RGB interleaved from the 3 S planes, 4 pixels (12 bytes) per step
-    const uint8_t* R = d.s_planes;
-    const uint8_t* G = d.s_planes + d.n;
-    const uint8_t* B = d.s_planes + 2 * d.n;
+    const uint8_t* R = d.s_planes + d.crc_p0;
+    const uint8_t* G = d.s_planes + d.n + d.crc_p0;
+    const uint8_t* B = d.s_planes + 2 * d.n + d.crc_p0;
     long long p = b0 / 3;
     const long long p1 = b1 / 3;  // chunks are whole pixels
     auto slice4 = [&](uint32_t w) {
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(256) k_crc_chunks(const ImgDesc* __restrict__ 
       c = tab[0][(c ^ B[p]) & 0xFF] ^ (c >> 8);
     }
   } else {
-    const uint8_t* src = job == 1 ? d.e_plane : d.res_planes + (long long)(job - 2) * d.n;
+    const uint8_t* src = (job == 1 ? d.e_plane : d.res_planes + (long long)(job - 2) * d.n) + d.crc_p0;
     long long i = b0;
     // planes c > 0 start at c * n, which need not be word aligned
     for (; i < b1 && (reinterpret_cast<uintptr_t>(src + i) & 3); i++) c = tab[0][(c ^ src[i]) & 0xFF] ^ (c >> 8);

@@ -41,10 +41,21 @@ struct ImgDesc {
   const uint8_t* sdr_in;  // lossy-coder plugin mode: (h, w, 3) SDR given directly (codec_core.py:430)
   int crc_mask;           // which of the 5 CRC jobs to run
 
+  // Row-band view (tile-sharded single image, api.cu band mode).  A band desc
+  // is an image of the band's compute rows; these fields place it in the full
+  // image.  Whole-image descs: full_n = n, pix_base = 0, every range complete.
+  long long full_n;           // pixels of the full image (tone-map mean, pairwise tree)
+  long long pix_base;         // full-image index of the desc's pixel 0
+  long long px0, px1;         // full-image pixels whose log(Lw) and max this desc computes
+  long long node0, node1;     // pairwise nodes (level tm_level) this desc sums
+  long long fit_p0, fit_m;    // fit samples: desc pixels [fit_p0, fit_p0 + fit_m); xs/ys plane stride
+  int fit_owner;              // 1: xs/ys/bin_* were filled by the exchange (skip the sort)
+  long long crc_p0, crc_np;   // CRC jobs cover desc pixels [crc_p0, crc_p0 + crc_np)
+
   // tone-map stage
-  double* logv;               // n: log(eps + Lw)
+  double* logv;               // desc pixels: log(eps + Lw)
   unsigned long long* maxlw;  // bits of max Lw (Lw >= 0)
-  double* tm_nodes;           // pairwise-sum level-L node values
+  double* tm_nodes;           // pairwise-sum level-L node values (all 2^L of the full image)
   int tm_level;               // L for the image-wide pairwise tree
   double* scalars;            // [0] log-sum, [1] log_avg, [2] white, [3] allzero flag
 
@@ -117,9 +128,21 @@ struct ChainTab {
   const long long* tile_base;  // [nchains+1] global tile index of each chain's tile 0
   const int* img;              // image of the chain
   const int* kind;             // 0 = DCT stream, 1..4 = plane (E, R, G, B)
+  const int* comp;             // DCT: the one component of the chain, or -1 for Y, Cb, Cr in turn
+  const long long* first;      // first coded unit in the image arrays (DCT block / plane row)
+  const long long* units;      // coded units (DCT: blocks per component; plane: rows)
   uint8_t* const* out;         // chain byte stream (4-byte aligned)
   const long long* cap;        // capacity in bytes
   unsigned long long* bits;    // [nchains] total bits (written by the last tile)
+  // A chain may continue a sequential coder run elsewhere (a row band of a
+  // tile-sharded image): its first tile starts from in_cnt / in_a instead of
+  // the reset state (count 0, A = 4).  mode 1 stops after the counts and
+  // mode 2 after the A-maps, reporting the chain totals in out_cnt / out_map.
+  const long long* in_cnt;     // [nchains][kMaxCtx] context counts before the chain
+  const int* in_a;             // [nchains][kMaxCtx] A entering the chain
+  long long* out_cnt;          // [nchains][kMaxCtx] counts after the chain (mode 1)
+  AMap* out_map;               // [nchains][kMaxCtx] the chain's composed A-map (mode 2)
+  int mode;                    // 0 full encode, 1 counts, 2 counts + A-maps
   // per global tile status (epoch-tagged)
   int* flags;                  // [ntiles][4]: cnt, map, bit, done
   long long* cnt;              // [ntiles][2][kMaxCtx]: aggregate, inclusive
@@ -149,9 +172,25 @@ struct AsmTab {
 void upload_base_constants();
 void upload_crc_constants();
 void launch_tonemap_stats(const ImgDesc*, int nimg, long long max_n, int max_level, cudaStream_t);
+void launch_tonemap_partial(const ImgDesc*, int nimg, long long max_n, int max_level, cudaStream_t);
+void launch_tonemap_scalars(const ImgDesc*, int nimg, cudaStream_t);
 void launch_base_layer(const ImgDesc*, int nimg, int max_tiles, cudaStream_t);
 void launch_prefilter(const ImgDesc*, int nimg, int max_w, int max_h, int max_radius, cudaStream_t);
 void launch_fit(const ImgDesc*, int nimg, int max_sort_tiles, long long max_nodes, int max_chunks, cudaStream_t);
+void launch_fit_sort(const ImgDesc*, int nimg, int max_sort_tiles, cudaStream_t);
+void launch_fit_bins(const ImgDesc*, int nimg, long long max_nodes, int max_chunks, cudaStream_t);
+struct RegroupTab {
+  int nsrc;
+  const uint8_t* recv;             // concatenated chunks, one per source rank
+  const long long* src_off;        // [nsrc+1] byte offset of each chunk
+  const long long* src_m;          // [nsrc] samples in each chunk
+  const unsigned* src_bin_off;     // [nsrc][257] sample offset of bin e inside the chunk (owned bins)
+  const unsigned* dst_bin_off;     // [nsrc][256] destination of the chunk's first sample of bin e
+  long long total;                 // samples received
+};
+void launch_fit_regroup(const ImgDesc* d, const RegroupTab&, cudaStream_t);
+void launch_bitcat(uint8_t* dst, const uint8_t* const* src, const unsigned long long* dst_bit, const unsigned long long* nbits,
+                   int npieces, unsigned long long max_bits, cudaStream_t);
 void launch_estimate(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
 void launch_crc(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
 void launch_entropy_dct(const ImgDesc*, const ChainTab&, cudaStream_t);

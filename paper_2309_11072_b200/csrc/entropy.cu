@@ -312,9 +312,10 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
     lbase[c] = warp_excl_sum((long long)cnt_in[c], &t);
     tot[c] = t;
   }
+  const bool chain_last = tin == ct.tile_base[chain + 1] - ct.tile_base[chain] - 1;
   long long incnt[NC];
 #pragma unroll
-  for (int c = 0; c < NC; c++) incnt[c] = 0;
+  for (int c = 0; c < NC; c++) incnt[c] = chain_start ? ct.in_cnt[chain * kMaxCtx + c] : 0;
   if (!chain_start) {
     if (lane == 0) {
       long long* cv = ct.cnt + g * 2 * kMaxCtx;
@@ -343,7 +344,10 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
 #pragma unroll
     for (int c = 0; c < NC; c++) cv[kMaxCtx + c] = incnt[c] + ((c >= base && c < base + NL) ? tot[c - base] : 0);
     publish(ct, g, 0, 2);
+    if (ct.mode == 1 && chain_last)
+      for (int c = 0; c < NC; c++) ct.out_cnt[chain * kMaxCtx + c] = cv[kMaxCtx + c];
   }
+  if (ct.mode == 1) return;
   int n0[NL];  // N before this lane's first symbol of each context
 #pragma unroll
   for (int c = 0; c < NL; c++) n0[c] = n_before(incnt[base + c] + lbase[c]);
@@ -381,9 +385,17 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
     AMap m{ls.mc[c * 32 + lane], ls.ms[c * 32 + lane], ls.mt[c * 32 + lane]};
     pre[c] = warp_excl_amap_small(m, &agg[c]);
   }
+  if (ct.mode == 2) {  // totals only: every tile's aggregate, composed per chain by k_chain_maps
+    if (lane == 0) {
+      AMap* mv = ct.maps + g * kMaxCtx;
+#pragma unroll
+      for (int c = 0; c < NC; c++) mv[c] = (c >= base && c < base + NL) ? agg[c - base] : amap_identity();
+    }
+    return;
+  }
   int ain[NC];
 #pragma unroll
-  for (int c = 0; c < NC; c++) ain[c] = 4;  // AdaptiveRiceState: A = 4, N = 1
+  for (int c = 0; c < NC; c++) ain[c] = chain_start ? ct.in_a[chain * kMaxCtx + c] : 4;
   if (!chain_start) {
     if (lane == 0) {
       AMap* mv = ct.maps + g * kMaxCtx;
@@ -471,7 +483,7 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
   if (lane == 0) {
     ct.bitv[g * 2 + 1] = (unsigned long long)(toff + tbits);
     publish(ct, g, 2, 2);
-    if (tin == ct.tile_base[chain + 1] - ct.tile_base[chain] - 1) ct.bits[chain] = (unsigned long long)(toff + tbits);
+    if (chain_last) ct.bits[chain] = (unsigned long long)(toff + tbits);
   }
 
   // ---- 4. emit ----
@@ -710,7 +722,7 @@ __global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict
   while (next_tile(ct, &chain, &tin, &g)) {
     const ImgDesc& d = descs[ct.img[chain]];
     const int kind = ct.kind[chain];
-    const int y = (int)tin, W = d.w;
+    const int y = (int)(ct.first[chain] + tin), W = d.w;  // row in the image arrays
     const uint8_t* src = kind == 1 ? d.e_plane : d.res_planes + (long long)(kind - 2) * d.n;
     const uint8_t* gcur = src + (long long)y * W;
     // stage the row and the row above (16-byte vectors when aligned)
@@ -756,12 +768,15 @@ __global__ void __launch_bounds__(128) k_entropy_dct(const ImgDesc* __restrict__
   long long tin, g;
   while (next_tile(ct, &chain, &tin, &g)) {
     const ImgDesc& d = descs[ct.img[chain]];
-    const long long tpc = (d.nblocks + 31) / 32;
-    const int ci = (int)(tin / tpc);
-    const long long bi = (tin % tpc) * 32 + lane;
+    const long long units = ct.units[chain];
+    const long long tpc = (units + 31) / 32;
+    const int comp = ct.comp[chain];
+    const int ci = comp >= 0 ? comp : (int)(tin / tpc);
+    const long long tl = comp >= 0 ? tin : tin % tpc;
+    const long long bi = ct.first[chain] + tl * 32 + lane;  // block index in the image arrays
     DctBlockGen gen{nullptr, 0ULL, 0u};
     int cnt[3] = {0, 0, 0};
-    if (bi < d.nblocks) {
+    if (tl * 32 + lane < units) {
       const int16_t* z = d.zz + ((long long)ci * d.nblocks + bi) * 64;
       // nonzero mask of the 64 zigzag coefficients, 128-bit loads
       const uint4* z4 = reinterpret_cast<const uint4*>(z);
@@ -831,6 +846,27 @@ __global__ void __launch_bounds__(256) k_entropy_fixup(ChainTab ct) {
 }
 
 // ---------------------------------------------------------------------------
+// mode 2: compose every chain's tile aggregates (oldest first) into out_map.
+// One warp per (chain, context): lanes compose contiguous runs, then the warp.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(32) k_chain_maps(ChainTab ct) {
+  const int chain = blockIdx.x, c = blockIdx.y, lane = threadIdx.x;
+  const long long t0 = ct.tile_base[chain], nt = ct.tile_base[chain + 1] - t0;
+  const long long per = (nt + 31) / 32;
+  AMap m = amap_identity();
+  for (long long j = lane * per; j < min(nt, (lane + 1) * per); j++) m = amap_then(m, ct.maps[(t0 + j) * kMaxCtx + c]);
+#pragma unroll 1
+  for (int d = 1; d < 32; d <<= 1) {  // lane 0 holds the oldest run: compose x then (lane + d)
+    AMap y;
+    y.c = __shfl_down_sync(0xffffffffu, m.c, d);
+    y.s = __shfl_down_sync(0xffffffffu, m.s, d);
+    y.t = __shfl_down_sync(0xffffffffu, m.t, d);
+    if (lane + d < 32) m = amap_then(m, y);
+  }
+  if (lane == 0) ct.out_map[chain * kMaxCtx + c] = m;
+}
+
+// ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
 static int num_sms() {
@@ -874,6 +910,11 @@ void launch_entropy_plane(const ImgDesc* d_descs, const ChainTab& ct, int max_w,
 
 void launch_entropy_fixup(const ChainTab& ct, cudaStream_t st) {
   if (ct.ntiles <= 0) return;
+  if (ct.mode == 2) {
+    k_chain_maps<<<dim3(ct.nchains, kMaxCtx), 32, 0, st>>>(ct);
+    return;
+  }
+  if (ct.mode == 1) return;
   k_entropy_fixup<<<(unsigned)((ct.ntiles + 255) / 256), 256, 0, st>>>(ct);
 }
 

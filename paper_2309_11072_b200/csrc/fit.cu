@@ -29,18 +29,18 @@ constexpr int kSegs = 3 * 256;
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_sort_hist(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
-  if (!d.slrme) return;
+  if (!d.slrme || d.fit_owner) return;
   const int tile = blockIdx.x;
   if (tile >= d.sort_tiles) return;
   __shared__ unsigned hist[256];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
   __syncthreads();
-  const long long p0 = (long long)tile * kSortTile;
-  const uint32_t* px = reinterpret_cast<const uint32_t*>(d.rgbe);
+  const long long p0 = (long long)tile * kSortTile;  // sample index; pixel fit_p0 + sample
+  const uint32_t* px = reinterpret_cast<const uint32_t*>(d.rgbe) + d.fit_p0;
   const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
   for (int k = threadIdx.x; k < kSortTile; k += blockDim.x) {
     const long long p = p0 + k;
-    const bool valid = p < d.n;
+    const bool valid = p < d.fit_m;
     const unsigned act = __ballot_sync(0xffffffffu, valid);
     if (!valid) continue;
     const unsigned e = px[p] >> 24;
@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(256) k_sort_hist(const ImgDesc* __restrict__ d
 // bin starts + per-tile absolute offsets (in place over tile_hist)
 __global__ void __launch_bounds__(256) k_sort_scan(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.x];
-  if (!d.slrme) return;
+  if (!d.slrme || d.fit_owner) return;
   const int e = threadIdx.x;
   __shared__ unsigned cnt[256];
   cnt[e] = d.bin_count[e];
@@ -95,15 +95,17 @@ struct ScatterSmem {
 
 __global__ void __launch_bounds__(256) k_sort_scatter(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
-  if (!d.slrme) return;
+  if (!d.slrme || d.fit_owner) return;
   const int tile = blockIdx.x;
   if (tile >= d.sort_tiles) return;
   extern __shared__ __align__(16) uint8_t sm_raw[];
   ScatterSmem& sm = *reinterpret_cast<ScatterSmem*>(sm_raw);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long t0 = (long long)tile * kSortTile;
-  const int tn = (int)min((long long)kSortTile, d.n - t0);
-  const uint32_t* px = reinterpret_cast<const uint32_t*>(d.rgbe);
+  const int tn = (int)min((long long)kSortTile, d.fit_m - t0);
+  const long long pb = d.fit_p0;  // desc pixel of sample 0
+  const uint32_t* px = reinterpret_cast<const uint32_t*>(d.rgbe) + pb;
+  const long long m = d.fit_m;
   const bool real = d.sigma_milli != 0;
   if (d.global_regression) {  // whole planes in raster order: identity placement
     for (int k = threadIdx.x; k < tn; k += blockDim.x) {
@@ -111,8 +113,9 @@ __global__ void __launch_bounds__(256) k_sort_scatter(const ImgDesc* __restrict_
       const uint32_t q = px[p];
 #pragma unroll
       for (int c = 0; c < 3; c++) {
-        d.xs[(long long)c * d.n + p] = real ? d.sstar[(long long)c * d.n + p] : (double)d.s_planes[(long long)c * d.n + p];
-        d.ys[(long long)c * d.n + p] = (uint8_t)((q >> (8 * c)) & 0xFF);
+        d.xs[(long long)c * m + p] =
+            real ? d.sstar[(long long)c * d.n + pb + p] : (double)d.s_planes[(long long)c * d.n + pb + p];
+        d.ys[(long long)c * m + p] = (uint8_t)((q >> (8 * c)) & 0xFF);
       }
     }
     return;
@@ -169,7 +172,8 @@ __global__ void __launch_bounds__(256) k_sort_scatter(const ImgDesc* __restrict_
       const unsigned slot = sm.wcnt[w][e] + __popc(peers & lt);
 #pragma unroll
       for (int c = 0; c < 3; c++) {
-        sm.xs[c][slot] = real ? d.sstar[(long long)c * d.n + p] : (double)d.s_planes[(long long)c * d.n + p];
+        sm.xs[c][slot] =
+            real ? d.sstar[(long long)c * d.n + pb + p] : (double)d.s_planes[(long long)c * d.n + pb + p];
         sm.ys[c][slot] = (uint8_t)((q >> (8 * c)) & 0xFF);
       }
       sm.es[slot] = (uint8_t)e;
@@ -184,8 +188,8 @@ __global__ void __launch_bounds__(256) k_sort_scatter(const ImgDesc* __restrict_
     const long long gpos = (long long)sm.g_off[e] + (q - sm.loc_off[e]);
 #pragma unroll
     for (int c = 0; c < 3; c++) {
-      d.xs[(long long)c * d.n + gpos] = sm.xs[c][q];
-      d.ys[(long long)c * d.n + gpos] = sm.ys[c][q];
+      d.xs[(long long)c * m + gpos] = sm.xs[c][q];
+      d.ys[(long long)c * m + gpos] = sm.ys[c][q];
     }
   }
 }
@@ -202,7 +206,7 @@ __device__ __forceinline__ SegView seg_view(const ImgDesc& d, int s) {
   int e = s & 255;
   SegView v;
   if (d.global_regression) {
-    v.n = e == 0 ? d.n : 0;
+    v.n = e == 0 ? d.fit_m : 0;
     v.off = 0;
     v.identity = true;
   } else {
@@ -219,7 +223,7 @@ struct XAcc {  // x[i] = S*_c of the i-th sample of a segment (contiguous after 
 };
 
 __device__ __forceinline__ XAcc x_acc(const ImgDesc& d, int c, const SegView& v) {
-  return XAcc{d.xs + (long long)c * d.n + v.off};
+  return XAcc{d.xs + (long long)c * d.fit_m + v.off};
 }
 
 __global__ void k_seg_setup(const ImgDesc* __restrict__ descs) {
@@ -416,7 +420,7 @@ __global__ void __launch_bounds__(32) k_seg_dot(const ImgDesc* __restrict__ desc
   const int lane = threadIdx.x & 31;
   const int c = s >> 8;
   const XAcc X = x_acc(d, c, v);
-  const MAcc M{d.ys + (long long)c * d.n + v.off};
+  const MAcc M{d.ys + (long long)c * d.fit_m + v.off};
   const int T = (v.n > 10000 && d.blas_threads > 1) ? min(d.blas_threads, kMaxBlasThreads) : 1;
   if (lane == 0)
     for (int k = 0; k < kStages; k++) mbar_init(&sm.bar[k], 1);
@@ -608,17 +612,65 @@ __global__ void __launch_bounds__(256) k_seg_reduce_coef(const ImgDesc* __restri
   if (!isfinite(a32) || !isfinite(b32)) atomicOr(d.status, kErrNonFinite);
 }
 
-void launch_fit(const ImgDesc* d_descs, int nimg, int max_sort_tiles, long long max_nodes, int max_chunks,
-                cudaStream_t st) {
+void launch_fit_sort(const ImgDesc* d_descs, int nimg, int max_sort_tiles, cudaStream_t st) {
   k_sort_hist<<<dim3(max_sort_tiles, nimg), 256, 0, st>>>(d_descs);
   k_sort_scan<<<nimg, 256, 0, st>>>(d_descs);
   cudaFuncSetAttribute(k_sort_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ScatterSmem));
   k_sort_scatter<<<dim3(max_sort_tiles, nimg), 256, sizeof(ScatterSmem), st>>>(d_descs);
+}
+
+void launch_fit_bins(const ImgDesc* d_descs, int nimg, long long max_nodes, int max_chunks, cudaStream_t st) {
   k_seg_setup<<<nimg, 32, 0, st>>>(d_descs);
   k_seg_nodes<<<dim3((unsigned)((max_nodes + 3) / 4), nimg), 128, 0, st>>>(d_descs);
   cudaFuncSetAttribute(k_seg_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DotSmem));
   k_seg_dot<<<dim3(kSegs, nimg, max_chunks), 32, sizeof(DotSmem), st>>>(d_descs);
   k_seg_reduce_coef<<<dim3(kSegs, nimg), 256, 0, st>>>(d_descs);
+}
+
+void launch_fit(const ImgDesc* d_descs, int nimg, int max_sort_tiles, long long max_nodes, int max_chunks,
+                cudaStream_t st) {
+  launch_fit_sort(d_descs, nimg, max_sort_tiles, st);
+  launch_fit_bins(d_descs, nimg, max_nodes, max_chunks, st);
+}
+
+// ---------------------------------------------------------------------------
+// Tile-sharded fit: an owner rank's received samples, one chunk per source
+// rank ([3][m] f64 S*, then [3][m] u8 M, each chunk sorted by exponent), are
+// regrouped bin-major with the sources in rank order inside a bin -- which is
+// raster order, since the bands are contiguous row ranges.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_fit_regroup(const ImgDesc* __restrict__ descs, RegroupTab rt) {
+  const ImgDesc& d = descs[0];
+  const long long M = d.fit_m;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < rt.total;
+       i += (long long)gridDim.x * blockDim.x) {
+    int r = 0;  // source chunk: cumulative sample counts
+    long long before = 0;
+    while (r + 1 < rt.nsrc && before + rt.src_m[r] <= i) before += rt.src_m[r++];
+    const long long j = i - before, m = rt.src_m[r];
+    const unsigned* bo = rt.src_bin_off + (long long)r * 257;
+    int lo = 0, hi = 256;  // bin e with bo[e] <= j < bo[e+1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (bo[mid] <= j) lo = mid; else hi = mid;
+    }
+    const long long dst = (long long)rt.dst_bin_off[r * 256 + lo] + (j - bo[lo]);
+    const uint8_t* chunk = rt.recv + rt.src_off[r];
+    const double* x = reinterpret_cast<const double*>(chunk);
+    const uint8_t* y = chunk + 24 * m;
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      d.xs[c * M + dst] = x[c * m + j];
+      d.ys[c * M + dst] = y[c * m + j];
+    }
+  }
+}
+
+void launch_fit_regroup(const ImgDesc* d_desc, const RegroupTab& rt, cudaStream_t st) {
+  if (rt.total <= 0) return;
+  long long blocks = (rt.total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_fit_regroup<<<(unsigned)blocks, 256, 0, st>>>(d_desc, rt);
 }
 
 }  // namespace hdll

@@ -35,28 +35,37 @@ __device__ __forceinline__ double luminance(double r, double g, double b) {
   return 0.2126 * r + 0.7152 * g + 0.0722 * b;
 }
 
-// Pass A: 4 pixels per thread via one 128-bit load.
+// Pass A over full-image pixels [px0, px1): 4 pixels per thread (one 128-bit
+// load when aligned).  logv and rgbe are indexed in desc pixels (p - pix_base).
 __global__ void __launch_bounds__(256) k_lum_log(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
-  long long nq = (d.n + 3) / 4;
+  const long long q0 = d.px0 - d.pix_base, q1 = d.px1 - d.pix_base;  // desc pixels
+  const long long lead = (4 - (q0 & 3)) & 3;                         // pixels before the first aligned quad
+  const long long nq = (q1 - q0 - lead + 3) / 4;
   double mx = 0.0;
-  for (long long qi = (long long)blockIdx.x * blockDim.x + threadIdx.x; qi < nq;
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(d.rgbe);
+  for (long long qi = (long long)blockIdx.x * blockDim.x + threadIdx.x; qi < nq + 1;
        qi += (long long)gridDim.x * blockDim.x) {
-    long long p0 = qi * 4;
-    uint4 v;
-    if (p0 + 3 < d.n) {
-      v = __ldg(reinterpret_cast<const uint4*>(d.rgbe) + qi);
+    long long p0;
+    int cnt;
+    uint32_t qs[4];
+    if (qi == nq) {  // the unaligned lead pixels
+      p0 = q0;
+      cnt = (int)min(lead, q1 - q0);
+      for (int k = 0; k < cnt; k++) qs[k] = src[p0 + k];
     } else {
-      const uint32_t* src = reinterpret_cast<const uint32_t*>(d.rgbe);
-      v.x = src[p0];
-      v.y = p0 + 1 < d.n ? src[p0 + 1] : 0u;
-      v.z = p0 + 2 < d.n ? src[p0 + 2] : 0u;
-      v.w = p0 + 3 < d.n ? src[p0 + 3] : 0u;
+      p0 = q0 + lead + qi * 4;
+      cnt = (int)min(4LL, q1 - p0);
+      if (cnt == 4) {
+        uint4 v = __ldg(reinterpret_cast<const uint4*>(src + p0));
+        qs[0] = v.x, qs[1] = v.y, qs[2] = v.z, qs[3] = v.w;
+      } else {
+        for (int k = 0; k < cnt; k++) qs[k] = src[p0 + k];
+      }
     }
-    uint32_t qs[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int k = 0; k < 4; k++) {
-      if (p0 + k >= d.n) break;
+      if (k >= cnt) break;
       double r, g, b;
       rgbe_to_rgb(qs[k], &r, &g, &b);
       double lw = luminance(r, g, b);
@@ -77,20 +86,20 @@ __global__ void __launch_bounds__(256) k_lum_log(const ImgDesc* __restrict__ des
   }
 }
 
-struct PtrAcc {
+struct PtrAcc {  // full-image index -> desc array
   const double* p;
-  __device__ double operator()(long long i) const { return p[i]; }
+  long long base;
+  __device__ double operator()(long long i) const { return p[i - base]; }
 };
 
-// Pairwise-sum depth-L nodes of every image's log array.
+// Pairwise-sum depth-L nodes [node0, node1) of every image's log array.
 __global__ void __launch_bounds__(128) k_tm_nodes(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
-  long long nn = 1LL << d.tm_level;
-  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= nn) return;
+  long long idx = d.node0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= d.node1) return;
   long long off, sz;
-  pairwise_node(d.n, d.tm_level, idx, &off, &sz);
-  d.tm_nodes[idx] = pairwise_seq(PtrAcc{d.logv}, off, sz);
+  pairwise_node(d.full_n, d.tm_level, idx, &off, &sz);
+  d.tm_nodes[idx] = pairwise_seq(PtrAcc{d.logv, d.pix_base}, off, sz);
 }
 
 // Combine the nodes, then the scalar tail of tone_map (tonemap.py:97-104).
@@ -100,7 +109,7 @@ __global__ void __launch_bounds__(256) k_tm_scalars(const ImgDesc* __restrict__ 
   double sum = tree_reduce_block(d.tm_nodes, d.tm_level, sm);
   if (threadIdx.x == 0) {
     double total = 0.0 + sum;                       // reduction initial value 0.0
-    double mean = total / (double)d.n;              // np.mean: sum / count
+    double mean = total / (double)d.full_n;         // np.mean: sum / count
     double log_avg = exp(mean);
     double maxlw = __longlong_as_double((long long)*d.maxlw);
     double white = d.white_point > 0 ? d.white_point : d.key * maxlw / log_avg;  // == scaled.max()
@@ -111,15 +120,23 @@ __global__ void __launch_bounds__(256) k_tm_scalars(const ImgDesc* __restrict__ 
   }
 }
 
-void launch_tonemap_stats(const ImgDesc* d_descs, int nimg, long long max_n, int max_level, cudaStream_t st) {
-  long long nq = (max_n + 3) / 4;
+void launch_tonemap_partial(const ImgDesc* d_descs, int nimg, long long max_n, int max_level, cudaStream_t st) {
+  long long nq = (max_n + 3) / 4 + 1;
   int gx = (int)((nq + 255) / 256);
   if (gx > 148 * 8) gx = 148 * 8;
   if (gx < 1) gx = 1;
   k_lum_log<<<dim3(gx, nimg), 256, 0, st>>>(d_descs);
   long long nn = 1LL << max_level;
   k_tm_nodes<<<dim3((unsigned)((nn + 127) / 128), nimg), 128, 0, st>>>(d_descs);
+}
+
+void launch_tonemap_scalars(const ImgDesc* d_descs, int nimg, cudaStream_t st) {
   k_tm_scalars<<<nimg, 256, 0, st>>>(d_descs);
+}
+
+void launch_tonemap_stats(const ImgDesc* d_descs, int nimg, long long max_n, int max_level, cudaStream_t st) {
+  launch_tonemap_partial(d_descs, nimg, max_n, max_level, st);
+  launch_tonemap_scalars(d_descs, nimg, st);
 }
 
 }  // namespace hdll
