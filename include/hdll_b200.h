@@ -111,6 +111,63 @@ int hdll_b200_stage_times(hdll_b200_ctx *ctx, float *ms, int n);
 
 const char *hdll_b200_status_string(int status);
 
+/* ---------------------------------------------------------------------------
+ * Tile-sharded single image (BASELINE config 3).  The reference
+ * encodes one image in one process (container.py:131-230); here each rank of
+ * a job codes a contiguous band of rows and the ranks exchange only the
+ * summaries the sequential stages need.  The phases below run in order on
+ * every rank; between them the host exchanges the named outputs (allgather,
+ * all-to-all) and passes the combined values to the next phase.  Each phase
+ * returns once its host outputs are ready.  Per rank, pieces 0..2 are the
+ * Y, Cb, Cr slices of the base-layer DCT stream and 3..6 the E, R, G, B plane
+ * streams; a chain's pieces are ordered by rank (DCT: component, then rank).
+ * ------------------------------------------------------------------------- */
+typedef struct hdll_b200_band {
+  uint32_t row0, row1;    /* rows coded by this rank; row0 % 8 == 0, row1 % 8 == 0 or row1 == height */
+  uint32_t crow0, crow1;  /* rows present at image.rgbe: the band plus halo, crow0 % 8 == 0 */
+  uint64_t node0, node1;  /* level-L pairwise nodes of the tone-map log sum this rank computes */
+} hdll_b200_band;
+
+enum { HDLL_B200_BAND_PIECES = 7, HDLL_B200_BAND_CTX = 6 };
+
+/* Phase 1.  img: full-image width/height/params; img->rgbe = device pointer to
+ * rows [crow0, crow1).  Out: the rank's node sums (node1 - node0 doubles) and
+ * its max luminance.  Exchange: allgather nodes (concatenate), max of maxlw. */
+int hdll_b200_band_begin(hdll_b200_ctx *ctx, const hdll_b200_image *img, const hdll_b200_band *band, void *stream,
+                         double *h_nodes, double *h_maxlw);
+/* Phase 2: tone-map scalars from all 2^L nodes, base layer, prefilter, sort of
+ * the band's fit samples by exponent.  Out: the band's exponent histogram. */
+int hdll_b200_band_layers(hdll_b200_ctx *ctx, const double *h_nodes_all, uint64_t n_nodes, double maxlw,
+                          uint32_t *h_hist);
+/* Phase 3: pack the sorted samples for their owners (owner o fits exponents
+ * [owner_lo[o], owner_lo[o+1])) into d_send; h_send_bytes[o] = chunk sizes.
+ * Exchange: all-to-all of the chunks. */
+int hdll_b200_band_fit_send(hdll_b200_ctx *ctx, const uint32_t *owner_lo, int nowners, uint8_t *d_send,
+                            uint64_t send_cap, uint64_t *h_send_bytes);
+/* Phase 4 (owner): fit exponents [e_lo, e_hi) from the received chunks (one per
+ * source rank, h_hist = every source's histogram).  Out: a32/b32 [3][256]
+ * (owned entries), error bits.  Exchange: allgather of the tables. */
+int hdll_b200_band_fit_owner(hdll_b200_ctx *ctx, const uint8_t *d_recv, const uint64_t *h_recv_bytes,
+                             const uint32_t *h_hist, int nsrc, uint32_t e_lo, uint32_t e_hi, float *h_a32,
+                             float *h_b32, uint32_t *h_status);
+/* Phase 5: estimate with the full table, CRCs of the band's rows, context
+ * counts of every piece.  Out: crc[5], counts [7][6].  Exchange: allgather counts. */
+int hdll_b200_band_code(hdll_b200_ctx *ctx, const float *h_a32, const float *h_b32, uint32_t *h_crc,
+                        int64_t *h_cnt);
+/* Phase 6: A-maps of every piece given the counts before it.  Out: [7][6][3]
+ * (c, s, t of common.cuh AMap).  Exchange: allgather maps. */
+int hdll_b200_band_maps(hdll_b200_ctx *ctx, const int64_t *h_in_cnt, int64_t *h_maps);
+/* Phase 7: code every piece given its entering A.  Out: bit lengths [7] and
+ * the device addresses of the piece streams (valid until the next begin). */
+int hdll_b200_band_emit(hdll_b200_ctx *ctx, const int32_t *h_in_a, uint64_t *h_bits, uint64_t *h_piece_ptr);
+/* Rank 0: concatenate the pieces of the 5 chains (npieces[k] each, in order;
+ * piece_ptr device addresses, piece_bits lengths) and serialize the stream
+ * with the combined CRCs, table and full-image exponent histogram. */
+int hdll_b200_assemble_pieces(hdll_b200_ctx *ctx, const hdll_b200_image *img, const uint32_t *crc,
+                              const float *a32, const float *b32, const uint32_t *hist, const int32_t *npieces,
+                              const uint64_t *piece_ptr, const uint64_t *piece_bits, uint8_t *d_out, uint64_t cap,
+                              uint64_t *d_len, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

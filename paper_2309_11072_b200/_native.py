@@ -22,7 +22,11 @@ EXPORTS = (
     "hdll_b200_encode_batch_device", "hdll_b200_sync", "hdll_b200_encode_host", "hdll_b200_trace",
     "hdll_b200_lossless_encode_plane", "hdll_b200_lossy_encode", "hdll_b200_last_launch_count",
     "hdll_b200_stage_times", "hdll_b200_status_string",
+    "hdll_b200_band_begin", "hdll_b200_band_layers", "hdll_b200_band_fit_send", "hdll_b200_band_fit_owner",
+    "hdll_b200_band_code", "hdll_b200_band_maps", "hdll_b200_band_emit", "hdll_b200_assemble_pieces",
 )
+
+BAND_PIECES, BAND_CTX = 7, 6
 
 
 class Params(ctypes.Structure):
@@ -43,6 +47,11 @@ class Image(ctypes.Structure):
         ("hdr_post", ctypes.c_void_p), ("hdr_post_len", ctypes.c_uint32),
         ("params", Params),
     ]
+
+
+class Band(ctypes.Structure):
+    _fields_ = [("row0", ctypes.c_uint32), ("row1", ctypes.c_uint32), ("crow0", ctypes.c_uint32),
+                ("crow1", ctypes.c_uint32), ("node0", ctypes.c_uint64), ("node1", ctypes.c_uint64)]
 
 
 _lib = None
@@ -87,6 +96,23 @@ def lib():
             L.hdll_b200_stage_times.restype = ctypes.c_int
             L.hdll_b200_status_string.argtypes = [ctypes.c_int]
             L.hdll_b200_status_string.restype = ctypes.c_char_p
+            dp, i64p = ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)
+            u32p, f32p = ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_float)
+            sig = {
+                "hdll_b200_band_begin": [vp, ctypes.POINTER(Image), ctypes.POINTER(Band), vp, dp, dp],
+                "hdll_b200_band_layers": [vp, dp, ctypes.c_uint64, ctypes.c_double, u32p],
+                "hdll_b200_band_fit_send": [vp, u32p, ctypes.c_int, vp, ctypes.c_uint64, u64p],
+                "hdll_b200_band_fit_owner": [vp, vp, u64p, u32p, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32,
+                                             f32p, f32p, u32p],
+                "hdll_b200_band_code": [vp, f32p, f32p, u32p, i64p],
+                "hdll_b200_band_maps": [vp, i64p, i64p],
+                "hdll_b200_band_emit": [vp, ctypes.POINTER(ctypes.c_int32), u64p, u64p],
+                "hdll_b200_assemble_pieces": [vp, ctypes.POINTER(Image), u32p, f32p, f32p, u32p,
+                                              ctypes.POINTER(ctypes.c_int32), u64p, u64p, vp, ctypes.c_uint64, vp, vp],
+            }
+            for name, args in sig.items():
+                getattr(L, name).argtypes = args
+                getattr(L, name).restype = ctypes.c_int
             _lib = L
     return _lib
 

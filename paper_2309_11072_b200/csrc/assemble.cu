@@ -146,6 +146,54 @@ __global__ void __launch_bounds__(256) k_assemble(const ImgDesc* __restrict__ de
   }
 }
 
+// ---------------------------------------------------------------------------
+// Bit concatenation (tile-sharded images): piece p's nbits[p] MSB-first bits
+// are OR-ed into dst at bit dst_bit[p].  Words shared with a neighbouring
+// piece (a piece's first and last) use atomicOr; dst starts zeroed.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t be_word(const uint8_t* p, long long k) {
+  return __byte_perm(reinterpret_cast<const uint32_t*>(p)[k], 0, 0x0123);
+}
+
+__global__ void __launch_bounds__(256) k_bitcat(uint8_t* dst, const uint8_t* const* src,
+                                                const unsigned long long* dst_bit, const unsigned long long* nbits) {
+  const int piece = blockIdx.y;
+  const long long L = (long long)nbits[piece];
+  if (L == 0) return;
+  const long long o = (long long)dst_bit[piece];
+  const uint8_t* sp = src[piece];
+  const long long w0 = o >> 5, w1 = (o + L - 1) >> 5, last_src = (L - 1) >> 5;
+  uint32_t* out = reinterpret_cast<uint32_t*>(dst);
+  for (long long w = w0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; w <= w1;
+       w += (long long)gridDim.x * blockDim.x) {
+    const long long off = 32 * w - o;  // source bit at the word's first bit
+    uint32_t v;
+    if (off < 0) {
+      v = be_word(sp, 0) >> (int)(-off);
+    } else {
+      const long long k = off >> 5;
+      const int sh = (int)(off & 31);
+      v = be_word(sp, k) << sh;
+      if (sh && k + 1 <= last_src) v |= be_word(sp, k + 1) >> (32 - sh);
+    }
+    const long long valid = L - off;  // source bits left from the word's first bit
+    if (valid < 32) v &= ~0u << (32 - valid);
+    const uint32_t le = __byte_perm(v, 0, 0x0123);
+    if (w == w0 || w == w1) atomicOr(out + w, le);
+    else out[w] = le;
+  }
+}
+
+void launch_bitcat(uint8_t* dst, const uint8_t* const* src, const unsigned long long* dst_bit,
+                   const unsigned long long* nbits, int npieces, unsigned long long max_bits, cudaStream_t st) {
+  if (npieces <= 0) return;
+  long long words = (long long)(max_bits / 32) + 2;
+  long long bx = (words + 255) / 256;
+  if (bx > 148 * 4) bx = 148 * 4;
+  if (bx < 1) bx = 1;
+  k_bitcat<<<dim3((unsigned)bx, npieces), 256, 0, st>>>(dst, src, dst_bit, nbits);
+}
+
 void launch_assemble(const ImgDesc* d_descs, int nimg, const AsmTab& at, long long max_out, cudaStream_t st) {
   long long blocks = (max_out + 256 * 16 - 1) / (256 * 16);
   if (blocks > 148 * 8) blocks = 148 * 8;

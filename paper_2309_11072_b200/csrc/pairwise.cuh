@@ -21,7 +21,7 @@
 namespace hdll {
 
 // (offset, size) of node `idx` at depth L of the pairwise tree over n elements.
-__device__ __forceinline__ void pairwise_node(long long n, int L, long long idx, long long* off, long long* size) {
+__host__ __device__ __forceinline__ void pairwise_node(long long n, int L, long long idx, long long* off, long long* size) {
   long long o = 0, m = n;
   for (int l = L - 1; l >= 0; l--) {
     long long n2 = m / 2;
