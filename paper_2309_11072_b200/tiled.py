@@ -341,9 +341,11 @@ def _prefix_states(cnts, maps_or_none, world):
     return in_cnt, in_a
 
 
-def encode_band(ex, prep, rows_ptr: int, spec: BandSpec, ctx, stream_handle: int, device):
+def encode_band(ex, prep, rows_ptr: int, spec: BandSpec, ctx, stream_handle: int, device, out=None):
     """Run one rank's band of a tile-sharded encode.  rows_ptr: device RGBE rows
-    [spec.crow0, spec.crow1).  Rank 0 returns the serialized stream (bytes)."""
+    [spec.crow0, spec.crow1).  Rank 0 returns the serialized stream (bytes), or,
+    given `out` = (device uint8 buffer of stream_capacity bytes, device int64[1]),
+    leaves it there and returns its length."""
     import torch
 
     L = _native.lib()
@@ -450,8 +452,11 @@ def encode_band(ex, prep, rows_ptr: int, spec: BandSpec, ctx, stream_handle: int
         crc_full[j] = acc
     hist_u32 = np.ascontiguousarray(hist_total.astype(np.uint32))
     cap = container.stream_capacity(prep)
-    d_out = torch.empty(cap, dtype=torch.uint8, device=device)
-    d_len = torch.zeros(1, dtype=torch.int64, device=device)
+    if out is not None:
+        d_out, d_len = out
+    else:
+        d_out = torch.empty(cap, dtype=torch.uint8, device=device)
+        d_len = torch.zeros(1, dtype=torch.int64, device=device)
     imf = container._image_struct(prep, 0)
     _native.check(L.hdll_b200_assemble_pieces(h, ctypes.byref(imf), _ptr(crc_full, ctypes.c_uint32),
                                               _ptr(A32, ctypes.c_float), _ptr(B32, ctypes.c_float),
@@ -459,10 +464,10 @@ def encode_band(ex, prep, rows_ptr: int, spec: BandSpec, ctx, stream_handle: int
                                               _ptr(pp, ctypes.c_uint64), _ptr(pb, ctypes.c_uint64), d_out.data_ptr(),
                                               cap, d_len.data_ptr(), stream_handle), "assemble_pieces")
     n = int(d_len.item())
-    out = bytes(d_out[:n].cpu().numpy())
+    res = n if out is not None else bytes(d_out[:n].cpu().numpy())
     del keep
     ex.barrier()
-    return out
+    return res
 
 
 # ---------------------------------------------------------------------------
