@@ -99,19 +99,37 @@ __global__ void __launch_bounds__(128, 4) k_base_layer(const ImgDesc* __restrict
   TmoConst tc;
   tc.g32 = (float)d.inv_gamma;
 
-  // 1. SDR (tone-map pass B) and YCC for every padded pixel of the tile
+  // 1. SDR (tone-map pass B) and YCC for every padded pixel of the tile:
+  //    thread t owns column t, rows 0..7; its 8 RGBE words are loaded up front
   unsigned amb = 0;  // samples the fp32 pow could not certify
-  for (int p = t; p < 8 * kTileCols; p += blockDim.x) {
-    int ry = p / kTileCols, rx = p % kTileCols;
-    if (rx >= nblk * 8) continue;
-    int y = by * 8 + ry, x = bx0 * 8 + rx;
-    int sy = min(y, d.h - 1), sx = min(x, d.w - 1);  // np.pad mode="edge"
+  const int rx = t;
+  const bool col_live = rx < nblk * 8;
+  const int x = bx0 * 8 + rx, sx = min(x, d.w - 1);  // np.pad mode="edge"
+  uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0, w4 = 0, w5 = 0, w6 = 0, w7 = 0;
+  if (col_live && !d.sdr_in) {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(d.rgbe) + sx;
+    const long long W = d.w;
+    const int y0 = by * 8, hm = d.h - 1;
+    w0 = __ldg(src + min(y0 + 0, hm) * W);
+    w1 = __ldg(src + min(y0 + 1, hm) * W);
+    w2 = __ldg(src + min(y0 + 2, hm) * W);
+    w3 = __ldg(src + min(y0 + 3, hm) * W);
+    w4 = __ldg(src + min(y0 + 4, hm) * W);
+    w5 = __ldg(src + min(y0 + 5, hm) * W);
+    w6 = __ldg(src + min(y0 + 6, hm) * W);
+    w7 = __ldg(src + min(y0 + 7, hm) * W);
+  }
+#pragma unroll 1
+  for (int ry = 0; ry < 8 && col_live; ry++) {
+    const int y = by * 8 + ry;
+    const int sy = min(y, d.h - 1);
     uint8_t s3[3];
     if (d.sdr_in) {
       const uint8_t* sp = d.sdr_in + ((long long)sy * d.w + sx) * 3;
       s3[0] = sp[0], s3[1] = sp[1], s3[2] = sp[2];
     } else {
-      uint32_t q = reinterpret_cast<const uint32_t*>(d.rgbe)[(long long)sy * d.w + sx];
+      const uint32_t q = w0;
+      w0 = w1, w1 = w2, w2 = w3, w3 = w4, w4 = w5, w5 = w6, w6 = w7;
       sdr_pixel(d, q, log_avg, white, tc, allzero, s3, &amb);
     }
     if (d.want_trace && y < d.h && x < d.w) {

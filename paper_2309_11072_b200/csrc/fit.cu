@@ -244,7 +244,7 @@ __global__ void k_seg_setup(const ImgDesc* __restrict__ descs) {
 __global__ void __launch_bounds__(128) k_seg_nodes(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
   if (!d.slrme) return;
-  __shared__ double leaves[4][kMaxLeaves];
+  __shared__ PwScratch pw[4];
   const int warp = threadIdx.x >> 5;
   const long long g = (long long)blockIdx.x * 4 + warp;
   if (g >= d.seg_node_off[kSegs]) return;
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(128) k_seg_nodes(const ImgDesc* __restrict__ d
   SegView v = seg_view(d, s);
   long long off, sz;
   pairwise_node(v.n, d.seg_level[s], g - d.seg_node_off[s], &off, &sz);
-  const double r = warp_pairwise(x_acc(d, s >> 8, v), off, sz, leaves[warp]);
+  const double r = warp_pairwise(x_acc(d, s >> 8, v), off, sz, pw[warp]);
   if ((threadIdx.x & 31) == 0) d.seg_nodes[g] = r;
 }
 

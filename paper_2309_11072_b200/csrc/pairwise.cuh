@@ -74,28 +74,76 @@ __device__ double pairwise_seq(const Acc& a, long long off, long long n) {
 // time by groups of 8 lanes -- lane j of a group is numpy's accumulator r[j],
 // so every addition happens in numpy's order -- then lane 0 combines the leaf
 // sums along the recursion tree.  Result in every lane.
+//
+// The recursion is walked without a stack: a node is its path from the root
+// (bit q = went right at depth q), recomputed from the root when the walk
+// moves to the next leaf, so all state stays in registers; the combine keeps
+// one pending left-sibling sum per depth in shared memory.
 constexpr int kMaxLeaves = 160;  // n <= 8192
 
-static __device__ __noinline__ double pairwise_combine(const double* leaf, int* li, long long m) {
-  if (m <= 128) return leaf[(*li)++];
-  long long n2 = m / 2;
-  n2 -= n2 % 8;
-  double left = pairwise_combine(leaf, li, n2);
-  return left + pairwise_combine(leaf, li, m - n2);
+struct PwScratch {
+  double leaf[kMaxLeaves];
+  long long lo[kMaxLeaves];
+  int ln[kMaxLeaves];
+  double pending[32];
+};
+
+__device__ __forceinline__ long long pw_split(long long m) {
+  const long long n2 = m / 2;
+  return n2 - n2 % 8;
+}
+
+// f(index, leaf offset, leaf size, path, depth) for every leaf, left to right
+template <class F>
+__device__ __forceinline__ void pw_leaves(long long off, long long n, F&& f) {
+  unsigned path = 0;
+  int depth = 0;
+  long long lo = off, m = n;
+  while (m > 128) {
+    m = pw_split(m);
+    depth++;
+  }
+  for (int idx = 0;; idx++) {
+    f(idx, lo, m, path, depth);
+    int k = depth - 1;  // deepest left turn
+    while (k >= 0 && ((path >> k) & 1u)) k--;
+    if (k < 0) break;
+    path = (path & ((1u << k) - 1u)) | (1u << k);
+    depth = k + 1;
+    lo = off;
+    m = n;
+    for (int q = 0; q < depth; q++) {
+      const long long n2 = pw_split(m);
+      if ((path >> q) & 1u) {
+        lo += n2;
+        m -= n2;
+      } else {
+        m = n2;
+      }
+    }
+    while (m > 128) {
+      m = pw_split(m);
+      depth++;
+    }
+  }
 }
 
 template <class Acc>
-__device__ double warp_pairwise(const Acc& a, long long off, long long n, double* leaf_buf /* kMaxLeaves */) {
+__device__ double warp_pairwise(const Acc& a, long long off, long long n, PwScratch& sc) {
   const int lane = threadIdx.x & 31, grp = lane >> 3, j = lane & 7;
-  long long st_off[24], st_n[24];
-  int sp = 0, nleaf = 0, nb = 0;
-  long long boff[4], bn[4];
-  st_off[0] = off;
-  st_n[0] = n;
-  sp = 1;
-  auto flush = [&]() {
-    const bool mine = grp < nb;
-    const long long lo = mine ? boff[grp] : 0, ln = mine ? bn[grp] : 0;
+  int nleaf = 0;
+  if (lane == 0)
+    pw_leaves(off, n, [&](int idx, long long lo, long long m, unsigned, int) {
+      sc.lo[idx] = lo;
+      sc.ln[idx] = (int)m;
+      nleaf = idx + 1;
+    });
+  nleaf = __shfl_sync(0xffffffffu, nleaf, 0);
+  __syncwarp();
+  for (int base = 0; base < nleaf; base += 4) {
+    const int li = base + grp;
+    const bool mine = li < nleaf;
+    const long long lo = mine ? sc.lo[li] : 0, ln = mine ? sc.ln[li] : 0;
     const long long lim = ln - (ln % 8);
     double r = 0.0;
     if (mine && ln >= 8) {
@@ -120,37 +168,23 @@ __device__ double warp_pairwise(const Acc& a, long long off, long long n, double
         res = s8;
         for (long long i = lim; i < ln; i++) res += a(lo + i);
       }
-      leaf_buf[nleaf - nb + grp] = res;
-    }
-    nb = 0;
-  };
-  while (sp > 0) {  // depth first, left to right: leaves come out in order
-    sp--;
-    const long long o = st_off[sp], m = st_n[sp];
-    if (m <= 128) {
-      boff[nb] = o;
-      bn[nb] = m;
-      nb++;
-      nleaf++;
-      if (nb == 4) flush();
-    } else {
-      long long n2 = m / 2;
-      n2 -= n2 % 8;
-      st_off[sp] = o + n2;
-      st_n[sp] = m - n2;
-      sp++;
-      st_off[sp] = o;
-      st_n[sp] = n2;
-      sp++;
+      sc.leaf[li] = res;
     }
   }
-  if (nb) flush();
   __syncwarp();
   double out = 0.0;
-  if (lane == 0) {
-    int li = 0;
-    out = pairwise_combine(leaf_buf, &li, n);
-  }
+  if (lane == 0)
+    pw_leaves(off, n, [&](int idx, long long, long long, unsigned path, int depth) {
+      double v = sc.leaf[idx];
+      int dd = depth;
+      while (dd > 0 && ((path >> (dd - 1)) & 1u)) {  // a right child completes its parent: left + right
+        v = sc.pending[dd - 1] + v;
+        dd--;
+      }
+      if (dd == 0) out = v;
+      else sc.pending[dd - 1] = v;
+    });
+  __syncwarp();
   return __shfl_sync(0xffffffffu, out, 0);
 }
 
