@@ -73,7 +73,7 @@ struct ImgDesc {
 
   // SLRME fit
   int sort_tiles;             // tiles of kSortTile pixels
-  unsigned* tile_hist;        // [sort_tiles][256] (then tile offsets)
+  unsigned* tile_hist;        // [256][sort_tiles] (then tile offsets)
   double* xs;                 // [3][n]: S* samples stable-sorted by E (raster order inside a bin)
   uint8_t* ys;                // [3][n]: M samples in the same order
   unsigned* bin_count;        // 256
@@ -109,7 +109,7 @@ struct ImgDesc {
 };
 
 constexpr int kMaxBlasThreads = 64;
-constexpr int kSortTile = 2048;
+constexpr int kSortTile = 1024;
 constexpr int kCrcChunk = 1024;       // bytes per CRC partial
 constexpr int kNodeTarget = 1024;     // pairwise-sum level-L node size target
 

@@ -50,34 +50,46 @@ __global__ void __launch_bounds__(256) k_sort_hist(const ImgDesc* __restrict__ d
   }
   __syncthreads();
   for (int e = threadIdx.x; e < 256; e += blockDim.x) {
-    d.tile_hist[(long long)tile * 256 + e] = hist[e];
+    d.tile_hist[(long long)e * d.sort_tiles + tile] = hist[e];
     if (hist[e]) atomicAdd(&d.bin_count[e], hist[e]);
   }
 }
 
-// bin starts + per-tile absolute offsets (in place over tile_hist)
+// bin starts + per-tile absolute offsets (in place over tile_hist, bin-major
+// [256][sort_tiles]): one CTA per bin, threads scan contiguous runs of tiles
 __global__ void __launch_bounds__(256) k_sort_scan(const ImgDesc* __restrict__ descs) {
-  const ImgDesc& d = descs[blockIdx.x];
+  const ImgDesc& d = descs[blockIdx.y];
   if (!d.slrme || d.fit_owner) return;
-  const int e = threadIdx.x;
-  __shared__ unsigned cnt[256];
-  cnt[e] = d.bin_count[e];
-  __syncthreads();
-  if (e == 0) {
-    unsigned run = 0;
-    for (int k = 0; k < 256; k++) {
-      d.bin_start[k] = run;
-      run += cnt[k];
+  const int e = blockIdx.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
+  __shared__ unsigned s_below, wsum[8];
+  if (w == 0) {  // bin start: counts of the lower bins
+    unsigned below = 0;
+    for (int k = lane; k < e; k += 32) below += d.bin_count[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
+    if (lane == 0) {
+      s_below = below;
+      d.bin_start[e] = below;
+      if (e == 255) d.bin_start[256] = below + d.bin_count[255];
     }
-    d.bin_start[256] = run;
   }
+  const long long T = d.sort_tiles;
+  unsigned* row = d.tile_hist + (long long)e * T;
+  const long long per = (T + 255) / 256;
+  const long long t0 = min(T, t * per), t1 = min(T, t0 + per);
+  unsigned run = 0;
+#pragma unroll 4
+  for (long long k = t0; k < t1; k++) run += row[k];
+  unsigned wt;
+  unsigned off = warp_excl_sum(run, &wt);
+  if (lane == 0) wsum[w] = wt;
   __syncthreads();
-  unsigned run = d.bin_start[e];
-  for (int t = 0; t < d.sort_tiles; t++) {
-    unsigned* slot = &d.tile_hist[(long long)t * 256 + e];
-    unsigned c = *slot;
-    *slot = run;
-    run += c;
+  for (int k = 0; k < w; k++) off += wsum[k];
+  off += s_below;
+  for (long long k = t0; k < t1; k++) {
+    const unsigned c = row[k];
+    row[k] = off;
+    off += c;
   }
 }
 
@@ -150,7 +162,7 @@ __global__ void __launch_bounds__(256) k_sort_scatter(const ImgDesc* __restrict_
     const unsigned off = pre + ex;
     sm.loc_off[e] = off;
     if (e == 255) sm.loc_off[256] = off + tot;
-    sm.g_off[e] = d.tile_hist[(long long)tile * 256 + e];
+    sm.g_off[e] = d.tile_hist[(long long)e * d.sort_tiles + tile];
     unsigned run = off;
     for (int k = 0; k < 8; k++) {
       unsigned c = sm.wcnt[k][e];
@@ -614,7 +626,7 @@ __global__ void __launch_bounds__(256) k_seg_reduce_coef(const ImgDesc* __restri
 
 void launch_fit_sort(const ImgDesc* d_descs, int nimg, int max_sort_tiles, cudaStream_t st) {
   k_sort_hist<<<dim3(max_sort_tiles, nimg), 256, 0, st>>>(d_descs);
-  k_sort_scan<<<nimg, 256, 0, st>>>(d_descs);
+  k_sort_scan<<<dim3(256, nimg), 256, 0, st>>>(d_descs);
   cudaFuncSetAttribute(k_sort_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ScatterSmem));
   k_sort_scatter<<<dim3(max_sort_tiles, nimg), 256, sizeof(ScatterSmem), st>>>(d_descs);
 }
