@@ -8,12 +8,13 @@
 //
 // Parallel form.  A *chain* is one sequential coder invocation (one DCT stream
 // per image, one plane stream per (image, plane)); it is cut into *tiles*
-// (a plane row, or 32 consecutive DCT blocks of one component), one warp per
-// tile, lane = contiguous slice of the tile.  The symbols of a tile depend
-// only on the data; the coder state carried between tiles is, per context,
-// (count, A).  Each warp generates its tile's symbols once into shared memory,
-// then runs three chained decoupled look-backs (tickets are dealt round-robin
-// over the chains in order, so every wait is on an older, running warp):
+// (32 plane rows, or 32 consecutive DCT blocks of one component), one warp per
+// tile, lane = one row / one block: a contiguous range of the chain's symbols.
+// The symbols of a tile depend only on the data; the coder state carried
+// between tiles is, per context, (count, A).  Each warp derives its lanes'
+// symbols from the data (once per pass) and runs three chained decoupled
+// look-backs (tickets are dealt round-robin over the chains in order, so every
+// wait is on an older, running warp):
 //   1. counts per context  -> global symbol index (halving points, N)
 //   2. A-maps per context  -> incoming A of the tile (common.cuh AMap)
 //   3. code lengths        -> bit offset of the tile in its chain
@@ -221,37 +222,13 @@ struct LaneBits {
 
 // ---------------------------------------------------------------------------
 // Symbol sources.  A generator enumerates a lane's symbols in coder order as
-// f(index, ctx, value, raw_len, raw_bits).  The plane coder keeps its symbols
-// in shared memory (u16: k << 11 | ctx << 8 | value) and records k there in the
-// length pass; the DCT coder re-derives them from the block each pass and the
-// emit pass re-runs the context state to recover k.
+// f(index, ctx, value, raw_len, raw_bits), re-deriving them from the data on
+// every pass (DCT blocks below, plane rows further down).
 // ---------------------------------------------------------------------------
-struct PlaneList {
-  static constexpr bool kStoresK = true;
-  uint16_t* syms;
-  int n;
-  template <class F>
-  __device__ __forceinline__ void for_each(F&& f) const {
-    for (int i = 0; i < n; i++) {
-      const uint16_t s = syms[i];
-      f(i, (s >> 8) & 7, s & 0xFF, 0, 0u);
-    }
-  }
-  __device__ __forceinline__ void set_k(int i, int k) const { syms[i] = (uint16_t)(syms[i] | (k << 11)); }
-  template <class F>
-  __device__ __forceinline__ void for_each_k(F&& f) const {  // f(value, k, raw_len, raw_bits)
-    for (int i = 0; i < n; i++) {
-      const uint16_t s = syms[i];
-      f(s & 0xFF, s >> 11, 0, 0u);
-    }
-  }
-};
-
 // One 8x8 block of zigzag coefficients (encode_dct_component, _kernels.py:280-324):
 // DC size (ctx 0) + raw bits, then per nonzero AC (zero run ctx 1, size ctx 2 +
 // raw bits), EOB = run 64 unless position 63 is coded.
 struct DctBlockGen {
-  static constexpr bool kStoresK = false;
   const int16_t* z;  // nullptr: idle lane
   unsigned long long nzm;
   unsigned dcu;      // interleaved DC difference
@@ -496,17 +473,8 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
   sink.status = status;
   LaneBits lb;
   lb.init(toff + loff);
-#ifdef HDLL_EXP_NO_EMIT
-  if constexpr (false) {
-  } else if constexpr (false) {
-#else
-  if constexpr (Gen::kStoresK) {
-#endif
-    gen.for_each_k([&](int v, int k, int xl, uint32_t xb) {
-      lb.put(sink, rice_bits(v, k), rice_len(v, k));
-      if (xl) lb.put(sink, xb, xl);
-    });
-  } else {
+#ifndef HDLL_EXP_NO_EMIT
+  {  // the emit pass re-runs each context's state to recover k
 #pragma unroll
     for (int c = 0; c < NL; c++) {
       ls.a[c * 32 + lane] = a_start[c];
@@ -528,6 +496,7 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
       if (xl) lb.put(sink, xb, xl);
     });
   }
+#endif
   // Lane partial words.  A lane that starts mid-word owes its first word to the
   // carry of the lanes before it; a lane whose bits sit inside one word
   // ("single") passes the carry on OR-ed with its bits.  The carry is a
@@ -582,177 +551,124 @@ __device__ __forceinline__ LaneState carve_state(uint8_t* p, int nl) {
 }
 
 // ---------------------------------------------------------------------------
-// Plane coder: tile = one row (encode_plane, _kernels.py:169-216)
+// Plane coder (encode_plane, _kernels.py:169-216): tile = 32 consecutive rows
+// of a plane, lane = one row, so a lane's symbols are one contiguous range of
+// the chain and each row starts in the reset automaton state.  The symbols are
+// regenerated from the plane (L1-cached loads) by every pass instead of staged.
 // ---------------------------------------------------------------------------
-enum { kFree = 0, kForced = 1, kInRun = 2 };
-
-// Rows are staged with one pad byte on the left: cur[-1] is the left
-// neighbour of x = 0 (the sample above, or 128 on row 0) and prev[-1] = prev[0],
-// so _neighbors (_kernels.py:131-143) is branch-free: a = cur[x-1], and
-// b = prev[x], c = prev[x-1] below row 0 (b = c = a on row 0).
-template <bool kHasPrev>
-struct RowView {
-  const uint8_t* cur;
-  const uint8_t* prev;
-  __device__ __forceinline__ void abc(int x, int& a, int& b, int& c) const {
-    a = cur[x - 1];
-    if (kHasPrev) {
-      b = prev[x];
-      c = prev[x - 1];
-    } else {
-      b = a;
-      c = a;
+struct PlaneRowGen {
+  const uint8_t* cur;   // the lane's row; nullptr: idle lane
+  const uint8_t* prev;  // the row above; nullptr on row 0
+  int W;
+  // f(index, ctx, value, 0, 0) in coder order.  _neighbors (_kernels.py:131-143):
+  // a = left (above at x = 0, 128 at the origin), b = above (else a),
+  // c = above-left (else b).
+  template <class F>
+  __device__ __forceinline__ void for_each(F&& f) const {
+    if (!cur) return;
+    int i = 0;
+    int a = prev ? __ldg(prev) : 128;
+    int c = a;  // above-left of x = 0 is the above sample
+    bool inrun = false;
+    int L = 0;
+    auto run_chunks = [&]() {  // chunks of <= 255; a chunk of 255 continues
+      for (;;) {
+        const int ch = L >= 255 ? 255 : L;
+        f(i++, kRunCtx, ch, 0, 0u);
+        L -= ch;
+        if (ch < 255) break;
+      }
+    };
+    auto sample = [&](int xv, int braw) {
+      const int b = prev ? braw : a;
+      const int cc = prev ? c : a;
+      const bool E = xv == a;
+      if (!inrun && a == b && b == cc) {  // run mode (not forced, a == b == c)
+        inrun = true;
+        L = 0;
+      }
+      bool regular = true;
+      if (inrun) {
+        if (E) {
+          L++;
+          regular = false;
+        } else {  // the run ends: its chunks, then this sample is forced regular
+          run_chunks();
+          inrun = false;
+        }
+      }
+      if (regular) {  // MED prediction, activity context, folded residual (_kernels.py:146-166)
+        const int mx = max(a, b), mn = min(a, b);
+        const int pred = cc >= mx ? mn : (cc <= mn ? mx : a + b - cc);
+        const int gg = abs(a - cc) + abs(cc - b);
+        const int ctx = gg == 0 ? 0 : (gg <= 2 ? 1 : (gg <= 8 ? 2 : 3));
+        int r = (xv - pred) & 255;
+        if (r > 127) r -= 256;
+        f(i++, ctx, r >= 0 ? 2 * r : -2 * r - 1, 0, 0u);
+      }
+      c = b;
+      a = xv;
+    };
+    // 16 samples per 128-bit load when the rows are aligned: one L1 wavefront
+    // per lane per 16 samples instead of one per sample
+    const uint8_t* pv = prev ? prev : cur;
+    int x = 0;
+    if (((reinterpret_cast<uintptr_t>(cur) | reinterpret_cast<uintptr_t>(pv)) & 15) == 0) {
+      for (; x + 16 <= W; x += 16) {
+        const uint4 c4 = __ldg(reinterpret_cast<const uint4*>(cur + x));
+        const uint4 p4 = __ldg(reinterpret_cast<const uint4*>(pv + x));
+#pragma unroll 1
+        for (int q = 0; q < 4; q++) {
+          uint32_t cw = q == 0 ? c4.x : (q == 1 ? c4.y : (q == 2 ? c4.z : c4.w));
+          uint32_t pw = q == 0 ? p4.x : (q == 1 ? p4.y : (q == 2 ? p4.z : p4.w));
+#pragma unroll 1
+          for (int k = 0; k < 4; k++) {
+            sample((int)(cw & 0xFF), (int)(pw & 0xFF));
+            cw >>= 8;
+            pw >>= 8;
+          }
+        }
+      }
     }
+    for (; x < W; x++) sample(__ldg(cur + x), __ldg(pv + x));
+    if (inrun) run_chunks();  // a run reaching the row end
   }
+  __device__ __forceinline__ void set_k(int, int) const {}
 };
 
-// The lane's slice of one row -> its symbols in coder order (encode_plane's
-// automaton, _kernels.py:183-215).  Returns the count; per-context counts in cnt.
-template <bool kHasPrev>
-__device__ __forceinline__ int plane_row_symbols(const RowView<kHasPrev> rv, int W, int lane, uint16_t* ssym,
-                                                 int lane_cap, int* cnt) {
-    const int P = (W + 31) / 32;
-    const int x0 = min(W, lane * P), x1 = min(W, x0 + P);
-    // one sweep: the slice's transition for the 3 entry states + its leading E-ones
-    int s0 = kFree, s1 = kForced, s2 = kInRun, lead = 0;
-    bool leading = true;
-    for (int x = x0; x < x1; x++) {
-      int a, b, c;
-      rv.abc(x, a, b, c);
-      const bool E = rv.cur[x] == a, F = a == b && b == c;
-      if (leading && E) lead++; else leading = false;
-      s0 = (s0 == kFree && F) || s0 == kInRun ? (E ? kInRun : kFree) : kFree;
-      s1 = (s1 == kFree && F) || s1 == kInRun ? (E ? kInRun : kFree) : kFree;
-      s2 = (s2 == kFree && F) || s2 == kInRun ? (E ? kInRun : kFree) : kFree;
-    }
-    int comp = s0 | (s1 << 2) | (s2 << 4);
-#pragma unroll
-    for (int dd = 1; dd < 32; dd <<= 1) {
-      int o = __shfl_up_sync(0xffffffffu, comp, dd);
-      if (lane >= dd) {
-        int r = 0;
-#pragma unroll
-        for (int q = 0; q < 3; q++) r |= ((comp >> (2 * ((o >> (2 * q)) & 3))) & 3) << (2 * q);
-        comp = r;
-      }
-    }
-    const int excl = __shfl_up_sync(0xffffffffu, comp, 1);
-    int st = lane == 0 ? kFree : (excl & 3);
-    // run continuation into the next slices: leading E-ones, passing whole slices
-    int val = lead;
-    bool fl = lead == x1 - x0;
-#pragma unroll
-    for (int dd = 1; dd < 32; dd <<= 1) {
-      int ov = __shfl_down_sync(0xffffffffu, val, dd);
-      bool of = __shfl_down_sync(0xffffffffu, fl, dd);
-      if (lane + dd < 32) {
-        if (fl) {
-          val += ov;
-          fl = of;
-        }
-      } else {
-        fl = false;
-      }
-    }
-    const int nx = __shfl_down_sync(0xffffffffu, val, 1);
-    const int cont_next = lane == 31 ? 0 : nx;
-    // generate the lane's symbols; per-context counts packed 12 bits apiece
-    int n = 0;
-    unsigned long long cntp = 0;
-    for (int x = x0; x < x1; x++) {
-      int a, b, c;
-      rv.abc(x, a, b, c);
-      const int xv = rv.cur[x];
-      const bool E = xv == a;
-      if (st == kFree && a == b && b == c) {
-        // run mode: samples equal to a from x; chunks of <= 255, 255 continues
-        int L = 0, xx = x;
-        bool e = E;
-        while (e) {
-          L++;
-          if (++xx >= x1) break;
-          e = rv.cur[xx] == rv.cur[xx - 1];
-        }
-        if (xx >= x1 && e) L += cont_next;
-        for (;;) {
-          int ch = L >= 255 ? 255 : L;
-          if (n < lane_cap) ssym[n] = (uint16_t)((kRunCtx << 8) | ch);
-          n++;
-          cntp += 1ULL << (12 * kRunCtx);
-          L -= ch;
-          if (ch < 255) break;
-        }
-        st = kInRun;
-      }
-      if (st == kInRun) {
-        if (E) continue;
-        st = kForced;
-      }
-      // regular sample: MED prediction, activity context, folded residual
-      const int mx = max(a, b), mn = min(a, b);
-      const int pred = c >= mx ? mn : (c <= mn ? mx : a + b - c);
-      const int gg = abs(a - c) + abs(c - b);
-      const int ctx = gg == 0 ? 0 : (gg <= 2 ? 1 : (gg <= 8 ? 2 : 3));
-      int r = (xv - pred) & 255;
-      if (r > 127) r -= 256;
-      const int u = r >= 0 ? 2 * r : -2 * r - 1;
-      if (n < lane_cap) ssym[n] = (uint16_t)((ctx << 8) | u);
-      n++;
-      cntp += 1ULL << (12 * ctx);
-      st = kFree;
-    }
-#pragma unroll
-    for (int q = 0; q < 5; q++) cnt[q] = (int)((cntp >> (12 * q)) & 0xFFF);
-    return n;
-}
-
-// grid-persistent; dynamic smem per warp: context state + 32 lane symbol lists
-__global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict__ descs, ChainTab ct, int row_bytes,
-                                                       int lane_cap) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
+// grid-persistent, 4 warps per CTA, each warp's context state in shared memory
+__global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict__ descs, ChainTab ct) {
+  __shared__ __align__(16) uint8_t smem_pl[4 * lane_state_bytes(5)];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const size_t per_warp = 2 * (size_t)row_bytes + lane_state_bytes(5) + 32 * (size_t)lane_cap * sizeof(uint16_t);
-  uint8_t* wbase = smem_raw + warp * per_warp;
-  uint8_t* srow_prev = wbase + 16;  // 16 bytes of left pad keep the rows 16-byte aligned
-  uint8_t* srow_cur = wbase + row_bytes + 16;
-  const LaneState ls = carve_state(wbase + 2 * row_bytes, 5);
-  uint16_t* ssym = reinterpret_cast<uint16_t*>(wbase + 2 * row_bytes + lane_state_bytes(5)) + lane * lane_cap;
+  const LaneState ls = carve_state(smem_pl + warp * lane_state_bytes(5), 5);
   int chain;
   long long tin, g;
   while (next_tile(ct, &chain, &tin, &g)) {
     const ImgDesc& d = descs[ct.img[chain]];
     const int kind = ct.kind[chain];
-    const int y = (int)(ct.first[chain] + tin), W = d.w;  // row in the image arrays
-    const uint8_t* src = kind == 1 ? d.e_plane : d.res_planes + (long long)(kind - 2) * d.n;
-    const uint8_t* gcur = src + (long long)y * W;
-    // stage the row and the row above (16-byte vectors when aligned)
-    if (((reinterpret_cast<uintptr_t>(gcur) | (uintptr_t)W) & 15) == 0) {
-      const uint4* c4 = reinterpret_cast<const uint4*>(gcur);
-      for (int q = lane; q < W / 16; q += 32) {
-        reinterpret_cast<uint4*>(srow_cur)[q] = __ldg(c4 + q);
-        if (y > 0) reinterpret_cast<uint4*>(srow_prev)[q] = __ldg(c4 + q - W / 16);
-      }
-    } else {
-      for (int x = lane; x < W; x += 32) {
-        srow_cur[x] = gcur[x];
-        if (y > 0) srow_prev[x] = gcur[x - W];
-      }
+    const long long r = tin * 32 + lane;  // row of the chain
+    PlaneRowGen gen{nullptr, nullptr, d.w};
+    int cnt[5] = {0, 0, 0, 0, 0};
+    if (r < ct.units[chain]) {
+      const long long y = ct.first[chain] + r;  // row in the image arrays
+      const uint8_t* src = kind == 1 ? d.e_plane : d.res_planes + (long long)(kind - 2) * d.n;
+      gen.cur = src + y * d.w;
+      gen.prev = y > 0 ? gen.cur - d.w : nullptr;
+      // counts per context (two 32-bit fields per word for the regular contexts)
+      unsigned long long p01 = 0, p23 = 0;
+      int c4 = 0;
+      gen.for_each([&](int, int c, int, int, uint32_t) {
+        if (c == kRunCtx) c4++;
+        else if (c < 2) p01 += 1ULL << (32 * c);
+        else p23 += 1ULL << (32 * (c - 2));
+      });
+      cnt[0] = (int)(p01 & 0xFFFFFFFFu);
+      cnt[1] = (int)(p01 >> 32);
+      cnt[2] = (int)(p23 & 0xFFFFFFFFu);
+      cnt[3] = (int)(p23 >> 32);
+      cnt[4] = c4;
     }
-    __syncwarp();
-    if (lane == 0) {
-      srow_cur[-1] = y > 0 ? srow_prev[0] : 128;
-      srow_prev[-1] = srow_prev[0];
-    }
-    __syncwarp();
-    int cnt[5];
-    int n;
-    if (y > 0) n = plane_row_symbols(RowView<true>{srow_cur, srow_prev}, W, lane, ssym, lane_cap, cnt);
-    else n = plane_row_symbols(RowView<false>{srow_cur, srow_prev}, W, lane, ssym, lane_cap, cnt);
-    if (n > lane_cap) {
-      atomicOr(d.status, kErrCapacity);
-      n = lane_cap;
-    }
-    run_tile<5, 5>(ct, chain, tin, g, 0, PlaneList{ssym, n}, cnt, ls, d.status);
+    run_tile<5, 5>(ct, chain, tin, g, 0, gen, cnt, ls, d.status);
     __syncwarp();
   }
 }
@@ -891,21 +807,14 @@ void launch_entropy_dct(const ImgDesc* d_descs, const ChainTab& ct, cudaStream_t
 }
 
 void launch_entropy_plane(const ImgDesc* d_descs, const ChainTab& ct, int max_w, cudaStream_t st) {
+  (void)max_w;
   if (ct.ntiles <= 0) return;
-  const int P = (max_w + 31) / 32;
-  const int lane_cap = 2 * P + max_w / 255 + 4;
-  const int row_bytes = (max_w + 16 + 31) / 16 * 16;
-  size_t per_warp = 2 * (size_t)row_bytes + lane_state_bytes(5) + 32 * (size_t)lane_cap * sizeof(uint16_t);
-  int warps = (int)std::min<size_t>(4, (200 * 1024) / per_warp);
-  if (warps < 1) warps = 1;
-  size_t smem = per_warp * warps;
-  cudaFuncSetAttribute(k_entropy_plane, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_entropy_plane, 32 * warps, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_entropy_plane, 128, 0);
   long long blocks = (long long)num_sms() * (per_sm > 0 ? per_sm : 1);
-  long long need = (ct.ntiles + warps - 1) / warps;
+  long long need = (ct.ntiles + 3) / 4;
   if (blocks > need) blocks = need;
-  k_entropy_plane<<<(unsigned)blocks, 32 * warps, smem, st>>>(d_descs, ct, row_bytes, lane_cap);
+  k_entropy_plane<<<(unsigned)blocks, 128, 0, st>>>(d_descs, ct);
 }
 
 void launch_entropy_fixup(const ChainTab& ct, cudaStream_t st) {

@@ -220,7 +220,7 @@ struct HostChains {
       in_cnt.push_back(0);
       in_a.push_back(4);  // AdaptiveRiceState: A = 4 (_kernels.py:114-128)
     }
-    const long long tiles = k == 0 ? (cp < 0 ? 3 : 1) * ((nunits + 31) / 32) : nunits;
+    const long long tiles = (k == 0 && cp < 0 ? 3 : 1) * ((nunits + 31) / 32);  // 32 blocks / 32 rows per tile
     tile_base.push_back(tile_base.back() + tiles);
   }
   int nchains() const { return (int)img.size(); }
