@@ -92,9 +92,6 @@ struct ImgDesc {
   long long crc_chunks[5];
   long long crc_part_off[5];
 
-  // entropy engines (bitstreams live in per-tile staging, see entropy.cu)
-  int n_dct_tiles;            // 3 * ceil(nblocks / 32)
-  int n_plane_tiles;          // 4 * h (one tile per row per plane)
 
   // output
   uint8_t* out;               // serialized stream
@@ -121,6 +118,9 @@ inline __host__ __device__ int pairwise_level(long long n) {
 }
 
 constexpr int kMaxCtx = 6;
+constexpr int kDctBlocksPerLane = 1;                      // entropy tile: 32 lanes x 1 block
+constexpr int kDctTileBlocks = 32 * kDctBlocksPerLane;
+constexpr int kPlaneTileRows = 32;                        // entropy tile: one row per lane
 
 // Sequential-coder chains for the entropy kernel (entropy.cu).
 struct ChainTab {

@@ -220,7 +220,8 @@ struct HostChains {
       in_cnt.push_back(0);
       in_a.push_back(4);  // AdaptiveRiceState: A = 4 (_kernels.py:114-128)
     }
-    const long long tiles = (k == 0 && cp < 0 ? 3 : 1) * ((nunits + 31) / 32);  // 32 blocks / 32 rows per tile
+    const long long per = k == 0 ? kDctTileBlocks : kPlaneTileRows;
+    const long long tiles = (k == 0 && cp < 0 ? 3 : 1) * ((nunits + per - 1) / per);
     tile_base.push_back(tile_base.back() + tiles);
   }
   int nchains() const { return (int)img.size(); }
@@ -433,8 +434,6 @@ inline void fill_desc(ImgDesc& d, const hdll_b200_image& im, const ImgLayout& L,
     d.crc_part_off[j] = po;
     po += d.crc_chunks[j];
   }
-  d.n_dct_tiles = (int)(3 * ((d.nblocks + 31) / 32));
-  d.n_plane_tiles = 4 * d.h;
 }
 
 // entropy status arena of at least `ntiles` tiles, and a fresh launch epoch
