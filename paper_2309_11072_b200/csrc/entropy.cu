@@ -668,7 +668,11 @@ __global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict
       cnt[3] = (int)(p23 >> 32);
       cnt[4] = c4;
     }
+#ifdef HDLL_EXP_COUNT_ONLY  // timing experiment: the generation pass alone
+    if (cnt[0] == -1) atomicOr(d.status, 1u);
+#else
     run_tile<5, 5>(ct, chain, tin, g, 0, gen, cnt, ls, d.status);
+#endif
     __syncwarp();
   }
 }
