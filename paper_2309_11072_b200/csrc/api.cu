@@ -146,8 +146,8 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   }
   mark(kStTonemap);
   if (mode != 1) {
-    launch_base_layer(dd, n, max_base_tiles, st);
-    c->launches += 1;
+    launch_base_layer(dd, n, max_base_tiles, max_n, st);
+    c->launches += 2;
   }
   mark(kStBase);
   if (mode == 0 && any_real) {

@@ -80,6 +80,68 @@ __device__ __forceinline__ void sdr_pixel(const ImgDesc& d, uint32_t q, double l
   for (int c = 0; c < 3; c++) out3[c] = quantize_pow(fmax(f[c] * ratio, 0.0), d.inv_gamma, tc.g32, amb);
 }
 
+// Pass 1, per pixel: tone-map pass B (or the given SDR in the lossy-coder
+// plugin mode) and _rgb_to_ycc with rounding and clamping (codec_core.py:391-403),
+// stored as bytes (Y in [0, 255], Cb / Cr in [-128, 127]).  Four pixels per
+// thread; the transform kernel below reads them back per 8x8 block.  Split from
+// the transforms so each runs at its own register budget.
+__device__ __forceinline__ void ycc_bytes(const uint8_t* s3, uint8_t* y, int8_t* cb, int8_t* cr) {
+  const double r = s3[0], g = s3[1], b = s3[2];
+  const double Y = 0.299 * r + 0.587 * g + 0.114 * b;
+  const double u = -0.168736 * r - 0.331264 * g + 0.5 * b;
+  const double v = 0.5 * r - 0.418688 * g - 0.081312 * b;
+  *y = (uint8_t)clampd(rha(Y), 0.0, 255.0);
+  *cb = (int8_t)clampd(rha(u), -128.0, 127.0);
+  *cr = (int8_t)clampd(rha(v), -128.0, 127.0);
+}
+
+__global__ void __launch_bounds__(256) k_sdr_ycc(const ImgDesc* __restrict__ descs) {
+  const ImgDesc& d = descs[blockIdx.y];
+  const double log_avg = d.sdr_in ? 1.0 : d.scalars[1], white = d.sdr_in ? 1.0 : d.scalars[2];
+  const bool allzero = d.sdr_in ? false : d.scalars[3] != 0.0;
+  TmoConst tc;
+  tc.g32 = (float)d.inv_gamma;
+  unsigned amb = 0;  // samples the fp32 pow could not certify
+  const long long nq = (d.n + 3) / 4;
+  uint8_t* Yp = d.ycc;
+  int8_t* Cb = reinterpret_cast<int8_t*>(d.ycc + d.n);
+  int8_t* Cr = reinterpret_cast<int8_t*>(d.ycc + 2 * d.n);
+  for (long long qi = (long long)blockIdx.x * blockDim.x + threadIdx.x; qi < nq;
+       qi += (long long)gridDim.x * blockDim.x) {
+    const long long p0 = qi * 4;
+    const int cnt = (int)min(4LL, d.n - p0);
+    uint32_t qs[4] = {0u, 0u, 0u, 0u};
+    if (!d.sdr_in) {
+      if (cnt == 4) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(d.rgbe) + qi);
+        qs[0] = v.x, qs[1] = v.y, qs[2] = v.z, qs[3] = v.w;
+      } else {
+        for (int k = 0; k < cnt; k++) qs[k] = reinterpret_cast<const uint32_t*>(d.rgbe)[p0 + k];
+      }
+    }
+#pragma unroll 1
+    for (int k = 0; k < cnt; k++) {
+      const long long p = p0 + k;
+      uint8_t s3[3];
+      if (d.sdr_in) {
+        s3[0] = d.sdr_in[3 * p], s3[1] = d.sdr_in[3 * p + 1], s3[2] = d.sdr_in[3 * p + 2];
+      } else {
+        const uint32_t q = k == 0 ? qs[0] : (k == 1 ? qs[1] : (k == 2 ? qs[2] : qs[3]));
+        sdr_pixel(d, q, log_avg, white, tc, allzero, s3, &amb);
+        if (d.want_trace) {
+          d.sdr[3 * p] = s3[0];
+          d.sdr[3 * p + 1] = s3[1];
+          d.sdr[3 * p + 2] = s3[2];
+        }
+      }
+      ycc_bytes(s3, Yp + p, Cb + p, Cr + p);
+    }
+  }
+  if (amb) atomicAdd(d.amb, amb);
+}
+
+// Pass 2: the 8x8 DCT round trip of one tile = 8 pixel rows x 128 columns
+// (16 blocks), everything in shared memory.
 __global__ void __launch_bounds__(128, 4) k_base_layer(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
   const int tiles_x = (d.nbx + kTileBlocks - 1) / kTileBlocks;
@@ -94,59 +156,23 @@ __global__ void __launch_bounds__(128, 4) k_base_layer(const ImgDesc* __restrict
   double* bufB = smem + 3 * 8 * kRowStride;  // [3][8][kRowStride]
   const int t = threadIdx.x;
 
-  const double log_avg = d.sdr_in ? 1.0 : d.scalars[1], white = d.sdr_in ? 1.0 : d.scalars[2];
-  const bool allzero = d.sdr_in ? false : d.scalars[3] != 0.0;
-  TmoConst tc;
-  tc.g32 = (float)d.inv_gamma;
-
-  // 1. SDR (tone-map pass B) and YCC for every padded pixel of the tile:
-  //    thread t owns column t, rows 0..7; its 8 RGBE words are loaded up front
-  unsigned amb = 0;  // samples the fp32 pow could not certify
-  const int rx = t;
-  const bool col_live = rx < nblk * 8;
-  const int x = bx0 * 8 + rx, sx = min(x, d.w - 1);  // np.pad mode="edge"
-  uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0, w4 = 0, w5 = 0, w6 = 0, w7 = 0;
-  if (col_live && !d.sdr_in) {
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(d.rgbe) + sx;
-    const long long W = d.w;
-    const int y0 = by * 8, hm = d.h - 1;
-    w0 = __ldg(src + min(y0 + 0, hm) * W);
-    w1 = __ldg(src + min(y0 + 1, hm) * W);
-    w2 = __ldg(src + min(y0 + 2, hm) * W);
-    w3 = __ldg(src + min(y0 + 3, hm) * W);
-    w4 = __ldg(src + min(y0 + 4, hm) * W);
-    w5 = __ldg(src + min(y0 + 5, hm) * W);
-    w6 = __ldg(src + min(y0 + 6, hm) * W);
-    w7 = __ldg(src + min(y0 + 7, hm) * W);
-  }
-#pragma unroll 1
-  for (int ry = 0; ry < 8 && col_live; ry++) {
-    const int y = by * 8 + ry;
-    const int sy = min(y, d.h - 1);
-    uint8_t s3[3];
-    if (d.sdr_in) {
-      const uint8_t* sp = d.sdr_in + ((long long)sy * d.w + sx) * 3;
-      s3[0] = sp[0], s3[1] = sp[1], s3[2] = sp[2];
-    } else {
-      const uint32_t q = w0;
-      w0 = w1, w1 = w2, w2 = w3, w3 = w4, w4 = w5, w5 = w6, w6 = w7;
-      sdr_pixel(d, q, log_avg, white, tc, allzero, s3, &amb);
+  // 1. the tile's YCC samples, edge-padded (np.pad mode="edge", codec_core.py:432-436)
+  {
+    const int rx = t;
+    const int x = bx0 * 8 + rx, sx = min(x, d.w - 1);
+    if (rx < nblk * 8) {
+      const uint8_t* Yp = d.ycc;
+      const int8_t* Cb = reinterpret_cast<const int8_t*>(d.ycc + d.n);
+      const int8_t* Cr = reinterpret_cast<const int8_t*>(d.ycc + 2 * d.n);
+#pragma unroll
+      for (int ry = 0; ry < 8; ry++) {
+        const long long pi = (long long)min(by * 8 + ry, d.h - 1) * d.w + sx;
+        bufA[(0 * 8 + ry) * kRowStride + rx] = (double)__ldg(Yp + pi);
+        bufA[(1 * 8 + ry) * kRowStride + rx] = (double)__ldg(Cb + pi);
+        bufA[(2 * 8 + ry) * kRowStride + rx] = (double)__ldg(Cr + pi);
+      }
     }
-    if (d.want_trace && y < d.h && x < d.w) {
-      uint8_t* o = d.sdr + ((long long)y * d.w + x) * 3;
-      o[0] = s3[0];
-      o[1] = s3[1];
-      o[2] = s3[2];
-    }
-    double r = s3[0], g = s3[1], b = s3[2];
-    double Y = 0.299 * r + 0.587 * g + 0.114 * b;
-    double cb = -0.168736 * r - 0.331264 * g + 0.5 * b;
-    double cr = 0.5 * r - 0.418688 * g - 0.081312 * b;
-    bufA[(0 * 8 + ry) * kRowStride + rx] = clampd(rha(Y), 0.0, 255.0);
-    bufA[(1 * 8 + ry) * kRowStride + rx] = clampd(rha(cb), -128.0, 127.0);
-    bufA[(2 * 8 + ry) * kRowStride + rx] = clampd(rha(cr), -128.0, 127.0);
   }
-  if (amb) atomicAdd(d.amb, amb);
   __syncthreads();
 
   // task t: block b = t / 8, line l = t % 8, for each of the 3 components
@@ -280,7 +306,12 @@ void upload_base_constants() {
   cudaMemcpyToSymbol(c_zigzag, inv, sizeof(inv));
 }
 
-void launch_base_layer(const ImgDesc* d_descs, int nimg, int max_tiles, cudaStream_t st) {
+void launch_base_layer(const ImgDesc* d_descs, int nimg, int max_tiles, long long max_n, cudaStream_t st) {
+  long long nq = (max_n + 3) / 4;
+  int gx = (int)((nq + 255) / 256);
+  if (gx > 148 * 8) gx = 148 * 8;
+  if (gx < 1) gx = 1;
+  k_sdr_ycc<<<dim3(gx, nimg), 256, 0, st>>>(d_descs);
   size_t smem = sizeof(double) * 2 * 3 * 8 * kRowStride;
   static bool attr = false;
   if (!attr) {

@@ -61,6 +61,7 @@ struct ImgDesc {
 
   // base layer
   uint8_t* sdr;               // trace: (h, w, 3) pre-coding SDR (optional)
+  uint8_t* ycc;               // 3 planes (h, w): Y u8, Cb i8, Cr i8 (rounded, clamped)
   uint8_t* s_planes;          // 3 planes (h, w): decoded S
   int16_t* zz;                // [3][nblocks][64] zigzag quantised coefficients
 
@@ -174,7 +175,7 @@ void upload_crc_constants();
 void launch_tonemap_stats(const ImgDesc*, int nimg, long long max_n, int max_level, cudaStream_t);
 void launch_tonemap_partial(const ImgDesc*, int nimg, long long max_n, int max_level, cudaStream_t);
 void launch_tonemap_scalars(const ImgDesc*, int nimg, cudaStream_t);
-void launch_base_layer(const ImgDesc*, int nimg, int max_tiles, cudaStream_t);
+void launch_base_layer(const ImgDesc*, int nimg, int max_tiles, long long max_n, cudaStream_t);
 void launch_prefilter(const ImgDesc*, int nimg, int max_w, int max_h, int max_radius, cudaStream_t);
 void launch_fit(const ImgDesc*, int nimg, int max_sort_tiles, long long max_nodes, int max_chunks, cudaStream_t);
 void launch_fit_sort(const ImgDesc*, int nimg, int max_sort_tiles, cudaStream_t);

@@ -54,7 +54,7 @@ inline long long max_seg_nodes(long long n) { return 3 * (2 * (n / kNodeTarget) 
 struct ImgLayout {
   size_t off_qt, off_taps, off_pre, off_post;
   size_t off_logv, off_tmnodes, off_scalars;
-  size_t off_sdr, off_s, off_zz;
+  size_t off_sdr, off_ycc, off_s, off_zz;
   size_t off_sstar, off_sstar_tmp, off_e, off_res, off_mstar;
   size_t off_tile_hist, off_xs, off_ys, off_bin_start, off_seg_nodes, off_seg_level, off_seg_node_off, off_dot, off_a32,
       off_b32;
@@ -159,6 +159,7 @@ inline ImgLayout plan(const hdll_b200_image& im, bool trace) {
   L.off_tmnodes = take(sizeof(double) * ((size_t)1 << pairwise_level(n)));
   L.off_scalars = take(sizeof(double) * 4);
   L.off_sdr = trace ? take(3 * n) : 0;
+  L.off_ycc = take(3 * n + 16);
   L.off_s = take(3 * n + 16);
   L.off_zz = take(sizeof(int16_t) * 3 * nb * 64);
   const bool real = im.params.slrme && im.params.sigma_milli != 0;
@@ -407,6 +408,7 @@ inline void fill_desc(ImgDesc& d, const hdll_b200_image& im, const ImgLayout& L,
   d.tm_level = pairwise_level(d.n);
   d.scalars = (double*)(B + L.off_scalars);
   d.sdr = d.want_trace ? B + L.off_sdr : nullptr;
+  d.ycc = B + L.off_ycc;
   d.s_planes = B + L.off_s;
   d.zz = (int16_t*)(B + L.off_zz);
   d.sstar = L.off_sstar ? (double*)(B + L.off_sstar) : nullptr;
