@@ -175,7 +175,9 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   }
   mark(kStEntropyDct);
   if (ct_pln.ntiles > 0) {
-    launch_entropy_plane(dd, ct_pln, max_w, st);
+    if (ensure(&c->plane_scratch, &c->plane_scratch_cap, plane_scratch_bytes(ct_pln, max_w), true))
+      return HDLL_B200_E_CUDA;
+    launch_entropy_plane(dd, ct_pln, max_w, c->plane_scratch, st);
     launch_entropy_fixup(ct_pln, st);
     c->launches += 2;
   }
@@ -247,6 +249,7 @@ void hdll_b200_ctx_destroy(hdll_b200_ctx* ctx) {
   if (c->d_out) cudaFree(c->d_out);
   if (c->d_len) cudaFree(c->d_len);
   band_free(c);
+  if (c->plane_scratch) cudaFree(c->plane_scratch);
   if (c->done_ev) cudaEventDestroy(c->done_ev);
   for (int k = 0; k <= kStages; k++)
     if (c->stage_ev[k]) cudaEventDestroy(c->stage_ev[k]);

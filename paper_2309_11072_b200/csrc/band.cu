@@ -97,7 +97,9 @@ int run_chains(Ctx* c, Band* b, int mode) {
   ChainTab ct_pln = b->hc_pln.table(b->sc_pln, D, E, c->estat_tiles, b->hc_dct.ntiles(), b->d_ticket + 2, c->epoch, mode);
   launch_entropy_dct(b->d_desc, ct_dct, b->st);
   launch_entropy_fixup(ct_dct, b->st);
-  launch_entropy_plane(b->d_desc, ct_pln, b->W, b->st);
+  if (ensure(&c->plane_scratch, &c->plane_scratch_cap, plane_scratch_bytes(ct_pln, b->W), true))
+    return HDLL_B200_E_CUDA;
+  launch_entropy_plane(b->d_desc, ct_pln, b->W, c->plane_scratch, b->st);
   launch_entropy_fixup(ct_pln, b->st);
   c->launches += 4;
   return sync_status(b);

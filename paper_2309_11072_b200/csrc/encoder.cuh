@@ -195,7 +195,8 @@ void launch_bitcat(uint8_t* dst, const uint8_t* const* src, const unsigned long 
 void launch_estimate(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
 void launch_crc(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
 void launch_entropy_dct(const ImgDesc*, const ChainTab&, cudaStream_t);
-void launch_entropy_plane(const ImgDesc*, const ChainTab&, int max_w, cudaStream_t);
+size_t plane_scratch_bytes(const ChainTab&, int max_w);
+void launch_entropy_plane(const ImgDesc*, const ChainTab&, int max_w, void* scratch, cudaStream_t);
 void launch_entropy_fixup(const ChainTab&, cudaStream_t);
 void launch_assemble(const ImgDesc*, int nimg, const AsmTab&, long long max_out, cudaStream_t);
 

@@ -229,6 +229,7 @@ struct LaneBits {
 // DC size (ctx 0) + raw bits, then per nonzero AC (zero run ctx 1, size ctx 2 +
 // raw bits), EOB = run 64 unless position 63 is coded.
 struct DctBlockGen {
+  static constexpr bool kStoresK = false;
   const int16_t* z;  // nullptr: idle lane
   unsigned long long nzm;
   unsigned dcu;      // interleaved DC difference
@@ -253,7 +254,6 @@ struct DctBlockGen {
       pos = nz + 1;
     }
   }
-  __device__ __forceinline__ void set_k(int, int) const {}
 };
 
 // Per-lane context state lives in shared memory, [context][lane], so a symbol
@@ -421,7 +421,7 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
     ls.nn[c * 32 + lane] = n0[c];
   }
   long long nbits = 0;
-  gen.for_each([&](int i, int c, int v, int xl, uint32_t) {
+  auto len_step = [&](int, int c, int v, int xl, uint32_t) {
     const int o = c * 32 + lane;
     int a = ls.a[o], nb = ls.nn[o];
     const int k = kfast(a, nb);
@@ -434,8 +434,10 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
     }
     ls.a[o] = a;
     ls.nn[o] = nb;
-    gen.set_k(i, k);
-  });
+    return k;
+  };
+  if constexpr (Gen::kStoresK) gen.for_each_setk(len_step);  // k kept for the emit pass
+  else gen.for_each(len_step);
   long long tbits;
   const long long loff = warp_excl_sum(nbits, &tbits);
   long long toff = 0;
@@ -474,7 +476,12 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
   LaneBits lb;
   lb.init(toff + loff);
 #ifndef HDLL_EXP_NO_EMIT
-  {  // the emit pass re-runs each context's state to recover k
+  if constexpr (Gen::kStoresK) {
+    gen.for_each_k([&](int v, int k, int xl, uint32_t xb) {
+      lb.put(sink, rice_bits(v, k), rice_len(v, k));
+      if (xl) lb.put(sink, xb, xl);
+    });
+  } else {  // the emit pass re-runs each context's state to recover k
 #pragma unroll
     for (int c = 0; c < NL; c++) {
       ls.a[c * 32 + lane] = a_start[c];
@@ -557,6 +564,7 @@ __device__ __forceinline__ LaneState carve_state(uint8_t* p, int nl) {
 // regenerated from the plane (L1-cached loads) by every pass instead of staged.
 // ---------------------------------------------------------------------------
 struct PlaneRowGen {
+  static constexpr bool kStoresK = false;
   const uint8_t* cur;   // the lane's row; nullptr: idle lane
   const uint8_t* prev;  // the row above; nullptr on row 0
   int W;
@@ -633,35 +641,124 @@ struct PlaneRowGen {
     for (; x < W; x++) sample(__ldg(cur + x), __ldg(pv + x));
     if (inrun) run_chunks();  // a run reaching the row end
   }
-  __device__ __forceinline__ void set_k(int, int) const {}
+};
+
+// The count pass keeps each row's symbols (u16: k << 11 | ctx << 8 | value)
+// in a global scratch slab of the warp, interleaved by lane in 16-byte chunks
+// (chunk q of lane l at slab[q * 32 + l]), so the later passes read 8 symbols
+// per coalesced 128-bit access instead of re-deriving them; the length pass
+// stores each symbol's Rice parameter k for the emit pass.
+struct SymChunk {  // 8 u16 symbols, shifted in at the top
+  unsigned long long lo = 0, hi = 0;
+  __device__ __forceinline__ void push(uint32_t s) {
+    lo = (lo >> 16) | (hi << 48);
+    hi = (hi >> 16) | ((unsigned long long)s << 48);
+  }
+  __device__ __forceinline__ uint32_t pop() {  // lowest symbol first
+    const uint32_t s = (uint32_t)(lo & 0xFFFFu);
+    lo = (lo >> 16) | (hi << 48);
+    hi >>= 16;
+    return s;
+  }
+  __device__ __forceinline__ void align(int m) {  // m < 8 pushed: move them to the bottom
+    const int sh = 16 * (8 - m);
+    if (sh < 64) {
+      lo = (lo >> sh) | (hi << (64 - sh));
+      hi >>= sh;
+    } else {
+      lo = hi >> (sh - 64);
+      hi = 0;
+    }
+  }
+  __device__ __forceinline__ uint4 word() const {
+    return make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32));
+  }
+  __device__ __forceinline__ void load(const uint4& w) {
+    lo = (unsigned long long)w.x | ((unsigned long long)w.y << 32);
+    hi = (unsigned long long)w.z | ((unsigned long long)w.w << 32);
+  }
+};
+
+struct PlaneBufGen {
+  static constexpr bool kStoresK = true;
+  uint4* slab;  // this lane's chunk 0
+  int n;        // symbols
+  template <class F>
+  __device__ __forceinline__ void for_each(F&& f) const {
+    for (int q0 = 0; q0 < n; q0 += 8) {
+      SymChunk ch;
+      ch.load(slab[(q0 >> 3) * 32]);
+      const int m = min(8, n - q0);
+      for (int j = 0; j < m; j++) {
+        const uint32_t sy = ch.pop();
+        f(q0 + j, (int)((sy >> 8) & 7), (int)(sy & 0xFF), 0, 0u);
+      }
+    }
+  }
+  template <class F>
+  __device__ __forceinline__ void for_each_setk(F&& f) const {  // f returns k
+    for (int q0 = 0; q0 < n; q0 += 8) {
+      SymChunk ch, out;
+      ch.load(slab[(q0 >> 3) * 32]);
+      const int m = min(8, n - q0);
+      for (int j = 0; j < m; j++) {
+        const uint32_t sy = ch.pop();
+        const int k = f(q0 + j, (int)((sy >> 8) & 7), (int)(sy & 0xFF), 0, 0u);
+        out.push((sy & 0x7FFu) | ((uint32_t)k << 11));
+      }
+      if (m < 8) out.align(m);
+      slab[(q0 >> 3) * 32] = out.word();
+    }
+  }
+  template <class F>
+  __device__ __forceinline__ void for_each_k(F&& f) const {  // f(value, k, raw_len, raw_bits)
+    for (int q0 = 0; q0 < n; q0 += 8) {
+      SymChunk ch;
+      ch.load(slab[(q0 >> 3) * 32]);
+      const int m = min(8, n - q0);
+      for (int j = 0; j < m; j++) {
+        const uint32_t sy = ch.pop();
+        f((int)(sy & 0xFF), (int)(sy >> 11), 0, 0u);
+      }
+    }
+  }
 };
 
 // grid-persistent, 4 warps per CTA, each warp's context state in shared memory
-__global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict__ descs, ChainTab ct) {
+__global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict__ descs, ChainTab ct, uint4* symbuf,
+                                                       int cap_chunks) {
   __shared__ __align__(16) uint8_t smem_pl[4 * lane_state_bytes(5)];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const LaneState ls = carve_state(smem_pl + warp * lane_state_bytes(5), 5);
+  uint4* slab = symbuf + ((long long)blockIdx.x * 4 + warp) * cap_chunks * 32 + lane;
   int chain;
   long long tin, g;
   while (next_tile(ct, &chain, &tin, &g)) {
     const ImgDesc& d = descs[ct.img[chain]];
     const int kind = ct.kind[chain];
-    const long long r = tin * 32 + lane;  // row of the chain
-    PlaneRowGen gen{nullptr, nullptr, d.w};
+    const long long r = tin * kPlaneTileRows + lane;  // row of the chain
     int cnt[5] = {0, 0, 0, 0, 0};
+    int n = 0;
     if (r < ct.units[chain]) {
       const long long y = ct.first[chain] + r;  // row in the image arrays
       const uint8_t* src = kind == 1 ? d.e_plane : d.res_planes + (long long)(kind - 2) * d.n;
-      gen.cur = src + y * d.w;
-      gen.prev = y > 0 ? gen.cur - d.w : nullptr;
+      PlaneRowGen gen{src + y * d.w, y > 0 ? src + (y - 1) * d.w : nullptr, d.w};
       // counts per context (two 32-bit fields per word for the regular contexts)
       unsigned long long p01 = 0, p23 = 0;
       int c4 = 0;
-      gen.for_each([&](int, int c, int, int, uint32_t) {
+      SymChunk ch;
+      gen.for_each([&](int i, int c, int v, int, uint32_t) {
         if (c == kRunCtx) c4++;
         else if (c < 2) p01 += 1ULL << (32 * c);
         else p23 += 1ULL << (32 * (c - 2));
+        ch.push((uint32_t)((c << 8) | v));
+        if ((i & 7) == 7) slab[(i >> 3) * 32] = ch.word();
+        n = i + 1;
       });
+      if (n & 7) {
+        ch.align(n & 7);
+        slab[(n >> 3) * 32] = ch.word();
+      }
       cnt[0] = (int)(p01 & 0xFFFFFFFFu);
       cnt[1] = (int)(p01 >> 32);
       cnt[2] = (int)(p23 & 0xFFFFFFFFu);
@@ -671,7 +768,7 @@ __global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict
 #ifdef HDLL_EXP_COUNT_ONLY  // timing experiment: the generation pass alone
     if (cnt[0] == -1) atomicOr(d.status, 1u);
 #else
-    run_tile<5, 5>(ct, chain, tin, g, 0, gen, cnt, ls, d.status);
+    run_tile<5, 5>(ct, chain, tin, g, 0, PlaneBufGen{slab, n}, cnt, ls, d.status);
 #endif
     __syncwarp();
   }
@@ -810,15 +907,24 @@ void launch_entropy_dct(const ImgDesc* d_descs, const ChainTab& ct, cudaStream_t
   k_entropy_dct<<<(unsigned)blocks, 128, 0, st>>>(d_descs, ct);
 }
 
-void launch_entropy_plane(const ImgDesc* d_descs, const ChainTab& ct, int max_w, cudaStream_t st) {
-  (void)max_w;
-  if (ct.ntiles <= 0) return;
+static long long plane_grid(const ChainTab& ct) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_entropy_plane, 128, 0);
   long long blocks = (long long)num_sms() * (per_sm > 0 ? per_sm : 1);
-  long long need = (ct.ntiles + 3) / 4;
-  if (blocks > need) blocks = need;
-  k_entropy_plane<<<(unsigned)blocks, 128, 0, st>>>(d_descs, ct);
+  const long long need = (ct.ntiles + 3) / 4;
+  return blocks < need ? blocks : need;
+}
+
+static int plane_cap_chunks(int max_w) { return (2 * max_w + 8) / 8 + 1; }  // <= 2 symbols per sample
+
+size_t plane_scratch_bytes(const ChainTab& ct, int max_w) {
+  if (ct.ntiles <= 0) return 0;
+  return (size_t)plane_grid(ct) * 4 * 32 * plane_cap_chunks(max_w) * sizeof(uint4);
+}
+
+void launch_entropy_plane(const ImgDesc* d_descs, const ChainTab& ct, int max_w, void* scratch, cudaStream_t st) {
+  if (ct.ntiles <= 0) return;
+  k_entropy_plane<<<(unsigned)plane_grid(ct), 128, 0, st>>>(d_descs, ct, (uint4*)scratch, plane_cap_chunks(max_w));
 }
 
 void launch_entropy_fixup(const ChainTab& ct, cudaStream_t st) {

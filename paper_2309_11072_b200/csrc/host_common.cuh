@@ -108,6 +108,8 @@ struct Ctx {
   size_t d_out_cap = 0;
   uint64_t* d_len = nullptr;
   Band* band = nullptr;  // row-band session (band.cu)
+  void* plane_scratch = nullptr;  // plane coder symbol slabs (entropy.cu)
+  size_t plane_scratch_cap = 0;
 };
 
 inline int cuda_fail(cudaError_t e, const char* what) {
