@@ -234,8 +234,6 @@ int hdll_b200_band_begin(hdll_b200_ctx* ctx, const hdll_b200_image* img, const h
   fill_desc(d, b->im, b->L, B, 0, false, D, sp);
   d.full_n = full_n;
   d.pix_base = (long long)b->c0 * W;
-  d.px0 = px0;
-  d.px1 = px1;
   d.node0 = b->node0;
   d.node1 = b->node1;
   d.tm_level = level;

@@ -46,14 +46,12 @@ struct ImgDesc {
   // image.  Whole-image descs: full_n = n, pix_base = 0, every range complete.
   long long full_n;           // pixels of the full image (tone-map mean, pairwise tree)
   long long pix_base;         // full-image index of the desc's pixel 0
-  long long px0, px1;         // full-image pixels whose log(Lw) and max this desc computes
   long long node0, node1;     // pairwise nodes (level tm_level) this desc sums
   long long fit_p0, fit_m;    // fit samples: desc pixels [fit_p0, fit_p0 + fit_m); xs/ys plane stride
   int fit_owner;              // 1: xs/ys/bin_* were filled by the exchange (skip the sort)
   long long crc_p0, crc_np;   // CRC jobs cover desc pixels [crc_p0, crc_p0 + crc_np)
 
   // tone-map stage
-  double* logv;               // desc pixels: log(eps + Lw)
   unsigned long long* maxlw;  // bits of max Lw (Lw >= 0)
   double* tm_nodes;           // pairwise-sum level-L node values (all 2^L of the full image)
   int tm_level;               // L for the image-wide pairwise tree

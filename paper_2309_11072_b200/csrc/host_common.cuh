@@ -53,7 +53,7 @@ inline long long max_seg_nodes(long long n) { return 3 * (2 * (n / kNodeTarget) 
 
 struct ImgLayout {
   size_t off_qt, off_taps, off_pre, off_post;
-  size_t off_logv, off_tmnodes, off_scalars;
+  size_t off_tmnodes, off_scalars;
   size_t off_sdr, off_ycc, off_s, off_zz;
   size_t off_sstar, off_sstar_tmp, off_e, off_res, off_mstar;
   size_t off_tile_hist, off_xs, off_ys, off_bin_start, off_seg_nodes, off_seg_level, off_seg_node_off, off_dot, off_a32,
@@ -157,7 +157,6 @@ inline ImgLayout plan(const hdll_b200_image& im, bool trace) {
   L.off_taps = take(sizeof(double) * (2 * (size_t)std::max(0, im.params.radius) + 1));
   L.off_pre = take(im.hdr_pre_len + 1);
   L.off_post = take(im.hdr_post_len + 1);
-  L.off_logv = take(sizeof(double) * n);
   L.off_tmnodes = take(sizeof(double) * ((size_t)1 << pairwise_level(n)));
   L.off_scalars = take(sizeof(double) * 4);
   L.off_sdr = trace ? take(3 * n) : 0;
@@ -396,8 +395,6 @@ inline void fill_desc(ImgDesc& d, const hdll_b200_image& im, const ImgLayout& L,
   d.sum_y = (long long*)(B + L.off_zero + 16 + 1024);
   d.full_n = d.n;
   d.pix_base = 0;
-  d.px0 = 0;
-  d.px1 = d.n;
   d.node0 = 0;
   d.node1 = 1LL << pairwise_level(d.n);
   d.fit_p0 = 0;
@@ -405,7 +402,6 @@ inline void fill_desc(ImgDesc& d, const hdll_b200_image& im, const ImgLayout& L,
   d.fit_owner = 0;
   d.crc_p0 = 0;
   d.crc_np = d.n;
-  d.logv = (double*)(B + L.off_logv);
   d.tm_nodes = (double*)(B + L.off_tmnodes);
   d.tm_level = pairwise_level(d.n);
   d.scalars = (double*)(B + L.off_scalars);
