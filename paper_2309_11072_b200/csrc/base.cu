@@ -106,12 +106,21 @@ __global__ void __launch_bounds__(256) k_sdr_ycc(const ImgDesc* __restrict__ des
   uint8_t* Yp = d.ycc;
   int8_t* Cb = reinterpret_cast<int8_t*>(d.ycc + d.n);
   int8_t* Cr = reinterpret_cast<int8_t*>(d.ycc + 2 * d.n);
-  for (long long qi = (long long)blockIdx.x * blockDim.x + threadIdx.x; qi < nq;
-       qi += (long long)gridDim.x * blockDim.x) {
+  // The fit's exponent histogram per 1024-pixel sort tile (fit.cu k_sort_hist)
+  // rides along: one pass of this grid-stride loop is exactly one sort tile.
+  __shared__ unsigned hist[256];
+  const bool fuse_hist = d.hist_fused != 0;
+  static_assert(kSortTile == 4 * 256, "one k_sdr_ycc block iteration covers one sort tile");
+  for (long long qb = (long long)blockIdx.x * blockDim.x; qb < nq; qb += (long long)gridDim.x * blockDim.x) {
+    const long long qi = qb + threadIdx.x;
+    if (fuse_hist) {  // (block-uniform branch: every thread reaches both barriers)
+      hist[threadIdx.x] = 0;
+      __syncthreads();
+    }
     const long long p0 = qi * 4;
-    const int cnt = (int)min(4LL, d.n - p0);
+    const int cnt = qi < nq ? (int)min(4LL, d.n - p0) : 0;
     uint32_t qs[4] = {0u, 0u, 0u, 0u};
-    if (!d.sdr_in) {
+    if (!d.sdr_in && cnt > 0) {
       if (cnt == 4) {
         const uint4 v = __ldg(reinterpret_cast<const uint4*>(d.rgbe) + qi);
         qs[0] = v.x, qs[1] = v.y, qs[2] = v.z, qs[3] = v.w;
@@ -135,6 +144,13 @@ __global__ void __launch_bounds__(256) k_sdr_ycc(const ImgDesc* __restrict__ des
         }
       }
       ycc_bytes(s3, Yp + p, Cb + p, Cr + p);
+    }
+    if (fuse_hist) {
+      for (int k = 0; k < cnt; k++) atomicAdd(&hist[qs[k] >> 24], 1u);
+      __syncthreads();
+      const unsigned hc = hist[threadIdx.x];
+      d.tile_hist[(long long)threadIdx.x * d.sort_tiles + qb / 256] = hc;
+      if (hc) atomicAdd(&d.bin_count[threadIdx.x], hc);
     }
   }
   if (amb) atomicAdd(d.amb, amb);

@@ -49,6 +49,7 @@ struct ImgDesc {
   long long node0, node1;     // pairwise nodes (level tm_level) this desc sums
   long long fit_p0, fit_m;    // fit samples: desc pixels [fit_p0, fit_p0 + fit_m); xs/ys plane stride
   int fit_owner;              // 1: xs/ys/bin_* were filled by the exchange (skip the sort)
+  int hist_fused;             // 1: k_sdr_ycc builds the sort's tile histograms (whole-image fit)
   long long crc_p0, crc_np;   // CRC jobs cover desc pixels [crc_p0, crc_p0 + crc_np)
 
   // tone-map stage

@@ -29,7 +29,7 @@ constexpr int kSegs = 3 * 256;
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_sort_hist(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
-  if (!d.slrme || d.fit_owner) return;
+  if (!d.slrme || d.fit_owner || d.hist_fused) return;
   const int tile = blockIdx.x;
   if (tile >= d.sort_tiles) return;
   __shared__ unsigned hist[256];

@@ -400,6 +400,7 @@ inline void fill_desc(ImgDesc& d, const hdll_b200_image& im, const ImgLayout& L,
   d.fit_p0 = 0;
   d.fit_m = d.n;
   d.fit_owner = 0;
+  d.hist_fused = (d.slrme && !d.global_regression && mode == 0) ? 1 : 0;  // band.cu clears it
   d.crc_p0 = 0;
   d.crc_np = d.n;
   d.tm_nodes = (double*)(B + L.off_tmnodes);
