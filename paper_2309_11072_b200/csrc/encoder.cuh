@@ -107,7 +107,8 @@ struct ImgDesc {
 
 constexpr int kMaxBlasThreads = 64;
 constexpr int kSortTile = 1024;
-constexpr int kCrcChunk = 1024;       // bytes per CRC partial
+constexpr int kCrcChunk = 1024;       // bytes per CRC partial of a plane (32 lanes x 32 bytes)
+constexpr int kCrcChunkRgb = 768;     // bytes per CRC partial of the interleaved RGB job (32 lanes x 8 pixels)
 constexpr int kNodeTarget = 1024;     // pairwise-sum level-L node size target
 
 // pairwise tree level so level-L nodes hold >= kNodeTarget elements

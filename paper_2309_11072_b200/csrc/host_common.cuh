@@ -181,7 +181,7 @@ inline ImgLayout plan(const hdll_b200_image& im, bool trace) {
   L.off_a32 = take(sizeof(float) * 768);
   L.off_b32 = take(sizeof(float) * 768);
   L.off_crc = take(sizeof(unsigned) * 8);
-  L.off_crc_part = take(sizeof(unsigned) * ((3 * n + 1019) / 1020 + 4 * ((n + kCrcChunk - 1) / kCrcChunk) + 8));
+  L.off_crc_part = take(sizeof(unsigned) * ((3 * n + kCrcChunkRgb - 1) / kCrcChunkRgb + 4 * ((n + kCrcChunk - 1) / kCrcChunk) + 8));
   L.chain_cap[0] = dct_chain_cap(nb);
   for (int k = 1; k < 5; k++) L.chain_cap[k] = plane_chain_cap(n);
   for (int k = 0; k < 5; k++) L.off_chain[k] = take(L.chain_cap[k]);
@@ -430,7 +430,7 @@ inline void fill_desc(ImgDesc& d, const hdll_b200_image& im, const ImgLayout& L,
   d.crc_part = (unsigned*)(B + L.off_crc_part);
   long long po = 0;
   for (int j = 0; j < 5; j++) {
-    long long len = j == 0 ? 3 * d.n : d.n, csz = j == 0 ? 1020 : kCrcChunk;
+    long long len = j == 0 ? 3 * d.n : d.n, csz = j == 0 ? kCrcChunkRgb : kCrcChunk;
     d.crc_chunks[j] = (len + csz - 1) / csz;
     d.crc_part_off[j] = po;
     po += d.crc_chunks[j];
