@@ -195,8 +195,11 @@ void launch_bitcat(uint8_t* dst, const uint8_t* const* src, const unsigned long 
 }
 
 void launch_assemble(const ImgDesc* d_descs, int nimg, const AsmTab& at, long long max_out, cudaStream_t st) {
-  long long blocks = (max_out + 256 * 16 - 1) / (256 * 16);
-  if (blocks > 148 * 8) blocks = 148 * 8;
+  // ~64 KiB per CTA, and about 8 CTAs per SM over the whole batch: every CTA
+  // recomputes the (small) layout first
+  long long blocks = (max_out + 65535) / 65536;
+  const long long cap = (148 * 8 + nimg - 1) / nimg;
+  if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   k_assemble<<<dim3((unsigned)blocks, nimg), 256, 0, st>>>(d_descs, at);
 }
