@@ -112,6 +112,36 @@ int hdll_b200_stage_times(hdll_b200_ctx *ctx, float *ms, int n);
 const char *hdll_b200_status_string(int status);
 
 /* ---------------------------------------------------------------------------
+ * GPU decoder: decode_hdr / decode_sdr (container.py:233-280),
+ * lossy_decode (codec_core.py:536-548), lossless_decode (:316-331).  The host
+ * parses the stream (header, table, frames); the coder bodies (after their
+ * <II> w, h) go to the device, the adaptive-Rice streams are decoded one
+ * thread per stream, the rest runs data parallel.
+ * ------------------------------------------------------------------------- */
+typedef struct hdll_b200_decode_image {
+  uint32_t width, height;
+  int32_t quality, slrme, sigma_milli, radius;
+  int32_t sdr_only;          /* 1: decode_sdr -- base layer only, output (h, w, 3) */
+  const double *taps;        /* host, 2 * radius + 1 Gaussian taps (sigma_milli > 0) */
+  const float *a32, *b32;    /* host [3][256] regression table, absent entries NaN */
+  const uint8_t *body[5];    /* host: base, E, R, G, B coder bodies without their <II> w, h */
+  uint64_t body_len[5];
+  uint32_t crc[5];           /* the frames' CRC-32 fields */
+} hdll_b200_decode_image;
+
+enum {
+  HDLL_B200_DEC_BAD = 1 << 0,        /* bit k: coder body k ended early or is inconsistent (CorruptPayloadError) */
+  HDLL_B200_DEC_CRC = 1 << 8,        /* bit 8 + k: payload k failed its CRC-32 (ChecksumError) */
+  HDLL_B200_DEC_NO_ENTRY = 1 << 13   /* an exponent has no regression entry (StreamError) */
+};
+
+/* Decode a batch; d_out[i] (device) receives image i's (h, w, 4) RGBE quads
+ * (or (h, w, 3) SDR), h_status[i] its decode status bits (0 = ok).  Returns
+ * after the batch completes. */
+int hdll_b200_decode_batch(hdll_b200_ctx *ctx, const hdll_b200_decode_image *imgs, int n, uint8_t *const *d_out,
+                           uint32_t *h_status, void *stream);
+
+/* ---------------------------------------------------------------------------
  * Tile-sharded single image (BASELINE config 3).  The reference
  * encodes one image in one process (container.py:131-230); here each rank of
  * a job codes a contiguous band of rows and the ranks exchange only the

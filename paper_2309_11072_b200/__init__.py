@@ -3,7 +3,8 @@ of arXiv 2309.11072 -- a drop-in for the reference package `hdll`'s encode path.
 
 `encode()` mirrors hdll.container.encode (reference container.py:131-230); all
 compute runs in the CUDA kernels of libhdll_b200.so (csrc/), reached through the
-C ABI in include/hdll_b200.h.  There is no CPU fallback.
+C ABI in include/hdll_b200.h.  There is no CPU fallback.  `decode_hdr` /
+`decode_sdr` (container.py:233-280) decode on the GPU as well.
 """
 
 from .container import (
@@ -29,5 +30,7 @@ from .container import (
     section_sizes,
     serialize,
 )
+
+from .decode import decode_hdr, decode_hdr_batch, decode_sdr
 
 __version__ = "0.1.0"

@@ -24,7 +24,10 @@ EXPORTS = (
     "hdll_b200_stage_times", "hdll_b200_status_string",
     "hdll_b200_band_begin", "hdll_b200_band_layers", "hdll_b200_band_fit_send", "hdll_b200_band_fit_owner",
     "hdll_b200_band_code", "hdll_b200_band_maps", "hdll_b200_band_emit", "hdll_b200_assemble_pieces",
+    "hdll_b200_decode_batch",
 )
+
+DEC_BAD, DEC_CRC, DEC_NO_ENTRY = 1 << 0, 1 << 8, 1 << 13
 
 BAND_PIECES, BAND_CTX = 7, 6
 
@@ -47,6 +50,14 @@ class Image(ctypes.Structure):
         ("hdr_post", ctypes.c_void_p), ("hdr_post_len", ctypes.c_uint32),
         ("params", Params),
     ]
+
+
+class DecodeImage(ctypes.Structure):
+    _fields_ = [("width", ctypes.c_uint32), ("height", ctypes.c_uint32), ("quality", ctypes.c_int32),
+                ("slrme", ctypes.c_int32), ("sigma_milli", ctypes.c_int32), ("radius", ctypes.c_int32),
+                ("sdr_only", ctypes.c_int32), ("taps", ctypes.POINTER(ctypes.c_double)),
+                ("a32", ctypes.POINTER(ctypes.c_float)), ("b32", ctypes.POINTER(ctypes.c_float)),
+                ("body", ctypes.c_void_p * 5), ("body_len", ctypes.c_uint64 * 5), ("crc", ctypes.c_uint32 * 5)]
 
 
 class Band(ctypes.Structure):
@@ -109,6 +120,8 @@ def lib():
                 "hdll_b200_band_emit": [vp, ctypes.POINTER(ctypes.c_int32), u64p, u64p],
                 "hdll_b200_assemble_pieces": [vp, ctypes.POINTER(Image), u32p, f32p, f32p, u32p,
                                               ctypes.POINTER(ctypes.c_int32), u64p, u64p, vp, ctypes.c_uint64, vp, vp],
+                "hdll_b200_decode_batch": [vp, ctypes.POINTER(DecodeImage), ctypes.c_int,
+                                           ctypes.POINTER(ctypes.c_void_p), u32p, vp],
             }
             for name, args in sig.items():
                 getattr(L, name).argtypes = args

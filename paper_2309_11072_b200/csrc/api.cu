@@ -204,6 +204,124 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   return HDLL_B200_OK;
 }
 
+// GPU decode of a batch (decode.cu); synchronous.
+int run_decode(Ctx* c, const hdll_b200_decode_image* imgs, int n, uint8_t* const* d_out, uint32_t* h_status,
+               cudaStream_t st) {
+  if (n <= 0) return HDLL_B200_E_ARG;
+  CK(cudaSetDevice(c->device));
+  c->launches = 0;
+  // each image as the encoder's descriptor (same arena layout), plus its coder bodies
+  std::vector<hdll_b200_image> ims(n);
+  std::vector<ImgLayout> lays(n);
+  std::vector<size_t> base(n);
+  size_t total = 0;
+  for (int i = 0; i < n; i++) {
+    const auto& di = imgs[i];
+    if (di.width == 0 || di.height == 0) return HDLL_B200_E_EMPTY;
+    if (di.quality < 1 || di.quality > 100 || di.sigma_milli < 0 || di.radius < 0) return HDLL_B200_E_ARG;
+    if (!di.sdr_only && di.slrme && di.sigma_milli && (!di.taps || di.radius < 1)) return HDLL_B200_E_ARG;
+    hdll_b200_image& im = ims[i];
+    memset(&im, 0, sizeof(im));
+    im.width = di.width;
+    im.height = di.height;
+    im.params.quality = di.quality;
+    im.params.sigma_milli = di.sigma_milli;
+    im.params.slrme = di.slrme;
+    im.params.blas_threads = 1;
+    im.params.radius = di.radius;
+    im.params.taps = di.taps;
+    lays[i] = plan(im, false);
+    base[i] = total;
+    total += lays[i].total;
+    for (int k = 0; k < 5; k++) total = align_up(total + (di.sdr_only && k ? 0 : di.body_len[k]) + 16);
+  }
+  if (ensure(&c->arena, &c->arena_cap, total, true)) return HDLL_B200_E_CUDA;
+  uint8_t* A = (uint8_t*)c->arena;
+  size_t stage_bytes = align_up(sizeof(ImgDesc) * n) + 4 * kAlign;
+  for (int i = 0; i < n; i++) stage_bytes += params_stage_bytes(ims[i]) + 2 * align_up(4 * 768);
+  const int slot = c->slot;
+  c->slot ^= 1;
+  if (c->slot_ev[slot]) CK(cudaEventSynchronize(c->slot_ev[slot]));
+  else CK(cudaEventCreateWithFlags(&c->slot_ev[slot], cudaEventDisableTiming));
+  if (ensure(&c->pinned_slot[slot], &c->pinned_cap_slot[slot], stage_bytes + 4096, false)) return HDLL_B200_E_CUDA;
+  if (ensure(&c->tabs_slot[slot], &c->tabs_cap_slot[slot], stage_bytes + 4096, true)) return HDLL_B200_E_CUDA;
+  uint8_t* H = (uint8_t*)c->pinned_slot[slot];
+  uint8_t* D = (uint8_t*)c->tabs_slot[slot];
+  size_t so = 0;
+  auto stage = [&](const void* src, size_t bytes) {
+    size_t r = so;
+    if (bytes && src) memcpy(H + so, src, bytes);
+    so = align_up(so + bytes);
+    return r;
+  };
+  const size_t t_descs = stage(nullptr, sizeof(ImgDesc) * n);
+  std::vector<ImgDesc> ds(n);
+  long long max_n = 0;
+  int max_w = 0, max_h = 0, max_radius = 0, max_base_tiles = 0;
+  bool any_real = false, all_sdr = true;
+  for (int i = 0; i < n; i++) {
+    const auto& di = imgs[i];
+    uint8_t* B = A + base[i];
+    const StagedParams sp = stage_params(stage, ims[i]);
+    ImgDesc& d = ds[i];
+    fill_desc(d, ims[i], lays[i], B, 0, false, D, sp);
+    d.decode = 1;
+    d.hist_fused = 0;
+    d.slrme = di.sdr_only ? 0 : di.slrme;
+    d.crc_mask = di.sdr_only ? 0x1 : 0x1F;
+    d.out_rgbe = d_out[i];
+    d.a32 = (float*)(D + stage(di.a32, 4 * 768));
+    d.b32 = (float*)(D + stage(di.b32, 4 * 768));
+    size_t o = base[i] + lays[i].total;
+    for (int k = 0; k < 5; k++) {
+      const size_t len = di.sdr_only && k ? 0 : di.body_len[k];
+      d.pay[k] = A + o;
+      d.pay_bytes[k] = (long long)len;
+      if (len) CK(cudaMemcpyAsync(A + o, di.body[k], len, cudaMemcpyHostToDevice, st));
+      o = align_up(o + len + 16);
+    }
+    max_n = std::max(max_n, d.n);
+    max_w = std::max(max_w, d.w);
+    max_h = std::max(max_h, d.h);
+    max_radius = std::max(max_radius, d.radius);
+    max_base_tiles = std::max(max_base_tiles, (d.nbx + 15) / 16 * d.nby);
+    any_real |= d.slrme && d.sigma_milli;
+    all_sdr &= di.sdr_only != 0;
+  }
+  memcpy(H + t_descs, ds.data(), sizeof(ImgDesc) * n);
+  CK(cudaMemcpyAsync(D, H, so, cudaMemcpyHostToDevice, st));
+  for (int i = 0; i < n; i++) {
+    CK(cudaMemsetAsync(A + base[i] + lays[i].off_zero, 0, kZeroBytes, st));
+    CK(cudaMemsetAsync(ds[i].zz, 0, sizeof(int16_t) * 3 * ds[i].nblocks * 64, st));
+  }
+  const ImgDesc* dd = (const ImgDesc*)(D + t_descs);
+  launch_decode_coders(dd, n, !all_sdr, st);
+  launch_reconstruct(dd, n, max_base_tiles, st);
+  c->launches += 2;
+  if (any_real) {
+    launch_prefilter(dd, n, max_w, max_h, max_radius, st);
+    c->launches += 1;
+  }
+  launch_decode_output(dd, n, max_n, st);
+  launch_crc(dd, n, max_n, st);
+  c->launches += 3;
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(c->slot_ev[slot], st));
+  CK(cudaStreamSynchronize(st));
+  for (int i = 0; i < n; i++) {
+    unsigned s = 0, crc[5] = {0, 0, 0, 0, 0};
+    CK(cudaMemcpy(&s, ds[i].status, 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(crc, ds[i].crc, sizeof(crc), cudaMemcpyDeviceToHost));
+    uint32_t out = (s >> 16) & 0x1F;                    // stream k failed to decode
+    if (s & (1u << 21)) out |= HDLL_B200_DEC_NO_ENTRY;  // exponent without a regression entry
+    for (int k = 0; k < 5; k++)
+      if (((ds[i].crc_mask >> k) & 1) && !((out >> k) & 1) && crc[k] != imgs[i].crc[k])
+        out |= HDLL_B200_DEC_CRC << k;
+    h_status[i] = out;
+  }
+  return HDLL_B200_OK;
+}
+
 int check_status(Ctx* c) {
   CK(cudaEventSynchronize(c->done_ev));
   unsigned worst = 0;
@@ -393,6 +511,13 @@ int hdll_b200_lossy_encode(hdll_b200_ctx* ctx, const uint8_t* h_rgb, uint32_t w,
   if (!c || !h_rgb || !h_body || !body_len || !crc || !h_decoded) return HDLL_B200_E_ARG;
   if (quality < 1 || quality > 100) return HDLL_B200_E_ARG;
   return plugin_common(c, h_rgb, (size_t)w * h * 3, w, h, quality, 2, h_body, cap, body_len, crc, h_decoded);
+}
+
+int hdll_b200_decode_batch(hdll_b200_ctx* ctx, const hdll_b200_decode_image* imgs, int n, uint8_t* const* d_out,
+                           uint32_t* h_status, void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !imgs || !d_out || !h_status) return HDLL_B200_E_ARG;
+  return run_decode(c, imgs, n, d_out, h_status, (cudaStream_t)stream);
 }
 
 int hdll_b200_last_launch_count(hdll_b200_ctx* ctx) {

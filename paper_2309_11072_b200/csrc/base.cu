@@ -157,7 +157,10 @@ __global__ void __launch_bounds__(256) k_sdr_ycc(const ImgDesc* __restrict__ des
 }
 
 // Pass 2: the 8x8 DCT round trip of one tile = 8 pixel rows x 128 columns
-// (16 blocks), everything in shared memory.
+// (16 blocks), everything in shared memory.  kDecode (the GPU decoder,
+// decode.cu): start from the decoded zigzag coefficients instead, i.e. only
+// _reconstruct (codec_core.py:478-489) -- the encoder's inverse half.
+template <bool kDecode>
 __global__ void __launch_bounds__(128, 4) k_base_layer(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
   const int tiles_x = (d.nbx + kTileBlocks - 1) / kTileBlocks;
@@ -172,6 +175,23 @@ __global__ void __launch_bounds__(128, 4) k_base_layer(const ImgDesc* __restrict
   double* bufB = smem + 3 * 8 * kRowStride;  // [3][8][kRowStride]
   const int t = threadIdx.x;
 
+  // task t: block b = t / 8, line l = t % 8, for each of the 3 components
+  const int b = t >> 3, l = t & 7;
+  const bool live = b < nblk;
+  const int col0 = b * 8;
+  const long long bi = (long long)by * d.nbx + bx0 + b;
+
+  if constexpr (kDecode) {  // dequantised coefficients, natural order (codec_core.py:481-483)
+    if (live)
+      for (int ci = 0; ci < 3; ci++) {
+        const double* qt = d.qt + (ci == 0 ? 0 : 64);
+        const int16_t* zz = d.zz + ((long long)ci * d.nblocks + bi) * 64;
+#pragma unroll
+        for (int v = 0; v < 8; v++)
+          bufA[(ci * 8 + l) * kRowStride + col0 + v] = (double)zz[c_zigzag[l * 8 + v]] * qt[l * 8 + v];
+      }
+    __syncthreads();
+  } else {
   // 1. the tile's YCC samples, edge-padded (np.pad mode="edge", codec_core.py:432-436)
   {
     const int rx = t;
@@ -190,11 +210,6 @@ __global__ void __launch_bounds__(128, 4) k_base_layer(const ImgDesc* __restrict
     }
   }
   __syncthreads();
-
-  // task t: block b = t / 8, line l = t % 8, for each of the 3 components
-  const int b = t >> 3, l = t & 7;
-  const bool live = b < nblk;
-  const int col0 = b * 8;
 
   // 2. forward pass 1 (dct_blocks first loop): tmp[u][x] = sum_t C[u][t] * blk[t][x], x = l
   if (live) {
@@ -215,7 +230,6 @@ __global__ void __launch_bounds__(128, 4) k_base_layer(const ImgDesc* __restrict
   __syncthreads();
 
   // 3. forward pass 2: out[u][v] = sum_t tmp[u][t] * C[v][t], u = l; quantise, zigzag, dequantise
-  const long long bi = (long long)by * d.nbx + bx0 + b;
   if (live) {
 #pragma unroll 1
     for (int ci = 0; ci < 3; ci++) {
@@ -237,6 +251,8 @@ __global__ void __launch_bounds__(128, 4) k_base_layer(const ImgDesc* __restrict
     }
   }
   __syncthreads();
+
+  }  // !kDecode
 
   // 4. inverse pass 1 (idct_blocks first loop): tmp[x][v] = sum_t C[t][x] * coef[t][v], v = l
   if (live) {
@@ -331,10 +347,17 @@ void launch_base_layer(const ImgDesc* d_descs, int nimg, int max_tiles, long lon
   size_t smem = sizeof(double) * 2 * 3 * 8 * kRowStride;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_base_layer, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_base_layer<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_base_layer<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_base_layer<<<dim3(max_tiles, nimg), 128, smem, st>>>(d_descs);
+  k_base_layer<false><<<dim3(max_tiles, nimg), 128, smem, st>>>(d_descs);
+}
+
+void launch_reconstruct(const ImgDesc* d_descs, int nimg, int max_tiles, cudaStream_t st) {
+  size_t smem = sizeof(double) * 2 * 3 * 8 * kRowStride;
+  cudaFuncSetAttribute(k_base_layer<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_base_layer<true><<<dim3(max_tiles, nimg), 128, smem, st>>>(d_descs);
 }
 
 }  // namespace hdll

@@ -15,6 +15,7 @@ constexpr int kRiceMaxK = 15;    // _kernels.py:13
 constexpr int kRiceEscapeQ = 24; // _kernels.py:14
 constexpr int kStateReset = 64;  // _kernels.py:15
 constexpr int kEOB = 64;         // _kernels.py:19
+constexpr int kRunCtx = 4;       // _kernels.py:17
 
 // Error bits written to the per-launch device status word.
 enum : uint32_t {

@@ -93,6 +93,12 @@ struct ImgDesc {
   long long crc_part_off[5];
 
 
+  // GPU decoder (decode.cu): coder bodies in, RGBE (or the SDR) out
+  int decode;                 // 1: this desc decodes
+  const uint8_t* pay[5];      // base, E, R, G, B coder bodies (MSB-first bits after the <II> w, h)
+  long long pay_bytes[5];
+  uint8_t* out_rgbe;          // (h, w, 4) decoded RGBE, or (h, w, 3) SDR for an SDR-only decode
+
   // output
   uint8_t* out;               // serialized stream
   unsigned long long* out_len;
@@ -176,6 +182,9 @@ void launch_tonemap_stats(const ImgDesc*, int nimg, long long max_n, int max_lev
 void launch_tonemap_partial(const ImgDesc*, int nimg, long long max_n, int max_level, cudaStream_t);
 void launch_tonemap_scalars(const ImgDesc*, int nimg, cudaStream_t);
 void launch_base_layer(const ImgDesc*, int nimg, int max_tiles, long long max_n, cudaStream_t);
+void launch_reconstruct(const ImgDesc*, int nimg, int max_tiles, cudaStream_t);
+void launch_decode_coders(const ImgDesc*, int nimg, bool planes, cudaStream_t);
+void launch_decode_output(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
 void launch_prefilter(const ImgDesc*, int nimg, int max_w, int max_h, int max_radius, cudaStream_t);
 void launch_fit(const ImgDesc*, int nimg, int max_sort_tiles, long long max_nodes, int max_chunks, cudaStream_t);
 void launch_fit_sort(const ImgDesc*, int nimg, int max_sort_tiles, cudaStream_t);

@@ -29,7 +29,6 @@
 
 namespace hdll {
 
-constexpr int kRunCtx = 4;  // _kernels.py:17
 constexpr long long kSpinLimit = 1LL << 24;
 constexpr int kDctLaneCap = 129;  // >= 127 symbols per block; odd stride against bank conflicts
 
