@@ -23,24 +23,30 @@ enum : uint32_t { kDecTruncated = 1u, kDecCorrupt = 2u, kDecBadShift = 16, kDecN
 // `avail` tells how many real bits remain (the reference fails on reading past
 // the end: _kernels.py:82-111).
 struct BitReader {
-  const uint8_t* p;
-  long long nbytes, next;  // next byte to load
+  const uint32_t* p;       // the body, 4-byte aligned (staged so by the host)
+  long long nbytes, next;  // next byte to load (a multiple of 4 while words remain)
   unsigned long long win;  // left-aligned
   int have;                // bits in win that came from the body
-  long long avail_after;   // body bits not yet loaded
 
   __device__ __forceinline__ void init(const uint8_t* data, long long bytes) {
-    p = data;
+    p = reinterpret_cast<const uint32_t*>(data);
     nbytes = bytes;
     next = 0;
     win = 0;
     have = 0;
     refill();
   }
+  // whole big-endian words while they fit; the last partial word is masked to
+  // the body (bytes past it read as 0 and do not count in `have`)
   __device__ __forceinline__ void refill() {
-    while (have <= 56 && next < nbytes) {
-      win |= (unsigned long long)p[next++] << (56 - have);
-      have += 8;
+    while (have <= 32 && next < nbytes) {
+      const uint32_t w = __byte_perm(__ldg(p + (next >> 2)), 0, 0x0123);
+      const long long left = nbytes - next;
+      const int nb = left >= 4 ? 4 : (int)left;
+      const uint32_t wm = nb == 4 ? w : (w & ~(0xFFFFFFFFu >> (8 * nb)));
+      win |= (unsigned long long)wm << (32 - have);
+      have += 8 * nb;
+      next += nb;
     }
   }
   __device__ __forceinline__ unsigned long long take(int k) {  // k in [1, 32], have >= k
@@ -82,20 +88,43 @@ struct BitReader {
   }
 };
 
-__device__ __forceinline__ int select_k_dec(long long a, long long n) {  // _select_k
-  int k = 0;
-  while ((n << k) < a && k < kRiceMaxK) k++;
-  return k;
+// _select_k (_kernels.py:114-119): smallest k <= 15 with (N << k) >= A, closed form
+__device__ __forceinline__ int select_k_dec(long long a, long long n) {
+  if (a <= n) return 0;
+  const int k0 = __clzll(n) - __clzll(a - 1);  // bitlen(a-1) - bitlen(n) >= 0
+  const int k = ((n << k0) >= a) ? k0 : k0 + 1;
+  return k < kRiceMaxK ? k : kRiceMaxK;
 }
 
-__device__ __forceinline__ void update_dec(long long* A, long long* N, int c, long long u) {  // _update_state
-  A[c] += u;
-  N[c] += 1;
-  if (N[c] >= kStateReset) {
-    A[c] >>= 1;
-    N[c] >>= 1;
+// Adaptive-Rice state of NC contexts in registers (no local-memory arrays on
+// the serial path); _update_state (_kernels.py:122-128)
+template <int NC>
+struct RiceState {
+  long long A[NC], N[NC];
+  __device__ __forceinline__ void reset() {
+#pragma unroll
+    for (int i = 0; i < NC; i++) A[i] = 4, N[i] = 1;
   }
-}
+  __device__ __forceinline__ int k(int c) const {
+    long long a = A[0], n = N[0];
+#pragma unroll
+    for (int i = 1; i < NC; i++)
+      if (c == i) a = A[i], n = N[i];
+    return select_k_dec(a, n);
+  }
+  __device__ __forceinline__ void update(int c, long long u) {
+#pragma unroll
+    for (int i = 0; i < NC; i++)
+      if (c == i) {
+        A[i] += u;
+        N[i] += 1;
+        if (N[i] >= kStateReset) {
+          A[i] >>= 1;
+          N[i] >>= 1;
+        }
+      }
+  }
+};
 
 __device__ __forceinline__ long long unzig(long long u) { return (u & 1) == 0 ? (u >> 1) : -((u + 1) >> 1); }
 
@@ -103,17 +132,17 @@ __device__ __forceinline__ long long unzig(long long u) { return (u & 1) == 0 ? 
 __device__ unsigned decode_dct_image(const ImgDesc& d) {
   BitReader br;
   br.init(d.pay[0], d.pay_bytes[0]);
-  long long A[6], N[6];
-  for (int i = 0; i < 6; i++) A[i] = 4, N[i] = 1;
+  RiceState<6> rs;
+  rs.reset();
   for (int ci = 0; ci < 3; ci++) {
     const int base = ci == 0 ? 0 : 3;
     int16_t* zc = d.zz + (long long)ci * d.nblocks * 64;
     long long prev_dc = 0;
     for (long long b = 0; b < d.nblocks; b++) {
       int16_t* z = zc + b * 64;
-      long long s = br.rice(select_k_dec(A[base], N[base]));
+      long long s = br.rice(rs.k(base));
       if (s < 0) return kDecTruncated;
-      update_dec(A, N, base, s);
+      rs.update(base, s);
       bool ok = true;
       const long long u = s > 0 ? br.raw(s, &ok) : 0;
       if (!ok) return kDecTruncated;
@@ -121,15 +150,15 @@ __device__ unsigned decode_dct_image(const ImgDesc& d) {
       z[0] = (int16_t)prev_dc;
       int pos = 1;
       while (pos < 64) {
-        const long long run = br.rice(select_k_dec(A[base + 1], N[base + 1]));
+        const long long run = br.rice(rs.k(base + 1));
         if (run < 0) return kDecTruncated;
-        update_dec(A, N, base + 1, run);
+        rs.update(base + 1, run);
         if (run == kEOB) break;
         pos += (int)run;
         if (run > 63 || pos > 63) return kDecCorrupt;
-        s = br.rice(select_k_dec(A[base + 2], N[base + 2]));
+        s = br.rice(rs.k(base + 2));
         if (s < 0) return kDecTruncated;
-        update_dec(A, N, base + 2, s);
+        rs.update(base + 2, s);
         if (s == 0 || s > 62) return kDecCorrupt;
         const long long v = br.raw(s, &ok);
         if (!ok) return kDecTruncated;
@@ -141,17 +170,20 @@ __device__ unsigned decode_dct_image(const ImgDesc& d) {
   return 0;
 }
 
-// decode_plane for one plane (kind 1 = E, 2..4 = residual R, G, B)
-__device__ unsigned decode_plane_dev(const ImgDesc& d, int kind) {
+// decode_plane for one plane (kind 1 = E, 2..4 = residual R, G, B); the row
+// above is kept in this thread's shared-memory buffers (the global copy was
+// just written, so it would come back from L2 on the serial path)
+__device__ unsigned decode_plane_dev(const ImgDesc& d, int kind, uint8_t* rows /* 2 * w */) {
   uint8_t* P = kind == 1 ? d.e_plane : d.res_planes + (long long)(kind - 2) * d.n;
   BitReader br;
   br.init(d.pay[kind], d.pay_bytes[kind]);
-  long long A[5], N[5];
-  for (int i = 0; i < 5; i++) A[i] = 4, N[i] = 1;
+  RiceState<5> rs;
+  rs.reset();
   const int w = d.w;
+  uint8_t* up = nullptr;
+  uint8_t* cur = rows;
   for (int y = 0; y < d.h; y++) {
-    uint8_t* row = P + (long long)y * w;
-    const uint8_t* up = y > 0 ? row - w : nullptr;
+    uint8_t* grow = P + (long long)y * w;
     int x = 0;
     bool forced = false;
     int left = up ? up[0] : 128;  // a at x = 0 (_kernels.py:131-143)
@@ -162,14 +194,17 @@ __device__ unsigned decode_plane_dev(const ImgDesc& d, int kind) {
       if (!forced && a == b && b == c) {
         long long run = 0;
         for (;;) {
-          const long long chunk = br.rice(select_k_dec(A[kRunCtx], N[kRunCtx]));
+          const long long chunk = br.rice(rs.k(kRunCtx));
           if (chunk < 0) return kDecTruncated;
-          update_dec(A, N, kRunCtx, chunk);
+          rs.update(kRunCtx, chunk);
           run += chunk;
           if (chunk < 255) break;
         }
         if (x + run > w) return kDecCorrupt;
-        for (long long i = 0; i < run; i++) row[x + i] = (uint8_t)a;
+        for (long long i = 0; i < run; i++) {
+          cur[x + i] = (uint8_t)a;
+          grow[x + i] = (uint8_t)a;
+        }
         x += (int)run;
         if (x < w) forced = true;
         continue;
@@ -178,27 +213,31 @@ __device__ unsigned decode_plane_dev(const ImgDesc& d, int kind) {
       const int pred = c >= mx ? mn : (c <= mn ? mx : a + b - c);
       const int gg = abs(a - c) + abs(c - b);
       const int ctx = gg == 0 ? 0 : (gg <= 2 ? 1 : (gg <= 8 ? 2 : 3));
-      const long long u = br.rice(select_k_dec(A[ctx], N[ctx]));
+      const long long u = br.rice(rs.k(ctx));
       if (u < 0) return kDecTruncated;
       const int v = (int)((pred + unzig(u)) & 255);
-      row[x] = (uint8_t)v;
+      cur[x] = (uint8_t)v;
+      grow[x] = (uint8_t)v;
       left = v;
-      update_dec(A, N, ctx, u);
+      rs.update(ctx, u);
       x++;
       forced = false;
     }
-    (void)left;
+    up = cur;
+    cur = cur == rows ? rows + w : rows;
   }
   return 0;
 }
 
-// one thread per stream: thread 0 of image i the base layer, threads 1..4 its planes
-__global__ void __launch_bounds__(32) k_decode_coders(const ImgDesc* __restrict__ descs, int with_planes) {
+// one thread per stream: thread 0 of image i the base layer, threads 1..4 its
+// planes (each with 2 rows of dynamic shared memory)
+__global__ void __launch_bounds__(32) k_decode_coders(const ImgDesc* __restrict__ descs, int with_planes, int max_w) {
+  extern __shared__ uint8_t dec_rows[];
   const ImgDesc& d = descs[blockIdx.x];
   const int t = threadIdx.x;
   unsigned st = 0;
   if (t == 0) st = decode_dct_image(d);
-  else if (t <= 4 && with_planes) st = decode_plane_dev(d, t);
+  else if (t <= 4 && with_planes) st = decode_plane_dev(d, t, dec_rows + (long long)(t - 1) * 2 * max_w);
   if (st) atomicOr(d.status, 1u << (kDecBadShift + t));
 }
 
@@ -241,8 +280,10 @@ __global__ void __launch_bounds__(256) k_decode_output(const ImgDesc* __restrict
   }
 }
 
-void launch_decode_coders(const ImgDesc* d_descs, int nimg, bool planes, cudaStream_t st) {
-  k_decode_coders<<<nimg, 32, 0, st>>>(d_descs, planes ? 1 : 0);
+void launch_decode_coders(const ImgDesc* d_descs, int nimg, bool planes, int max_w, cudaStream_t st) {
+  const size_t smem = planes ? (size_t)8 * max_w : 0;
+  cudaFuncSetAttribute(k_decode_coders, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_decode_coders<<<nimg, 32, smem, st>>>(d_descs, planes ? 1 : 0, max_w);
 }
 
 void launch_decode_output(const ImgDesc* d_descs, int nimg, long long max_n, cudaStream_t st) {

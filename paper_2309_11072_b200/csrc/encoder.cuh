@@ -183,7 +183,7 @@ void launch_tonemap_partial(const ImgDesc*, int nimg, long long max_n, int max_l
 void launch_tonemap_scalars(const ImgDesc*, int nimg, cudaStream_t);
 void launch_base_layer(const ImgDesc*, int nimg, int max_tiles, long long max_n, cudaStream_t);
 void launch_reconstruct(const ImgDesc*, int nimg, int max_tiles, cudaStream_t);
-void launch_decode_coders(const ImgDesc*, int nimg, bool planes, cudaStream_t);
+void launch_decode_coders(const ImgDesc*, int nimg, bool planes, int max_w, cudaStream_t);
 void launch_decode_output(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
 void launch_prefilter(const ImgDesc*, int nimg, int max_w, int max_h, int max_radius, cudaStream_t);
 void launch_fit(const ImgDesc*, int nimg, int max_sort_tiles, long long max_nodes, int max_chunks, cudaStream_t);
