@@ -345,12 +345,7 @@ void launch_base_layer(const ImgDesc* d_descs, int nimg, int max_tiles, long lon
   if (gx < 1) gx = 1;
   k_sdr_ycc<<<dim3(gx, nimg), 256, 0, st>>>(d_descs);
   size_t smem = sizeof(double) * 2 * 3 * 8 * kRowStride;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_base_layer<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_base_layer<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  cudaFuncSetAttribute(k_base_layer<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  // per device
   k_base_layer<false><<<dim3(max_tiles, nimg), 128, smem, st>>>(d_descs);
 }
 
