@@ -127,18 +127,76 @@ __device__ __forceinline__ void prefilter_tile(const ImgDesc& d, int c, int y0, 
 __global__ void __launch_bounds__(256) k_prefilter_fused(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.z / 3];
   const int c = blockIdx.z % 3;
-  if (!d.slrme || d.sigma_milli == 0 || d.radius > kFusedMaxR) return;
+  if (!d.slrme || d.sigma_milli == 0 || d.radius > kFusedMaxR || d.radius == 3) return;
   const int tiles_x = (d.w + kTW - 1) / kTW;
   const int ty = blockIdx.x / tiles_x, tx = blockIdx.x % tiles_x;
   const int y0 = ty * kTH, x0 = tx * kTW;
   if (y0 >= d.h) return;
   __shared__ PfSmem sm;
-  if (d.radius == 3) prefilter_tile<3>(d, c, y0, x0, sm);  // sigma 1.0 (the default)
-  else prefilter_tile<0>(d, c, y0, x0, sm);
+  prefilter_tile<0>(d, c, y0, x0, sm);  // radius 3 (sigma 1.0, the default) runs in k_prefilter_cols
+}
+
+// Column kernel for a compile-time radius R (the default sigma = 1 has R = 3):
+// a CTA of 256 threads owns 256 - 2R output columns x kCR output rows of one
+// channel.  Vertical pass: thread = staged column, a (2R + 1)-sample window
+// slides down it in registers (coalesced u8 row loads).  Horizontal pass:
+// thread = output column, reading the vertical results of its row from
+// shared memory.  Same operation order as scipy's symmetric branch.
+constexpr int kCR = 16;
+
+template <int R>
+__global__ void __launch_bounds__(256) k_prefilter_cols(const ImgDesc* __restrict__ descs) {
+  const ImgDesc& d = descs[blockIdx.z / 3];
+  const int c = blockIdx.z % 3;
+  if (!d.slrme || d.sigma_milli == 0 || d.radius != R) return;
+  constexpr int kOut = 256 - 2 * R;
+  const int tiles_x = (d.w + kOut - 1) / kOut;
+  const int ty = blockIdx.x / tiles_x, tx = blockIdx.x % tiles_x;
+  const int y0 = ty * kCR, x0 = tx * kOut;
+  if (y0 >= d.h) return;
+  __shared__ double vt[kCR][256 + 1];
+  const int t = threadIdx.x;
+  double fw[R + 1];  // fw[j] = taps[R - j]: centre, then outward
+#pragma unroll
+  for (int j = 0; j <= R; j++) fw[j] = d.taps[R - j];
+  const uint8_t* S = d.s_planes + (long long)c * d.n;
+  const int gx = reflect_idx((long long)x0 - R + t, d.w);
+  // vertical pass over rows y0 .. y0 + kCR - 1 of column gx
+  double win[2 * R + 1];
+#pragma unroll
+  for (int i = 0; i < 2 * R; i++) win[i + 1] = (double)__ldg(S + (long long)reflect_idx((long long)y0 - R + i, d.h) * d.w + gx);
+#pragma unroll
+  for (int oy = 0; oy < kCR; oy++) {
+#pragma unroll
+    for (int i = 0; i < 2 * R; i++) win[i] = win[i + 1];
+    win[2 * R] = (double)__ldg(S + (long long)reflect_idx((long long)y0 + oy + R, d.h) * d.w + gx);
+    double o = win[R] * fw[0];
+#pragma unroll
+    for (int j = R; j >= 1; j--) o += (win[R - j] + win[R + j]) * fw[j];
+    vt[oy][t] = o;
+  }
+  __syncthreads();
+  // horizontal pass
+  const int x = x0 + t - R;
+  if (t < R || t >= 256 - R || x >= d.w) return;
+  double* out = d.sstar + (long long)c * d.n;
+#pragma unroll 4
+  for (int oy = 0; oy < kCR; oy++) {
+    const int y = y0 + oy;
+    if (y >= d.h) break;
+    double o = vt[oy][t] * fw[0];
+#pragma unroll
+    for (int j = R; j >= 1; j--) o += (vt[oy][t - j] + vt[oy][t + j]) * fw[j];
+    out[(long long)y * d.w + x] = o;
+  }
 }
 
 void launch_prefilter(const ImgDesc* d_descs, int nimg, int max_w, int max_h, int max_radius, cudaStream_t st) {
-  if (max_radius <= kFusedMaxR) {
+  if (max_radius >= 3) {  // the images of radius 3 (sigma 1, the default); the others return at once
+    const int tiles = ((max_w + 249) / 250) * ((max_h + kCR - 1) / kCR);
+    k_prefilter_cols<3><<<dim3(tiles, 1, nimg * 3), 256, 0, st>>>(d_descs);
+  }
+  if (max_radius <= kFusedMaxR) {  // (images of other radii; radius-3 ones return at once)
     const int tiles = ((max_w + kTW - 1) / kTW) * ((max_h + kTH - 1) / kTH);
     k_prefilter_fused<<<dim3(tiles, 1, nimg * 3), 256, 0, st>>>(d_descs);
     return;
