@@ -19,10 +19,13 @@ __global__ void __launch_bounds__(256) k_estimate(const ImgDesc* __restrict__ de
     }
   __syncthreads();
   const bool real = d.sigma_milli != 0;
-  long long nq = (d.n + 3) / 4;
+  const long long nq = (d.n + 3) / 4;
+  // whole quads go through 128-bit S* loads and 32-bit plane stores when the
+  // channel planes (c * n) keep that alignment (n % 4 == 0)
+  const bool vec = (d.n & 3) == 0 && !d.want_trace;
   for (long long qi = (long long)blockIdx.x * blockDim.x + threadIdx.x; qi < nq;
        qi += (long long)gridDim.x * blockDim.x) {
-    long long p0 = qi * 4;
+    const long long p0 = qi * 4;
     const uint32_t* src = reinterpret_cast<const uint32_t*>(d.rgbe);
     uint32_t qs[4];
     if (p0 + 3 < d.n) {
@@ -30,6 +33,44 @@ __global__ void __launch_bounds__(256) k_estimate(const ImgDesc* __restrict__ de
       qs[0] = v.x, qs[1] = v.y, qs[2] = v.z, qs[3] = v.w;
     } else {
       for (int k = 0; k < 4; k++) qs[k] = p0 + k < d.n ? src[p0 + k] : 0u;
+    }
+    if (vec && p0 + 3 < d.n) {
+      double sv[3][4];
+#pragma unroll
+      for (int c = 0; c < 3; c++) {
+        if (d.slrme && real) {
+          const double2* sp = reinterpret_cast<const double2*>(d.sstar + (long long)c * d.n + p0);
+          const double2 lo = __ldg(sp), hi = __ldg(sp + 1);
+          sv[c][0] = lo.x, sv[c][1] = lo.y, sv[c][2] = hi.x, sv[c][3] = hi.y;
+        } else {
+          const uint32_t s4 = *reinterpret_cast<const uint32_t*>(d.s_planes + (long long)c * d.n + p0);
+#pragma unroll
+          for (int k = 0; k < 4; k++) sv[c][k] = (double)((s4 >> (8 * k)) & 0xFF);
+        }
+      }
+      uint32_t e4 = 0, r4[3] = {0u, 0u, 0u};
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const uint32_t q = qs[k];
+        const unsigned e = q >> 24;
+        e4 |= e << (8 * k);
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+          const unsigned m = (q >> (8 * c)) & 0xFF;
+          unsigned ms;
+          if (d.slrme) {
+            const double est = (double)sa[c * 256 + e] * sv[c][k] + (double)sb[c * 256 + e];
+            ms = (unsigned)clampd(rha(est), 0.0, 255.0);
+          } else {
+            ms = (unsigned)sv[c][k];
+          }
+          r4[c] |= ((m - ms) & 255u) << (8 * k);
+        }
+      }
+      *reinterpret_cast<uint32_t*>(d.e_plane + p0) = e4;
+#pragma unroll
+      for (int c = 0; c < 3; c++) *reinterpret_cast<uint32_t*>(d.res_planes + (long long)c * d.n + p0) = r4[c];
+      continue;
     }
 #pragma unroll
     for (int k = 0; k < 4; k++) {
