@@ -347,6 +347,8 @@ int hdll_b200_ctx_create(hdll_b200_ctx** out, int device) {
   c->device = device;
   upload_base_constants();
   upload_crc_constants();
+  upload_fit_constants();
+  upload_tonemap_constants();
   CK(cudaGetLastError());
   *out = reinterpret_cast<hdll_b200_ctx*>(c);
   return HDLL_B200_OK;

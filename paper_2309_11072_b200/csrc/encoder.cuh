@@ -178,6 +178,8 @@ struct AsmTab {
 
 void upload_base_constants();
 void upload_crc_constants();
+void upload_fit_constants();
+void upload_tonemap_constants();
 void launch_tonemap_stats(const ImgDesc*, int nimg, long long max_n, int max_level, cudaStream_t);
 void launch_tonemap_partial(const ImgDesc*, int nimg, long long max_n, int max_level, cudaStream_t);
 void launch_tonemap_scalars(const ImgDesc*, int nimg, cudaStream_t);

@@ -685,4 +685,6 @@ void launch_fit_regroup(const ImgDesc* d_desc, const RegroupTab& rt, cudaStream_
   k_fit_regroup<<<(unsigned)blocks, 256, 0, st>>>(d_desc, rt);
 }
 
+void upload_fit_constants() { upload_pw_table(); }
+
 }  // namespace hdll

@@ -75,16 +75,17 @@ __device__ double pairwise_seq(const Acc& a, long long off, long long n) {
 // so every addition happens in numpy's order -- then lane 0 combines the leaf
 // sums along the recursion tree.  Result in every lane.
 //
-// The recursion is walked without a stack: a node is its path from the root
-// (bit q = went right at depth q), recomputed from the root when the walk
-// moves to the next leaf, so all state stays in registers; the combine keeps
-// one pending left-sibling sum per depth in shared memory.
+// Every lane finds its own leaves by descending from the root with a table of
+// leaf counts per subtree size; a leaf's path (bit q = went right at depth q)
+// drives the combine, which keeps one pending left-sibling sum per depth in
+// shared memory.
 constexpr int kMaxLeaves = 160;  // n <= 8192
 
 struct PwScratch {
   double leaf[kMaxLeaves];
   long long lo[kMaxLeaves];
-  int ln[kMaxLeaves];
+  int ln[kMaxLeaves];         // size | depth << 16
+  unsigned path[kMaxLeaves];  // bit q: went right at depth q
   double pending[32];
 };
 
@@ -93,57 +94,63 @@ __device__ __forceinline__ long long pw_split(long long m) {
   return n2 - n2 % 8;
 }
 
-// f(index, leaf offset, leaf size, path, depth) for every leaf, left to right
-template <class F>
-__device__ __forceinline__ void pw_leaves(long long off, long long n, F&& f) {
-  unsigned path = 0;
-  int depth = 0;
-  long long lo = off, m = n;
-  while (m > 128) {
-    m = pw_split(m);
-    depth++;
-  }
-  for (int idx = 0;; idx++) {
-    f(idx, lo, m, path, depth);
-    int k = depth - 1;  // deepest left turn
-    while (k >= 0 && ((path >> k) & 1u)) k--;
-    if (k < 0) break;
-    path = (path & ((1u << k) - 1u)) | (1u << k);
-    depth = k + 1;
-    lo = off;
-    m = n;
-    for (int q = 0; q < depth; q++) {
-      const long long n2 = pw_split(m);
-      if ((path >> q) & 1u) {
-        lo += n2;
-        m -= n2;
-      } else {
-        m = n2;
-      }
-    }
-    while (m > 128) {
-      m = pw_split(m);
-      depth++;
+// Leaves of a subtree of m <= kPwTableN elements, by size (host-built table:
+// pairwise_leaf_counts), so every lane can descend to its own leaf directly.
+constexpr int kPwTableN = 8192;
+
+__host__ __device__ inline void pairwise_leaf_counts(uint8_t* cnt /* kPwTableN + 1 */) {
+  for (int m = 0; m <= kPwTableN; m++) {
+    if (m <= 128) {
+      cnt[m] = 1;
+    } else {
+      int n2 = m / 2;
+      n2 -= n2 % 8;
+      cnt[m] = (uint8_t)(cnt[n2] + cnt[m - n2]);
     }
   }
 }
 
+// one copy per translation unit that sums pairwise trees (fit.cu, tonemap.cu)
+static __constant__ uint8_t c_pw_leaves[kPwTableN + 1];
+
+static inline void upload_pw_table() {
+  static uint8_t cnt[kPwTableN + 1];
+  pairwise_leaf_counts(cnt);
+  cudaMemcpyToSymbol(c_pw_leaves, cnt, sizeof(cnt));
+}
+
 template <class Acc>
 __device__ double warp_pairwise(const Acc& a, long long off, long long n, PwScratch& sc) {
+  const uint8_t* leaves_of = c_pw_leaves;
   const int lane = threadIdx.x & 31, grp = lane >> 3, j = lane & 7;
-  int nleaf = 0;
-  if (lane == 0)
-    pw_leaves(off, n, [&](int idx, long long lo, long long m, unsigned, int) {
-      sc.lo[idx] = lo;
-      sc.ln[idx] = (int)m;
-      nleaf = idx + 1;
-    });
-  nleaf = __shfl_sync(0xffffffffu, nleaf, 0);
+  const int nleaf = leaves_of[n];
+  // every lane descends to its leaves: (offset, size), and the path / depth the combine needs
+  for (int i = lane; i < nleaf; i += 32) {
+    long long lo = off, m = n;
+    int idx = i, depth = 0;
+    unsigned path = 0;
+    while (m > 128) {
+      const long long n2 = pw_split(m);
+      const int cl = leaves_of[n2];
+      if (idx < cl) {
+        m = n2;
+      } else {
+        idx -= cl;
+        lo += n2;
+        m -= n2;
+        path |= 1u << depth;
+      }
+      depth++;
+    }
+    sc.lo[i] = lo;
+    sc.ln[i] = (int)m | (depth << 16);
+    sc.path[i] = path;
+  }
   __syncwarp();
   for (int base = 0; base < nleaf; base += 4) {
     const int li = base + grp;
     const bool mine = li < nleaf;
-    const long long lo = mine ? sc.lo[li] : 0, ln = mine ? sc.ln[li] : 0;
+    const long long lo = mine ? sc.lo[li] : 0, ln = mine ? (sc.ln[li] & 0xFFFF) : 0;
     const long long lim = ln - (ln % 8);
     double r = 0.0;
     if (mine && ln >= 8) {
@@ -174,16 +181,17 @@ __device__ double warp_pairwise(const Acc& a, long long off, long long n, PwScra
   __syncwarp();
   double out = 0.0;
   if (lane == 0)
-    pw_leaves(off, n, [&](int idx, long long, long long, unsigned path, int depth) {
-      double v = sc.leaf[idx];
-      int dd = depth;
-      while (dd > 0 && ((path >> (dd - 1)) & 1u)) {  // a right child completes its parent: left + right
+    for (int i = 0; i < nleaf; i++) {  // post-order combine: a right child completes its parent
+      double v = sc.leaf[i];
+      const unsigned path = sc.path[i];
+      int dd = sc.ln[i] >> 16;
+      while (dd > 0 && ((path >> (dd - 1)) & 1u)) {
         v = sc.pending[dd - 1] + v;
         dd--;
       }
       if (dd == 0) out = v;
       else sc.pending[dd - 1] = v;
-    });
+    }
   __syncwarp();
   return __shfl_sync(0xffffffffu, out, 0);
 }

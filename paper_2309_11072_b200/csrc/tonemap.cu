@@ -112,4 +112,6 @@ void launch_tonemap_stats(const ImgDesc* d_descs, int nimg, long long max_n, int
   launch_tonemap_scalars(d_descs, nimg, st);
 }
 
+void upload_tonemap_constants() { upload_pw_table(); }
+
 }  // namespace hdll
