@@ -142,6 +142,32 @@ int hdll_b200_decode_batch(hdll_b200_ctx *ctx, const hdll_b200_decode_image *img
                            uint32_t *h_status, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * Radiance .hdr scanlines (radiance_io.py:119-317).  The host
+ * parses the text header and resolution line; these code the binary part.
+ * ------------------------------------------------------------------------- */
+enum {  /* scanline format errors (RadianceFormatError in the reference) */
+  HDLL_B200_HDR_LENGTH = 16,        /* new-RLE scanline length != width (detail: length, width) */
+  HDLL_B200_HDR_TRUNC_LINE = 17,    /* truncated new-RLE scanline */
+  HDLL_B200_HDR_TRUNC_RUN = 18,     /* truncated new-RLE run */
+  HDLL_B200_HDR_RUN_OVERFLOW = 19,  /* RLE run overflows scanline width */
+  HDLL_B200_HDR_ZERO_LITERAL = 20,  /* zero-length literal packet */
+  HDLL_B200_HDR_LIT_OVERFLOW = 21,  /* RLE literal overflows scanline width */
+  HDLL_B200_HDR_TRUNC_LIT = 22,     /* truncated new-RLE literal */
+  HDLL_B200_HDR_TRUNC_DATA = 23,    /* truncated scanline data (flat / old-RLE) */
+  HDLL_B200_HDR_REPEAT_FIRST = 24,  /* repeat marker before any pixel */
+  HDLL_B200_HDR_REPEAT_OVERFLOW = 25 /* old-RLE repeat overflows scanline width */
+};
+
+/* Scanline bytes (everything after the resolution line) -> d_rgbe (h, w, 4)
+ * on the device.  h_consumed: bytes used; h_detail[2]: values for the message. */
+int hdll_b200_hdr_decode(hdll_b200_ctx *ctx, const uint8_t *h_data, uint64_t len, uint32_t width, uint32_t height,
+                         uint8_t *d_rgbe, uint64_t *h_consumed, int64_t *h_detail, void *stream);
+/* d_rgbe (h, w, 4) on the device -> scanline bytes on the host (new-RLE for
+ * widths 8..32767 when rle, else flat).  Capacity: 4 h (1 + w + (w + 127) / 128) + 4 h w suffices. */
+int hdll_b200_hdr_encode(hdll_b200_ctx *ctx, const uint8_t *d_rgbe, uint32_t width, uint32_t height, int32_t rle,
+                         uint8_t *h_out, uint64_t cap, uint64_t *h_len, void *stream);
+
+/* ---------------------------------------------------------------------------
  * Tile-sharded single image (BASELINE config 3).  The reference
  * encodes one image in one process (container.py:131-230); here each rank of
  * a job codes a contiguous band of rows and the ranks exchange only the

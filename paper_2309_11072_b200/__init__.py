@@ -32,5 +32,6 @@ from .container import (
 )
 
 from .decode import decode_hdr, decode_hdr_batch, decode_sdr
+from .hdr_io import RadianceFormatError, parse_hdr, read_hdr_file, write_hdr, write_hdr_file
 
 __version__ = "0.1.0"

@@ -24,7 +24,7 @@ EXPORTS = (
     "hdll_b200_stage_times", "hdll_b200_status_string",
     "hdll_b200_band_begin", "hdll_b200_band_layers", "hdll_b200_band_fit_send", "hdll_b200_band_fit_owner",
     "hdll_b200_band_code", "hdll_b200_band_maps", "hdll_b200_band_emit", "hdll_b200_assemble_pieces",
-    "hdll_b200_decode_batch",
+    "hdll_b200_decode_batch", "hdll_b200_hdr_decode", "hdll_b200_hdr_encode",
 )
 
 DEC_BAD, DEC_CRC, DEC_NO_ENTRY = 1 << 0, 1 << 8, 1 << 13
@@ -122,6 +122,9 @@ def lib():
                                               ctypes.POINTER(ctypes.c_int32), u64p, u64p, vp, ctypes.c_uint64, vp, vp],
                 "hdll_b200_decode_batch": [vp, ctypes.POINTER(DecodeImage), ctypes.c_int,
                                            ctypes.POINTER(ctypes.c_void_p), u32p, vp],
+                "hdll_b200_hdr_decode": [vp, vp, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, vp, u64p, i64p, vp],
+                "hdll_b200_hdr_encode": [vp, vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int32, vp, ctypes.c_uint64,
+                                         u64p, vp],
             }
             for name, args in sig.items():
                 getattr(L, name).argtypes = args

@@ -371,6 +371,7 @@ void hdll_b200_ctx_destroy(hdll_b200_ctx* ctx) {
   if (c->d_len) cudaFree(c->d_len);
   band_free(c);
   if (c->plane_scratch) cudaFree(c->plane_scratch);
+  if (c->hdr_buf) cudaFree(c->hdr_buf);
   if (c->done_ev) cudaEventDestroy(c->done_ev);
   for (int k = 0; k <= kStages; k++)
     if (c->stage_ev[k]) cudaEventDestroy(c->stage_ev[k]);

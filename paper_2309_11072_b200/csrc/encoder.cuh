@@ -187,6 +187,10 @@ void launch_base_layer(const ImgDesc*, int nimg, int max_tiles, long long max_n,
 void launch_reconstruct(const ImgDesc*, int nimg, int max_tiles, cudaStream_t);
 void launch_decode_coders(const ImgDesc*, int nimg, bool planes, int max_w, cudaStream_t);
 void launch_decode_output(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
+void launch_hdr_sizes(const uint8_t* rgbe, int w, int h, long long* sizes, cudaStream_t);
+void launch_hdr_write(const uint8_t* rgbe, int w, int h, const long long* offs, uint8_t* out, cudaStream_t);
+void launch_hdr_expand(const uint8_t* data, const long long* starts, const uint8_t* newrle, int w, int h, uint8_t* rgbe,
+                       cudaStream_t);
 void launch_prefilter(const ImgDesc*, int nimg, int max_w, int max_h, int max_radius, cudaStream_t);
 void launch_fit(const ImgDesc*, int nimg, int max_sort_tiles, long long max_nodes, int max_chunks, cudaStream_t);
 void launch_fit_sort(const ImgDesc*, int nimg, int max_sort_tiles, cudaStream_t);

@@ -110,6 +110,8 @@ struct Ctx {
   Band* band = nullptr;  // row-band session (band.cu)
   void* plane_scratch = nullptr;  // plane coder symbol slabs (entropy.cu)
   size_t plane_scratch_cap = 0;
+  void* hdr_buf = nullptr;  // .hdr scanline coding (hdrio.cu)
+  size_t hdr_cap = 0;
 };
 
 inline int cuda_fail(cudaError_t e, const char* what) {
