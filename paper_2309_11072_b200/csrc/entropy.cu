@@ -397,7 +397,10 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
           m.s = pm[c].s;
           m.t = pm[c].t;
         }
-        acc[c] = amap_then_slow(warp_compose_down(m), acc[c]);
+        // a context no tile of the window touched composes to the identity (the
+        // DCT chain's Y tiles never touch Cb/Cr's contexts and vice versa)
+        if (__any_sync(0xffffffffu, m.c != 0 || m.s != 0))
+          acc[c] = amap_then_slow(warp_compose_down(m), acc[c]);
         if (k < 32) ain[c] = (int)amap_apply(acc[c], __shfl_sync(0xffffffffu, st ? ps[c] : 0, k));
       }
       if (k < 32) break;
