@@ -20,6 +20,42 @@ using namespace hdll;
 using namespace hdll_host;
 
 namespace {
+
+// The per-batch staging block (descriptors, parameters, chain tables) lives in
+// pinned host memory; this kernel pulls it over PCIe itself instead of a
+// cudaMemcpyAsync, which would queue on the copy engine behind any large
+// host->device transfer in flight (the next chunk's RGBE in HostPipeline) and
+// stall the whole batch.  It also zeroes every image's small reset block.
+constexpr int kMaxZero = 256;
+__global__ void __launch_bounds__(256) k_stage(uint8_t* dst, const uint8_t* src, size_t bytes,
+                                               uint8_t* const* zp, int nz) {
+  __shared__ uint8_t* zs[kMaxZero];
+  for (int i = threadIdx.x; i < nz; i += blockDim.x) zs[i] = zp[i];
+  __syncthreads();
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x, stride = (long long)gridDim.x * blockDim.x;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  for (long long i = tid; i < (long long)(bytes / 16); i += stride) d4[i] = s4[i];
+  constexpr int zq = (int)(kZeroBytes / 16);
+  for (long long j = tid; j < (long long)nz * zq; j += stride)
+    reinterpret_cast<uint4*>(zs[j / zq])[j % zq] = make_uint4(0, 0, 0, 0);
+}
+static_assert(kZeroBytes % 16 == 0, "reset blocks are zeroed in 16-byte words");
+
+// stage `bytes` of H (pinned) into D and zero the reset blocks at zp[0..nz)
+int stage_upload(uint8_t* D, const uint8_t* H, size_t bytes, uint8_t* const* zp, int nz, cudaStream_t st) {
+  for (int z0 = 0; z0 < nz || z0 == 0; z0 += kMaxZero) {
+    const int cnt = std::min(kMaxZero, nz - z0);
+    const size_t b = z0 == 0 ? bytes : 0;
+    long long blocks = (long long)(b / 16 + cnt * (kZeroBytes / 16) + 255) / 256;
+    if (blocks > 148 * 4) blocks = 148 * 4;
+    if (blocks < 1) blocks = 1;
+    k_stage<<<(unsigned)blocks, 256, 0, st>>>(D, H, b, zp + z0, cnt < 0 ? 0 : cnt);
+    if (nz == 0) break;
+  }
+  return cuda_fail(cudaGetLastError(), "stage");
+}
+
 // mode: 0 full encode, 1 lossless plane (rgbe -> plane bytes), 2 lossy image (rgbe -> sdr rgb)
 int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out, const uint64_t* out_cap,
               uint64_t* d_out_len, cudaStream_t st, int mode) {
@@ -65,7 +101,8 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   hc_dct.schedule();
   hc_pln.schedule();
   const long long ntiles = hc_dct.ntiles() + hc_pln.ntiles();
-  size_t tab_bytes = align_up(sizeof(ImgDesc) * n) + hc_dct.staged_bytes() + hc_pln.staged_bytes() + 16 * kAlign;
+  size_t tab_bytes = align_up(sizeof(ImgDesc) * n) + hc_dct.staged_bytes() + hc_pln.staged_bytes() + 16 * kAlign +
+                     align_up(8 * (size_t)n);
   // the batch that last used this staging slot may still read it
   const int slot = c->slot;
   c->slot ^= 1;
@@ -88,6 +125,8 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   const size_t t_descs = stage(nullptr, sizeof(ImgDesc) * n);
   const HostChains::Staged sc_dct = hc_dct.stage(stage), sc_pln = hc_pln.stage(stage);
   const size_t t_ticket = stage(nullptr, 16);
+  const size_t t_zero = stage(nullptr, 8 * (size_t)n);  // read by k_stage from the pinned block itself
+  uint8_t** zero_ptrs = reinterpret_cast<uint8_t**>(H + t_zero);
 
   long long max_n = 0, max_sort_tiles = 0, max_nodes = 0, max_out = 0;
   int max_w = 0, max_h = 0, max_radius = 0, max_level = 0, max_base_tiles = 0, max_chunks = 1;
@@ -119,8 +158,8 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   }
   memcpy(H + t_descs, ds.data(), sizeof(ImgDesc) * n);
   memset(H + t_ticket, 0, 16);
-  CK(cudaMemcpyAsync(D, H, so, cudaMemcpyHostToDevice, st));
-  for (int i = 0; i < n; i++) CK(cudaMemsetAsync(A + base[i] + lays[i].off_zero, 0, kZeroBytes, st));
+  for (int i = 0; i < n; i++) zero_ptrs[i] = A + base[i] + lays[i].off_zero;
+  if (int rc = stage_upload(D, H, so, zero_ptrs, n, st)) return rc;
   c->d_descs = (ImgDesc*)(D + t_descs);
   const ImgDesc* dd = c->d_descs;
 
