@@ -458,7 +458,7 @@ def main():
     ap.add_argument("--quality", type=int, default=85)
     ap.add_argument("--sigma", type=float, default=1.0)
     ap.add_argument("--cpu-sample", type=int, default=4)
-    ap.add_argument("--chunk", type=int, default=32)
+    ap.add_argument("--chunk", type=int, default=64)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--tiled", action="store_true", help="config 3: tile-sharded path even on one rank")
     args = ap.parse_args()
