@@ -95,7 +95,7 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
     for (int k = 0; k < 5; k++) {
       bool active = (mode == 0) || (mode == 1 && k == 1) || (mode == 2 && k == 0);
       (k == 0 ? hc_dct : hc_pln).add(i, k, -1, 0, active ? (k == 0 ? nb : h) : 0, A + base[i] + lays[i].off_chain[k],
-                                     lays[i].chain_cap[k]);
+                                     lays[i].chain_cap[k], (int)w);
     }
   }
   hc_dct.schedule();

@@ -127,7 +127,14 @@ inline __host__ __device__ int pairwise_level(long long n) {
 constexpr int kMaxCtx = 6;
 constexpr int kDctBlocksPerLane = 1;                      // entropy tile: 32 lanes x 1 block
 constexpr int kDctTileBlocks = 32 * kDctBlocksPerLane;
-constexpr int kPlaneTileRows = 32;                        // entropy tile: one row per lane
+constexpr int kPlaneTileRows = 32;                        // entropy tile: one row (segment) per lane
+
+// plane rows per entropy tile: 32 / segments per row (entropy.cu plane_segs)
+inline int plane_tile_rows(int w) {
+  int s = 1;
+  while (s < 32 && (long long)s * 2048 < w) s <<= 1;
+  return kPlaneTileRows / s;
+}
 
 // Sequential-coder chains for the entropy kernel (entropy.cu).
 struct ChainTab {

@@ -565,11 +565,19 @@ __device__ __forceinline__ LaneState carve_state(uint8_t* p, int nl) {
 // the chain and each row starts in the reset automaton state.  The symbols are
 // regenerated from the plane (L1-cached loads) by every pass instead of staged.
 // ---------------------------------------------------------------------------
+// A lane codes one segment [x0, x1) of a row.  Wide rows are cut into S
+// segments (plane_segs) so single large images still fill the GPU; a segment
+// other than the first enters in the automaton state the previous segments
+// leave: either free, or inside a run of L samples so far (the run's chunks
+// go out where it ends, _kernels.py:183-198, so no symbol moves between lanes).
 struct PlaneRowGen {
   static constexpr bool kStoresK = false;
   const uint8_t* cur;   // the lane's row; nullptr: idle lane
   const uint8_t* prev;  // the row above; nullptr on row 0
-  int W;
+  int x0, x1;           // the segment
+  bool last;            // x1 == width: a run open at x1 ends with the row
+  bool inrun0;          // entry state
+  int L0;               // samples of the entering run so far
   // f(index, ctx, value, 0, 0) in coder order.  _neighbors (_kernels.py:131-143):
   // a = left (above at x = 0, 128 at the origin), b = above (else a),
   // c = above-left (else b).
@@ -577,10 +585,10 @@ struct PlaneRowGen {
   __device__ __forceinline__ void for_each(F&& f) const {
     if (!cur) return;
     int i = 0;
-    int a = prev ? __ldg(prev) : 128;
-    int c = a;  // above-left of x = 0 is the above sample
-    bool inrun = false;
-    int L = 0;
+    int a = x0 > 0 ? cur[x0 - 1] : (prev ? __ldg(prev) : 128);
+    int c = x0 > 0 ? (prev ? prev[x0 - 1] : a) : a;  // above-left (the above sample at x = 0)
+    bool inrun = inrun0;
+    int L = L0;
     auto run_chunks = [&]() {  // chunks of <= 255; a chunk of 255 continues
       for (;;) {
         const int ch = L >= 255 ? 255 : L;
@@ -620,11 +628,11 @@ struct PlaneRowGen {
       a = xv;
     };
     // 16 samples per 128-bit load when the rows are aligned: one L1 wavefront
-    // per lane per 16 samples instead of one per sample
+    // per lane per 16 samples instead of one per sample (x0 is a multiple of 16)
     const uint8_t* pv = prev ? prev : cur;
-    int x = 0;
-    if (((reinterpret_cast<uintptr_t>(cur) | reinterpret_cast<uintptr_t>(pv)) & 15) == 0) {
-      for (; x + 16 <= W; x += 16) {
+    int x = x0;
+    if (((reinterpret_cast<uintptr_t>(cur + x0) | reinterpret_cast<uintptr_t>(pv + x0)) & 15) == 0) {
+      for (; x + 16 <= x1; x += 16) {
         const uint4 c4 = __ldg(reinterpret_cast<const uint4*>(cur + x));
         const uint4 p4 = __ldg(reinterpret_cast<const uint4*>(pv + x));
 #pragma unroll 1
@@ -640,10 +648,121 @@ struct PlaneRowGen {
         }
       }
     }
-    for (; x < W; x++) sample(__ldg(cur + x), __ldg(pv + x));
-    if (inrun) run_chunks();  // a run reaching the row end
+    for (; x < x1; x++) sample(__ldg(cur + x), __ldg(pv + x));
+    if (inrun && last) run_chunks();  // a run reaching the row end
   }
 };
+
+// The automaton's effect across one segment, as a function of the entry state:
+// entering free -> (f_in, f_L) whatever the count; entering inside a run of L
+// -> (true, L + cov) when the run covers the whole segment (full), otherwise
+// the run ends inside and the exit is (r_in, r_L).  These compose, so a warp
+// scan gives every segment its entry state.
+struct SegFn {
+  bool f_in, full, r_in;
+  int f_L, cov, r_L;
+};
+
+__device__ __forceinline__ SegFn segfn_identity() { return SegFn{false, true, false, 0, 0, 0}; }
+
+__device__ __forceinline__ void segfn_apply(const SegFn& f, bool& in, int& L) {
+  if (!in) {
+    in = f.f_in;
+    L = f.f_L;
+  } else if (f.full) {
+    L += f.cov;
+  } else {
+    in = f.r_in;
+    L = f.r_L;
+  }
+}
+
+__device__ __forceinline__ SegFn segfn_then(const SegFn& f, const SegFn& g) {  // f, then g
+  SegFn h;
+  h.f_in = f.f_in;
+  h.f_L = f.f_L;
+  segfn_apply(g, h.f_in, h.f_L);
+  if (f.full) {
+    h.full = g.full;
+    h.cov = f.cov + g.cov;
+    h.r_in = g.r_in;
+    h.r_L = g.r_L;
+  } else {
+    h.full = false;
+    h.cov = 0;
+    h.r_in = f.r_in;
+    h.r_L = f.r_L;
+    segfn_apply(g, h.r_in, h.r_L);
+  }
+  return h;
+}
+
+// one sweep of the segment for both entry states
+__device__ SegFn segment_fn(const uint8_t* cur, const uint8_t* prev, int x0, int x1) {
+  int a = x0 > 0 ? cur[x0 - 1] : (prev ? __ldg(prev) : 128);
+  int c = x0 > 0 ? (prev ? prev[x0 - 1] : a) : a;
+  bool fin = false, rin = true, carried = true;
+  int fL = 0, rL = 0, cov = 0;
+  for (int x = x0; x < x1; x++) {
+    const int xv = __ldg(cur + x);
+    const int b = prev ? __ldg(prev + x) : a;
+    const int cc = prev ? c : a;
+    const bool E = xv == a, F = a == b && b == cc;
+    // entered free
+    if (!fin && F) fin = true, fL = 0;
+    if (fin) {
+      if (E) fL++;
+      else fin = false;
+    }
+    // entered inside a run
+    if (carried) {
+      if (E) cov++;
+      else carried = false, rin = false;
+    } else {
+      if (!rin && F) rin = true, rL = 0;
+      if (rin) {
+        if (E) rL++;
+        else rin = false;
+      }
+    }
+    c = b;
+    a = xv;
+  }
+  SegFn f;
+  f.f_in = fin;
+  f.f_L = fL;
+  f.full = carried;
+  f.cov = cov;
+  f.r_in = carried ? true : rin;
+  f.r_L = carried ? 0 : rL;
+  return f;
+}
+
+__device__ __forceinline__ SegFn shfl_up_segfn(const SegFn& f, int d) {
+  const unsigned bits = (unsigned)f.f_in | ((unsigned)f.full << 1) | ((unsigned)f.r_in << 2);
+  const unsigned ob = __shfl_up_sync(0xffffffffu, bits, d);
+  SegFn g;
+  g.f_in = ob & 1;
+  g.full = (ob >> 1) & 1;
+  g.r_in = (ob >> 2) & 1;
+  g.f_L = __shfl_up_sync(0xffffffffu, f.f_L, d);
+  g.cov = __shfl_up_sync(0xffffffffu, f.cov, d);
+  g.r_L = __shfl_up_sync(0xffffffffu, f.r_L, d);
+  return g;
+}
+
+// segments per row for a plane of width w: a power of two dividing 32, about
+// 2048 samples each
+__host__ __device__ __forceinline__ int plane_segs(int w) {
+  int s = 1;
+  while (s < 32 && (long long)s * 2048 < w) s <<= 1;
+  return s;
+}
+
+__host__ __device__ __forceinline__ int plane_seg_width(int w) {  // multiple of 16
+  const int s = plane_segs(w);
+  return ((w + s - 1) / s + 15) / 16 * 16;
+}
 
 // The count pass keeps each row's symbols (u16: k << 11 | ctx << 8 | value)
 // in a global scratch slab of the warp, interleaved by lane in 16-byte chunks
@@ -738,13 +857,31 @@ __global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict
   while (next_tile(ct, &chain, &tin, &g)) {
     const ImgDesc& d = descs[ct.img[chain]];
     const int kind = ct.kind[chain];
-    const long long r = tin * kPlaneTileRows + lane;  // row of the chain
+    const int S = plane_segs(d.w), wseg = plane_seg_width(d.w);
+    const long long r = tin * (kPlaneTileRows / S) + lane / S;  // row of the chain
+    const int sg = lane & (S - 1);
+    const int x0 = min(d.w, sg * wseg), x1 = min(d.w, x0 + wseg);
+    const bool live = r < ct.units[chain];
+    const uint8_t* src = kind == 1 ? d.e_plane : d.res_planes + (long long)(kind - 2) * d.n;
+    const long long y = ct.first[chain] + (live ? r : 0);  // row in the image arrays
+    const uint8_t* cur = src + y * d.w;
+    const uint8_t* prev = y > 0 ? cur - d.w : nullptr;
+    // entry state of the segment: segmented scan of the segments' functions
+    bool in0 = false;
+    int L0 = 0;
+    if (S > 1) {
+      SegFn f = live ? segment_fn(cur, prev, x0, x1) : segfn_identity();
+      for (int dd = 1; dd < S; dd <<= 1) {
+        const SegFn o = shfl_up_segfn(f, dd);
+        if (sg >= dd) f = segfn_then(o, f);
+      }
+      const SegFn ex = shfl_up_segfn(f, 1);
+      if (sg > 0) segfn_apply(ex, in0, L0);
+    }
     int cnt[5] = {0, 0, 0, 0, 0};
     int n = 0;
-    if (r < ct.units[chain]) {
-      const long long y = ct.first[chain] + r;  // row in the image arrays
-      const uint8_t* src = kind == 1 ? d.e_plane : d.res_planes + (long long)(kind - 2) * d.n;
-      PlaneRowGen gen{src + y * d.w, y > 0 ? src + (y - 1) * d.w : nullptr, d.w};
+    if (live) {
+      PlaneRowGen gen{cur, prev, x0, x1, x1 == d.w, in0, L0};
       // counts per context (two 32-bit fields per word for the regular contexts)
       unsigned long long p01 = 0, p23 = 0;
       int c4 = 0;
@@ -917,7 +1054,12 @@ static long long plane_grid(const ChainTab& ct) {
   return blocks < need ? blocks : need;
 }
 
-static int plane_cap_chunks(int max_w) { return (2 * max_w + 8) / 8 + 1; }  // <= 2 symbols per sample
+// a segment: <= 2 symbols per sample, plus the 255-chunks of a run that may
+// have begun anywhere earlier in the row (segments are <= 2080 samples)
+static int plane_cap_chunks(int max_w) {
+  const int ws = max_w < 2080 ? max_w : 2080;
+  return (2 * ws + max_w / 255 + 16) / 8 + 1;
+}
 
 size_t plane_scratch_bytes(const ChainTab& ct, int max_w) {
   if (ct.ntiles <= 0) return 0;

@@ -211,8 +211,9 @@ struct HostChains {
   std::vector<long long> seg_r0, seg_t0;
   std::vector<int> seg_active;
 
-  // chain of image i, kind k over `units` blocks / rows from `first`, DCT component cp (-1: all three)
-  void add(int i, int k, int cp, long long fst, long long nunits, uint8_t* o, long long c) {
+  // chain of image i, kind k over `units` blocks / rows from `first`, DCT component cp (-1: all three);
+  // plane tiles hold plane_tile_rows(width) rows
+  void add(int i, int k, int cp, long long fst, long long nunits, uint8_t* o, long long c, int width) {
     img.push_back(i);
     kind.push_back(k);
     comp.push_back(cp);
@@ -224,7 +225,7 @@ struct HostChains {
       in_cnt.push_back(0);
       in_a.push_back(4);  // AdaptiveRiceState: A = 4 (_kernels.py:114-128)
     }
-    const long long per = k == 0 ? kDctTileBlocks : kPlaneTileRows;
+    const long long per = k == 0 ? kDctTileBlocks : plane_tile_rows(width);
     const long long tiles = (k == 0 && cp < 0 ? 3 : 1) * ((nunits + per - 1) / per);
     tile_base.push_back(tile_base.back() + tiles);
   }
@@ -255,7 +256,7 @@ struct HostChains {
       seg_active.push_back(1);
     }
     if (rr_chain.empty()) rr_chain.push_back(0);
-    if (img.empty()) add(0, 1, -1, 0, 0, nullptr, 0);  // keep device arrays non-empty
+    if (img.empty()) add(0, 1, -1, 0, 0, nullptr, 0, 1);  // keep device arrays non-empty
   }
   size_t staged_bytes() const {
     size_t nc = img.size() + 2;

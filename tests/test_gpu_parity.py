@@ -201,3 +201,34 @@ def test_errors(gpu):
         gpu.encode(_image(gpu, px), quality=101)
     with pytest.raises(gpu.UnknownCoderError):
         gpu.encode(_image(gpu, px), lossless_coder=99)
+
+
+# ---------------------------------------------------------------------------
+# wide rows: the plane coder cuts rows wider than 2048 samples into segments
+# whose automaton entry state comes from a scan (runs carried across them)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("w,h,kind", [(4100, 24, "scene"), (9000, 12, "flat"), (6000, 10, "stripes"),
+                                      (2049, 16, "scene"), (65536 + 8, 2, "flat")])
+def test_wide_rows_match_oracle(w, h, kind, gpu):
+    from paper_2309_11072_b200 import synth
+    rng = np.random.default_rng(w + h)
+    if kind == "scene":
+        px = np.tile(synth.make_config(0, 1), (1, -(-w // 768), 1))[:h, :w].copy()
+    elif kind == "flat":  # long constant runs crossing every segment boundary, a few breaks
+        px = np.zeros((h, w, 4), np.uint8)
+        px[...] = (140, 130, 120, 128)
+        for y in range(h):
+            for x in rng.integers(0, w, 5):
+                px[y, x] = rng.integers(0, 256, 4)
+    else:  # runs of random lengths around the 255-chunk and segment sizes
+        px = np.zeros((h, w, 4), np.uint8)
+        for y in range(h):
+            x = 0
+            while x < w:
+                ln = int(rng.choice([1, 3, 254, 255, 256, 510, 2047, 2048, 2049, 3000]))
+                px[y, x:x + ln] = rng.integers(0, 256, 4)
+                x += ln
+    img = _image(gpu, px, [("FORMAT", "32-bit_rle_rgbe")])
+    got = gpu.serialize(gpu.encode(img))
+    want = O.encode(px, header_vars=[("FORMAT", "32-bit_rle_rgbe")])
+    assert got == want
