@@ -89,6 +89,15 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   // sequential-coder chains: the DCT stream of every image (kind 0) and its 4
   // plane streams (kinds 1..4), each family driven by its own kernel
   HostChains hc_dct, hc_pln;
+  {
+    long long rows = 0;
+    int mw = 1;
+    for (int i = 0; i < n; i++) {
+      rows += (mode == 0 ? 4 : (mode == 1 ? 1 : 0)) * (long long)imgs[i].height;
+      mw = std::max(mw, (int)imgs[i].width);
+    }
+    hc_pln.segw = plane_segw_for(rows, mw);
+  }
   for (int i = 0; i < n; i++) {
     const long long w = imgs[i].width, h = imgs[i].height;
     const long long nb = ((w + 7) / 8) * ((h + 7) / 8);

@@ -129,11 +129,24 @@ constexpr int kDctBlocksPerLane = 1;                      // entropy tile: 32 la
 constexpr int kDctTileBlocks = 32 * kDctBlocksPerLane;
 constexpr int kPlaneTileRows = 32;                        // entropy tile: one row (segment) per lane
 
-// plane rows per entropy tile: 32 / segments per row (entropy.cu plane_segs)
-inline int plane_tile_rows(int w) {
+// Plane entropy tiles: a row of width w is cut into the power-of-two number of
+// segments (<= 32) that brings them to at most segw samples; a tile holds
+// 32 / segments rows.
+__host__ __device__ inline int plane_row_segments(int w, int segw) {
   int s = 1;
-  while (s < 32 && (long long)s * 2048 < w) s <<= 1;
-  return kPlaneTileRows / s;
+  while (s < 32 && (long long)s * segw < w) s <<= 1;
+  return s;
+}
+inline int plane_tile_rows(int w, int segw) { return kPlaneTileRows / plane_row_segments(w, segw); }
+
+// target segment width for a launch coding `rows` plane rows in all: about
+// two waves of tiles over the GPU's warps, segments of >= 256 samples
+inline int plane_segw_for(long long rows, int max_w) {
+  const long long want_tiles = 2LL * 148 * 28;
+  long long s = 1;
+  while (s < 32 && rows * s / kPlaneTileRows < want_tiles) s <<= 1;
+  int segw = (int)((max_w + s - 1) / s);
+  return segw < 256 ? 256 : segw;
 }
 
 // Sequential-coder chains for the entropy kernel (entropy.cu).
@@ -157,6 +170,7 @@ struct ChainTab {
   long long* out_cnt;          // [nchains][kMaxCtx] counts after the chain (mode 1)
   AMap* out_map;               // [nchains][kMaxCtx] the chain's composed A-map (mode 2)
   int mode;                    // 0 full encode, 1 counts, 2 counts + A-maps
+  int plane_segw;              // plane rows are cut into segments of <= plane_segw samples
   // per global tile status (epoch-tagged)
   int* flags;                  // [ntiles][4]: cnt, map, bit, done
   long long* cnt;              // [ntiles][2][kMaxCtx]: aggregate, inclusive

@@ -751,16 +751,13 @@ __device__ __forceinline__ SegFn shfl_up_segfn(const SegFn& f, int d) {
   return g;
 }
 
-// segments per row for a plane of width w: a power of two dividing 32, about
-// 2048 samples each
-__host__ __device__ __forceinline__ int plane_segs(int w) {
-  int s = 1;
-  while (s < 32 && (long long)s * 2048 < w) s <<= 1;
-  return s;
-}
+// segments per row of a plane of width w: the power of two (dividing 32) that
+// brings segments to at most segw samples (ChainTab::plane_segw, chosen per
+// launch so that the tiles fill the GPU)
+__host__ __device__ __forceinline__ int plane_segs(int w, int segw) { return plane_row_segments(w, segw); }
 
-__host__ __device__ __forceinline__ int plane_seg_width(int w) {  // multiple of 16
-  const int s = plane_segs(w);
+__host__ __device__ __forceinline__ int plane_seg_width(int w, int segw) {  // multiple of 16
+  const int s = plane_segs(w, segw);
   return ((w + s - 1) / s + 15) / 16 * 16;
 }
 
@@ -857,7 +854,7 @@ __global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict
   while (next_tile(ct, &chain, &tin, &g)) {
     const ImgDesc& d = descs[ct.img[chain]];
     const int kind = ct.kind[chain];
-    const int S = plane_segs(d.w), wseg = plane_seg_width(d.w);
+    const int S = plane_segs(d.w, ct.plane_segw), wseg = plane_seg_width(d.w, ct.plane_segw);
     const long long r = tin * (kPlaneTileRows / S) + lane / S;  // row of the chain
     const int sg = lane & (S - 1);
     const int x0 = min(d.w, sg * wseg), x1 = min(d.w, x0 + wseg);
@@ -1055,20 +1052,22 @@ static long long plane_grid(const ChainTab& ct) {
 }
 
 // a segment: <= 2 symbols per sample, plus the 255-chunks of a run that may
-// have begun anywhere earlier in the row (segments are <= 2080 samples)
-static int plane_cap_chunks(int max_w) {
-  const int ws = max_w < 2080 ? max_w : 2080;
+// have begun anywhere earlier in the row
+static int plane_cap_chunks(int max_w, int segw) {
+  int ws = segw + 16;
+  if (ws > max_w) ws = max_w;
   return (2 * ws + max_w / 255 + 16) / 8 + 1;
 }
 
 size_t plane_scratch_bytes(const ChainTab& ct, int max_w) {
   if (ct.ntiles <= 0) return 0;
-  return (size_t)plane_grid(ct) * 4 * 32 * plane_cap_chunks(max_w) * sizeof(uint4);
+  return (size_t)plane_grid(ct) * 4 * 32 * plane_cap_chunks(max_w, ct.plane_segw) * sizeof(uint4);
 }
 
 void launch_entropy_plane(const ImgDesc* d_descs, const ChainTab& ct, int max_w, void* scratch, cudaStream_t st) {
   if (ct.ntiles <= 0) return;
-  k_entropy_plane<<<(unsigned)plane_grid(ct), 128, 0, st>>>(d_descs, ct, (uint4*)scratch, plane_cap_chunks(max_w));
+  k_entropy_plane<<<(unsigned)plane_grid(ct), 128, 0, st>>>(d_descs, ct, (uint4*)scratch,
+                                                             plane_cap_chunks(max_w, ct.plane_segw));
 }
 
 void launch_entropy_fixup(const ChainTab& ct, cudaStream_t st) {
