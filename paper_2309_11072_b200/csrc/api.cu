@@ -257,6 +257,7 @@ int run_decode(Ctx* c, const hdll_b200_decode_image* imgs, int n, uint8_t* const
                cudaStream_t st) {
   if (n <= 0) return HDLL_B200_E_ARG;
   CK(cudaSetDevice(c->device));
+  if (c->done_ev) CK(cudaEventSynchronize(c->done_ev));  // an encode batch may still use the arena
   c->launches = 0;
   // each image as the encoder's descriptor (same arena layout), plus its coder bodies
   std::vector<hdll_b200_image> ims(n);
