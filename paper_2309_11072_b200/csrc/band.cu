@@ -163,6 +163,7 @@ int hdll_b200_band_begin(hdll_b200_ctx* ctx, const hdll_b200_image* img, const h
   }
   if (px0 < (long long)bd.crow0 * W || px1 > (long long)bd.crow1 * W) return HDLL_B200_E_ARG;
   CK(cudaSetDevice(c->device));
+  if (c->done_ev) CK(cudaEventSynchronize(c->done_ev));  // the shared coder scratch of an encode batch
   c->launches = 0;
   if (!c->band) c->band = new Band();
   Band* b = c->band;
