@@ -20,7 +20,25 @@
 
 namespace hdll {
 
-__constant__ double c_dct[64];  // DCT_MATRIX, _kernels.py:23-43 (row u, column t)
+// DCT_MATRIX, _kernels.py:23-43 (row u, column t), compile-time constants so the
+// fully unrolled transforms take them as instruction operands
+__device__ constexpr double kDctM[64] = {
+      0.35355339059327373, 0.35355339059327373, 0.35355339059327373, 0.35355339059327373,
+      0.35355339059327373, 0.35355339059327373, 0.35355339059327373, 0.35355339059327373,
+      0.4903926402016152,  0.4157348061512726,  0.27778511650980114, 0.09754516100806417,
+      -0.0975451610080641, -0.277785116509801,  -0.4157348061512727, -0.4903926402016152,
+      0.46193976625564337, 0.19134171618254492, -0.19134171618254486, -0.46193976625564337,
+      -0.4619397662556434, -0.19134171618254517, 0.191341716182545,   0.46193976625564326,
+      0.4157348061512726,  -0.0975451610080641, -0.4903926402016152, -0.2777851165098011,
+      0.2777851165098009,  0.4903926402016152,  0.09754516100806439, -0.41573480615127256,
+      0.3535533905932738,  -0.35355339059327373, -0.35355339059327384, 0.3535533905932737,
+      0.35355339059327384, -0.35355339059327334, -0.35355339059327356, 0.3535533905932733,
+      0.27778511650980114, -0.4903926402016152, 0.09754516100806415, 0.41573480615127273,
+      -0.41573480615127256, -0.09754516100806401, 0.4903926402016153, -0.27778511650980076,
+      0.19134171618254492, -0.4619397662556434, 0.46193976625564326, -0.19134171618254495,
+      -0.19134171618254528, 0.46193976625564337, -0.4619397662556432, 0.19134171618254478,
+      0.09754516100806417, -0.2777851165098011, 0.41573480615127273, -0.4903926402016153,
+      0.4903926402016152,  -0.4157348061512725, 0.27778511650980076, -0.09754516100806429};
 __constant__ int c_zigzag[64];  // ZIGZAG, codec_core.py:364-372
 
 constexpr int kTileBlocks = 16;
@@ -222,7 +240,7 @@ __global__ void __launch_bounds__(128, 4) k_base_layer(const ImgDesc* __restrict
       for (int u = 0; u < 8; u++) {
         double s = 0.0;
 #pragma unroll
-        for (int tt = 0; tt < 8; tt++) s += c_dct[u * 8 + tt] * in[tt];
+        for (int tt = 0; tt < 8; tt++) s += kDctM[u * 8 + tt] * in[tt];
         bufB[(ci * 8 + u) * kRowStride + col0 + l] = s;
       }
     }
@@ -242,7 +260,7 @@ __global__ void __launch_bounds__(128, 4) k_base_layer(const ImgDesc* __restrict
       for (int v = 0; v < 8; v++) {
         double s = 0.0;
 #pragma unroll
-        for (int tt = 0; tt < 8; tt++) s += in[tt] * c_dct[v * 8 + tt];
+        for (int tt = 0; tt < 8; tt++) s += in[tt] * kDctM[v * 8 + tt];
         const double qv = qt[l * 8 + v];
         const double qz = rha(s / qv);  // B200 fp64 division is cheaper than a certified reciprocal
         zz[c_zigzag[l * 8 + v]] = (int16_t)qz;
@@ -265,7 +283,7 @@ __global__ void __launch_bounds__(128, 4) k_base_layer(const ImgDesc* __restrict
       for (int x = 0; x < 8; x++) {
         double s = 0.0;
 #pragma unroll
-        for (int tt = 0; tt < 8; tt++) s += c_dct[tt * 8 + x] * in[tt];
+        for (int tt = 0; tt < 8; tt++) s += kDctM[tt * 8 + x] * in[tt];
         bufB[(ci * 8 + x) * kRowStride + col0 + l] = s;
       }
     }
@@ -283,7 +301,7 @@ __global__ void __launch_bounds__(128, 4) k_base_layer(const ImgDesc* __restrict
       for (int y = 0; y < 8; y++) {
         double s = 0.0;
 #pragma unroll
-        for (int tt = 0; tt < 8; tt++) s += in[tt] * c_dct[tt * 8 + y];
+        for (int tt = 0; tt < 8; tt++) s += in[tt] * kDctM[tt * 8 + y];
         bufA[(ci * 8 + l) * kRowStride + col0 + y] = s;
       }
     }
@@ -309,23 +327,6 @@ __global__ void __launch_bounds__(128, 4) k_base_layer(const ImgDesc* __restrict
 }
 
 void upload_base_constants() {
-  static const double dct[64] = {
-      0.35355339059327373, 0.35355339059327373, 0.35355339059327373, 0.35355339059327373,
-      0.35355339059327373, 0.35355339059327373, 0.35355339059327373, 0.35355339059327373,
-      0.4903926402016152,  0.4157348061512726,  0.27778511650980114, 0.09754516100806417,
-      -0.0975451610080641, -0.277785116509801,  -0.4157348061512727, -0.4903926402016152,
-      0.46193976625564337, 0.19134171618254492, -0.19134171618254486, -0.46193976625564337,
-      -0.4619397662556434, -0.19134171618254517, 0.191341716182545,   0.46193976625564326,
-      0.4157348061512726,  -0.0975451610080641, -0.4903926402016152, -0.2777851165098011,
-      0.2777851165098009,  0.4903926402016152,  0.09754516100806439, -0.41573480615127256,
-      0.3535533905932738,  -0.35355339059327373, -0.35355339059327384, 0.3535533905932737,
-      0.35355339059327384, -0.35355339059327334, -0.35355339059327356, 0.3535533905932733,
-      0.27778511650980114, -0.4903926402016152, 0.09754516100806415, 0.41573480615127273,
-      -0.41573480615127256, -0.09754516100806401, 0.4903926402016153, -0.27778511650980076,
-      0.19134171618254492, -0.4619397662556434, 0.46193976625564326, -0.19134171618254495,
-      -0.19134171618254528, 0.46193976625564337, -0.4619397662556432, 0.19134171618254478,
-      0.09754516100806417, -0.2777851165098011, 0.41573480615127273, -0.4903926402016153,
-      0.4903926402016152,  -0.4157348061512725, 0.27778511650980076, -0.09754516100806429};
   static const int zig[64] = {0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25, 18, 11, 4,  5,
                               12, 19, 26, 33, 40, 48, 41, 34, 27, 20, 13, 6,  7,  14, 21, 28,
                               35, 42, 49, 56, 57, 50, 43, 36, 29, 22, 15, 23, 30, 37, 44, 51,
@@ -334,7 +335,6 @@ void upload_base_constants() {
   // position j to zz slot inv[j] where ZIGZAG[inv[j]] == j.
   int inv[64];
   for (int k = 0; k < 64; k++) inv[zig[k]] = k;
-  cudaMemcpyToSymbol(c_dct, dct, sizeof(dct));
   cudaMemcpyToSymbol(c_zigzag, inv, sizeof(inv));
 }
 
