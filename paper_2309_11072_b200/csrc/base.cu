@@ -189,8 +189,11 @@ __global__ void __launch_bounds__(128, 4) k_base_layer(const ImgDesc* __restrict
   const int nblk = min(kTileBlocks, d.nbx - bx0);
 
   extern __shared__ double smem[];
-  double* bufA = smem;                      // [3][8][kRowStride]
-  double* bufB = smem + 3 * 8 * kRowStride;  // [3][8][kRowStride]
+  // [3][8][kRowStride], transformed in place: in every pass a thread reads its
+  // whole line (a column or a row of one block) before writing it back, and
+  // no two threads share a line within a pass
+  double* bufA = smem;
+  double* bufB = smem;
   const int t = threadIdx.x;
 
   // task t: block b = t / 8, line l = t % 8, for each of the 3 components
@@ -344,13 +347,13 @@ void launch_base_layer(const ImgDesc* d_descs, int nimg, int max_tiles, long lon
   if (gx > 148 * 8) gx = 148 * 8;
   if (gx < 1) gx = 1;
   k_sdr_ycc<<<dim3(gx, nimg), 256, 0, st>>>(d_descs);
-  size_t smem = sizeof(double) * 2 * 3 * 8 * kRowStride;
+  size_t smem = sizeof(double) * 3 * 8 * kRowStride;
   cudaFuncSetAttribute(k_base_layer<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  // per device
   k_base_layer<false><<<dim3(max_tiles, nimg), 128, smem, st>>>(d_descs);
 }
 
 void launch_reconstruct(const ImgDesc* d_descs, int nimg, int max_tiles, cudaStream_t st) {
-  size_t smem = sizeof(double) * 2 * 3 * 8 * kRowStride;
+  size_t smem = sizeof(double) * 3 * 8 * kRowStride;
   cudaFuncSetAttribute(k_base_layer<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_base_layer<true><<<dim3(max_tiles, nimg), 128, smem, st>>>(d_descs);
 }
