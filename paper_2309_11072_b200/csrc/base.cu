@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(256) k_sdr_ycc(const ImgDesc* __restrict__ des
 // decode.cu): start from the decoded zigzag coefficients instead, i.e. only
 // _reconstruct (codec_core.py:478-489) -- the encoder's inverse half.
 template <bool kDecode>
-__global__ void __launch_bounds__(128, 4) k_base_layer(const ImgDesc* __restrict__ descs) {
+__global__ void __launch_bounds__(128, 8) k_base_layer(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
   const int tiles_x = (d.nbx + kTileBlocks - 1) / kTileBlocks;
   const int tile = blockIdx.x;
