@@ -161,15 +161,28 @@ __global__ void __launch_bounds__(256) k_prefilter_cols(const ImgDesc* __restric
   for (int j = 0; j <= R; j++) fw[j] = d.taps[R - j];
   const uint8_t* S = d.s_planes + (long long)c * d.n;
   const int gx = reflect_idx((long long)x0 - R + t, d.w);
-  // vertical pass over rows y0 .. y0 + kCR - 1 of column gx
+  // vertical pass over rows y0 .. y0 + kCR - 1 of column gx; away from the top
+  // and bottom edges the rows are consecutive (no reflection arithmetic)
+  const bool inner = y0 >= R && y0 + kCR + R <= d.h;
+  const uint8_t* col = S + gx;
+  const long long W = d.w;
+  const uint8_t* rp = col + (inner ? (long long)(y0 - R) * W : 0);
+  auto row_at = [&](int i) -> double {  // input row y0 - R + i of the column
+    if (inner) {
+      const double v = (double)__ldg(rp);
+      rp += W;
+      return v;
+    }
+    return (double)__ldg(col + (long long)reflect_idx((long long)y0 - R + i, d.h) * W);
+  };
   double win[2 * R + 1];
 #pragma unroll
-  for (int i = 0; i < 2 * R; i++) win[i + 1] = (double)__ldg(S + (long long)reflect_idx((long long)y0 - R + i, d.h) * d.w + gx);
+  for (int i = 0; i < 2 * R; i++) win[i + 1] = row_at(i);
 #pragma unroll
   for (int oy = 0; oy < kCR; oy++) {
 #pragma unroll
     for (int i = 0; i < 2 * R; i++) win[i] = win[i + 1];
-    win[2 * R] = (double)__ldg(S + (long long)reflect_idx((long long)y0 + oy + R, d.h) * d.w + gx);
+    win[2 * R] = row_at(oy + 2 * R);
     double o = win[R] * fw[0];
 #pragma unroll
     for (int j = R; j >= 1; j--) o += (win[R - j] + win[R + j]) * fw[j];
@@ -179,15 +192,15 @@ __global__ void __launch_bounds__(256) k_prefilter_cols(const ImgDesc* __restric
   // horizontal pass
   const int x = x0 + t - R;
   if (t < R || t >= 256 - R || x >= d.w) return;
-  double* out = d.sstar + (long long)c * d.n;
+  double* out = d.sstar + (long long)c * d.n + (long long)y0 * W + x;
+  const int rows = min(kCR, d.h - y0);
 #pragma unroll 4
-  for (int oy = 0; oy < kCR; oy++) {
-    const int y = y0 + oy;
-    if (y >= d.h) break;
+  for (int oy = 0; oy < rows; oy++) {
     double o = vt[oy][t] * fw[0];
 #pragma unroll
     for (int j = R; j >= 1; j--) o += (vt[oy][t - j] + vt[oy][t + j]) * fw[j];
-    out[(long long)y * d.w + x] = o;
+    *out = o;
+    out += W;
   }
 }
 
