@@ -229,6 +229,7 @@ struct LaneBits {
 // raw bits), EOB = run 64 unless position 63 is coded.
 struct DctBlockGen {
   static constexpr bool kStoresK = false;
+  static constexpr bool kStaticCtx = true;  // every f() call names its context
   const int16_t* z;  // nullptr: idle lane
   unsigned long long nzm;
   unsigned dcu;      // interleaved DC difference
@@ -337,23 +338,52 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
     ls.nn[c * 32 + lane] = n0[c];
   }
 #ifndef HDLL_EXP_NO_MAPS
-  gen.for_each([&](int, int c, int v, int, uint32_t) {
-    const int o = c * 32 + lane;
-    const int nb = ls.nn[o];
-    const int h = nb == kStateReset - 1;  // N reaches 64: A and N halve
-    ls.nn[o] = h ? kStateReset / 2 : nb + 1;
-    const int sft = ls.ms[o];
-    if (sft >= 0 && sft + h < kADomainBits) {
-      ls.mc[o] += (long long)v << sft;
-      ls.ms[o] = sft + h;
-    } else {
-      AMap m{ls.mc[o], sft, ls.mt[o]};
-      m = amap_push_slow(m, v, h);
-      ls.mc[o] = m.c;
-      ls.ms[o] = m.s;
-      ls.mt[o] = m.t;
+  if constexpr (Gen::kStaticCtx) {  // every call site names its context: the state stays in registers
+    long long rmc[NL];
+    int rms[NL], rmt[NL], rnn[NL];
+#pragma unroll
+    for (int c = 0; c < NL; c++) rmc[c] = 0, rms[c] = 0, rmt[c] = 0, rnn[c] = n0[c];
+    gen.for_each([&](int, int c, int v, int, uint32_t) {
+      const int nb = rnn[c];
+      const int h = nb == kStateReset - 1;  // N reaches 64: A and N halve
+      rnn[c] = h ? kStateReset / 2 : nb + 1;
+      const int sft = rms[c];
+      if (sft >= 0 && sft + h < kADomainBits) {
+        rmc[c] += (long long)v << sft;
+        rms[c] = sft + h;
+      } else {
+        AMap m{rmc[c], sft, rmt[c]};
+        m = amap_push_slow(m, v, h);
+        rmc[c] = m.c;
+        rms[c] = m.s;
+        rmt[c] = m.t;
+      }
+    });
+#pragma unroll
+    for (int c = 0; c < NL; c++) {
+      ls.mc[c * 32 + lane] = rmc[c];
+      ls.ms[c * 32 + lane] = rms[c];
+      ls.mt[c * 32 + lane] = rmt[c];
     }
-  });
+  } else {
+    gen.for_each([&](int, int c, int v, int, uint32_t) {
+      const int o = c * 32 + lane;
+      const int nb = ls.nn[o];
+      const int h = nb == kStateReset - 1;  // N reaches 64: A and N halve
+      ls.nn[o] = h ? kStateReset / 2 : nb + 1;
+      const int sft = ls.ms[o];
+      if (sft >= 0 && sft + h < kADomainBits) {
+        ls.mc[o] += (long long)v << sft;
+        ls.ms[o] = sft + h;
+      } else {
+        AMap m{ls.mc[o], sft, ls.mt[o]};
+        m = amap_push_slow(m, v, h);
+        ls.mc[o] = m.c;
+        ls.ms[o] = m.s;
+        ls.mt[o] = m.t;
+      }
+    });
+  }
 #endif
   AMap pre[NL], agg[NL];
 #pragma unroll 1
@@ -423,23 +453,40 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
     ls.nn[c * 32 + lane] = n0[c];
   }
   long long nbits = 0;
-  auto len_step = [&](int, int c, int v, int xl, uint32_t) {
-    const int o = c * 32 + lane;
-    int a = ls.a[o], nb = ls.nn[o];
-    const int k = kfast(a, nb);
-    nbits += rice_len(v, k) + xl;
-    a += v;  // _update_state
-    nb += 1;
-    if (nb >= kStateReset) {
-      a >>= 1;
-      nb >>= 1;
-    }
-    ls.a[o] = a;
-    ls.nn[o] = nb;
-    return k;
-  };
-  if constexpr (Gen::kStoresK) gen.for_each_setk(len_step);  // k kept for the emit pass
-  else gen.for_each(len_step);
+  if constexpr (Gen::kStaticCtx) {
+    int ra[NL], rnn[NL];
+#pragma unroll
+    for (int c = 0; c < NL; c++) ra[c] = a_start[c], rnn[c] = n0[c];
+    gen.for_each([&](int, int c, int v, int xl, uint32_t) {
+      const int k = kfast(ra[c], rnn[c]);
+      nbits += rice_len(v, k) + xl;
+      ra[c] += v;  // _update_state
+      rnn[c] += 1;
+      if (rnn[c] >= kStateReset) {
+        ra[c] >>= 1;
+        rnn[c] >>= 1;
+      }
+      return k;
+    });
+  } else {
+    auto len_step = [&](int, int c, int v, int xl, uint32_t) {
+      const int o = c * 32 + lane;
+      int a = ls.a[o], nb = ls.nn[o];
+      const int k = kfast(a, nb);
+      nbits += rice_len(v, k) + xl;
+      a += v;  // _update_state
+      nb += 1;
+      if (nb >= kStateReset) {
+        a >>= 1;
+        nb >>= 1;
+      }
+      ls.a[o] = a;
+      ls.nn[o] = nb;
+      return k;
+    };
+    if constexpr (Gen::kStoresK) gen.for_each_setk(len_step);  // k kept for the emit pass
+    else gen.for_each(len_step);
+  }
   long long tbits;
   const long long loff = warp_excl_sum(nbits, &tbits);
   long long toff = 0;
@@ -484,23 +531,17 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
       if (xl) lb.put(sink, xb, xl);
     });
   } else {  // the emit pass re-runs each context's state to recover k
+    int ra[NL], rnn[NL];
 #pragma unroll
-    for (int c = 0; c < NL; c++) {
-      ls.a[c * 32 + lane] = a_start[c];
-      ls.nn[c * 32 + lane] = n0[c];
-    }
+    for (int c = 0; c < NL; c++) ra[c] = a_start[c], rnn[c] = n0[c];
     gen.for_each([&](int, int c, int v, int xl, uint32_t xb) {
-      const int o = c * 32 + lane;
-      int a = ls.a[o], nb = ls.nn[o];
-      const int k = kfast(a, nb);
-      a += v;
-      nb += 1;
-      if (nb >= kStateReset) {
-        a >>= 1;
-        nb >>= 1;
+      const int k = kfast(ra[c], rnn[c]);
+      ra[c] += v;
+      rnn[c] += 1;
+      if (rnn[c] >= kStateReset) {
+        ra[c] >>= 1;
+        rnn[c] >>= 1;
       }
-      ls.a[o] = a;
-      ls.nn[o] = nb;
       lb.put(sink, rice_bits(v, k), rice_len(v, k));
       if (xl) lb.put(sink, xb, xl);
     });
@@ -572,6 +613,7 @@ __device__ __forceinline__ LaneState carve_state(uint8_t* p, int nl) {
 // go out where it ends, _kernels.py:183-198, so no symbol moves between lanes).
 struct PlaneRowGen {
   static constexpr bool kStoresK = false;
+  static constexpr bool kStaticCtx = false;
   const uint8_t* cur;   // the lane's row; nullptr: idle lane
   const uint8_t* prev;  // the row above; nullptr on row 0
   int x0, x1;           // the segment
@@ -799,6 +841,7 @@ struct SymChunk {  // 8 u16 symbols, shifted in at the top
 
 struct PlaneBufGen {
   static constexpr bool kStoresK = true;
+  static constexpr bool kStaticCtx = false;
   uint4* slab;  // this lane's chunk 0
   int n;        // symbols
   template <class F>
