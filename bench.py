@@ -193,7 +193,7 @@ def run_b200(args):
     #      chunks pipelined so transfers overlap compute (container.HostPipeline) ----
     h_out = [torch.empty(c, dtype=torch.uint8).pin_memory() for c in caps]
     h_in_flat = [t.view(-1) for t in h_in]
-    pipe = container.HostPipeline(preps, device=local, chunk=args.chunk)
+    pipe = container.HostPipeline(preps, device=local, chunk=args.chunk, ctx=ctx)  # the device leg's arena
     pipe.run(h_in_flat, h_out)  # warm-up (allocations)
     if dist:
         dist.barrier()
@@ -453,7 +453,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--config", type=int, default=1)
-    ap.add_argument("--images", type=int, default=64)
+    ap.add_argument("--images", type=int, default=None, help="per rank; default 64 (c0, c1, c4), 1 (c2, c3)")
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--quality", type=int, default=85)
     ap.add_argument("--sigma", type=float, default=1.0)
@@ -463,6 +463,8 @@ def main():
     ap.add_argument("--tiled", action="store_true", help="config 3: tile-sharded path even on one rank")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.images is None:
+        args.images = 1 if args.config in (2, 3) else 64
     if args.impl == "reference":
         run_reference(args)
     elif args.config == 3 and (dist_env()[1] > 1 or args.tiled):

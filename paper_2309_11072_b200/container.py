@@ -558,7 +558,7 @@ class HostPipeline:
 
     NSLOT = 3
 
-    def __init__(self, preps, device: int = 0, chunk: int = 8):
+    def __init__(self, preps, device: int = 0, chunk: int = 8, ctx=None):
         import torch
 
         self.torch = torch
@@ -567,17 +567,18 @@ class HostPipeline:
         self.preps = preps
         self.chunk = max(1, chunk)
         self.chunks = [list(range(i, min(len(preps), i + self.chunk))) for i in range(0, len(preps), self.chunk)]
-        self.ctx = _native.Context(device)
+        self.ctx = ctx if ctx is not None else _native.Context(device)
         self.s_comp = torch.cuda.Stream(self.dev)
         self.s_h2d = torch.cuda.Stream(self.dev)
         self.s_d2h = torch.cuda.Stream(self.dev)
         mx = max(len(c) for c in self.chunks)
-        in_mx = max(p.pixels.nbytes for p in preps)
         self.caps = [stream_capacity(p) for p in preps]
-        cap_mx = max(self.caps)
+        # buffer k of a slot holds the k-th image of whichever chunk lands there
+        in_k = [max(preps[c[k]].pixels.nbytes for c in self.chunks if k < len(c)) for k in range(mx)]
+        cap_k = [max(self.caps[c[k]] for c in self.chunks if k < len(c)) for k in range(mx)]
         n = self.NSLOT
-        self.d_in = [[torch.empty(in_mx, dtype=torch.uint8, device=self.dev) for _ in range(mx)] for _ in range(n)]
-        self.d_out = [[torch.empty(cap_mx, dtype=torch.uint8, device=self.dev) for _ in range(mx)] for _ in range(n)]
+        self.d_in = [[torch.empty(in_k[k], dtype=torch.uint8, device=self.dev) for k in range(mx)] for _ in range(n)]
+        self.d_out = [[torch.empty(cap_k[k], dtype=torch.uint8, device=self.dev) for k in range(mx)] for _ in range(n)]
         self.d_len = [torch.zeros(mx, dtype=torch.int64, device=self.dev) for _ in range(n)]
         self.h_len = [torch.zeros(mx, dtype=torch.int64).pin_memory() for _ in range(n)]
         self.slot_free = [torch.cuda.Event() for _ in range(n)]
