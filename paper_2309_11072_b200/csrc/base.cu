@@ -178,6 +178,35 @@ __global__ void __launch_bounds__(256) k_sdr_ycc(const ImgDesc* __restrict__ des
 // (16 blocks), everything in shared memory.  kDecode (the GPU decoder,
 // decode.cu): start from the decoded zigzag coefficients instead, i.e. only
 // _reconstruct (codec_core.py:478-489) -- the encoder's inverse half.
+// out[o] = sum_t M[t][o] * in[t], t ascending, as idct_blocks (_kernels.py:404-422)
+// sums it -- except that terms whose input is zero in every lane of the warp
+// are skipped, and the sum starts at its first term rather than at 0.0.  A
+// skipped term adds an exact zero, so every sum keeps its value (only the sign
+// of a zero sum can differ, which no later rounding or clamp distinguishes).
+// Chroma blocks at Q=85 are mostly zero above DC, so this removes most of
+// their inverse-transform work.  All 32 lanes must call it.
+__device__ __forceinline__ void idct_line(const double (&in)[8], double (&out)[8]) {
+  unsigned m = 0;
+#pragma unroll
+  for (int tt = 0; tt < 8; tt++) m |= (in[tt] != 0.0 ? 1u : 0u) << tt;
+  m = __reduce_or_sync(0xffffffffu, m);
+#pragma unroll
+  for (int o = 0; o < 8; o++) out[o] = 0.0;
+  bool first = true;
+#pragma unroll
+  for (int tt = 0; tt < 8; tt++) {
+    if (!(m & (1u << tt))) continue;
+    if (first) {
+#pragma unroll
+      for (int o = 0; o < 8; o++) out[o] = kDctM[tt * 8 + o] * in[tt];
+    } else {
+#pragma unroll
+      for (int o = 0; o < 8; o++) out[o] += kDctM[tt * 8 + o] * in[tt];
+    }
+    first = false;
+  }
+}
+
 template <bool kDecode>
 __global__ void __launch_bounds__(128, 8) k_base_layer(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
@@ -241,9 +270,9 @@ __global__ void __launch_bounds__(128, 8) k_base_layer(const ImgDesc* __restrict
       for (int tt = 0; tt < 8; tt++) in[tt] = bufA[(ci * 8 + tt) * kRowStride + col0 + l];
 #pragma unroll
       for (int u = 0; u < 8; u++) {
-        double s = 0.0;
+        double s = kDctM[u * 8] * in[0];  // (0.0 + first term: same value up to the sign of a zero)
 #pragma unroll
-        for (int tt = 0; tt < 8; tt++) s += kDctM[u * 8 + tt] * in[tt];
+        for (int tt = 1; tt < 8; tt++) s += kDctM[u * 8 + tt] * in[tt];
         bufB[(ci * 8 + u) * kRowStride + col0 + l] = s;
       }
     }
@@ -261,9 +290,9 @@ __global__ void __launch_bounds__(128, 8) k_base_layer(const ImgDesc* __restrict
       int16_t* zz = d.zz + ((long long)ci * d.nblocks + bi) * 64;
 #pragma unroll
       for (int v = 0; v < 8; v++) {
-        double s = 0.0;
+        double s = in[0] * kDctM[v * 8];
 #pragma unroll
-        for (int tt = 0; tt < 8; tt++) s += in[tt] * kDctM[v * 8 + tt];
+        for (int tt = 1; tt < 8; tt++) s += in[tt] * kDctM[v * 8 + tt];
         const double qv = qt[l * 8 + v];
         const double qz = rha(s / qv);  // B200 fp64 division is cheaper than a certified reciprocal
         zz[c_zigzag[l * 8 + v]] = (int16_t)qz;
@@ -276,38 +305,28 @@ __global__ void __launch_bounds__(128, 8) k_base_layer(const ImgDesc* __restrict
   }  // !kDecode
 
   // 4. inverse pass 1 (idct_blocks first loop): tmp[x][v] = sum_t C[t][x] * coef[t][v], v = l
-  if (live) {
 #pragma unroll 1
-    for (int ci = 0; ci < 3; ci++) {
-      double in[8];
+  for (int ci = 0; ci < 3; ci++) {
+    double in[8], out[8];
 #pragma unroll
-      for (int tt = 0; tt < 8; tt++) in[tt] = bufA[(ci * 8 + tt) * kRowStride + col0 + l];
+    for (int tt = 0; tt < 8; tt++) in[tt] = live ? bufA[(ci * 8 + tt) * kRowStride + col0 + l] : 0.0;
+    idct_line(in, out);
+    if (live)
 #pragma unroll
-      for (int x = 0; x < 8; x++) {
-        double s = 0.0;
-#pragma unroll
-        for (int tt = 0; tt < 8; tt++) s += kDctM[tt * 8 + x] * in[tt];
-        bufB[(ci * 8 + x) * kRowStride + col0 + l] = s;
-      }
-    }
+      for (int x = 0; x < 8; x++) bufB[(ci * 8 + x) * kRowStride + col0 + l] = out[x];
   }
   __syncthreads();
 
   // 5. inverse pass 2: out[x][y] = sum_t tmp[x][t] * C[t][y], x = l
-  if (live) {
 #pragma unroll 1
-    for (int ci = 0; ci < 3; ci++) {
-      double in[8];
+  for (int ci = 0; ci < 3; ci++) {
+    double in[8], out[8];
 #pragma unroll
-      for (int tt = 0; tt < 8; tt++) in[tt] = bufB[(ci * 8 + l) * kRowStride + col0 + tt];
+    for (int tt = 0; tt < 8; tt++) in[tt] = live ? bufB[(ci * 8 + l) * kRowStride + col0 + tt] : 0.0;
+    idct_line(in, out);
+    if (live)
 #pragma unroll
-      for (int y = 0; y < 8; y++) {
-        double s = 0.0;
-#pragma unroll
-        for (int tt = 0; tt < 8; tt++) s += in[tt] * kDctM[tt * 8 + y];
-        bufA[(ci * 8 + l) * kRowStride + col0 + y] = s;
-      }
-    }
+      for (int y = 0; y < 8; y++) bufA[(ci * 8 + l) * kRowStride + col0 + y] = out[y];
   }
   __syncthreads();
 
