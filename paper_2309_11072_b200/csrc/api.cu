@@ -217,7 +217,10 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   c->launches += 2;
   mark(kStCrc);
   if (ct_dct.ntiles > 0) {
-    launch_entropy_dct(dd, ct_dct, st);
+    if (ensure(&c->plane_scratch, &c->plane_scratch_cap,
+               std::max(dct_scratch_bytes(ct_dct), plane_scratch_bytes(ct_pln, max_w)), true))
+      return HDLL_B200_E_CUDA;
+    launch_entropy_dct(dd, ct_dct, c->plane_scratch, st);
     launch_entropy_fixup(ct_dct, st);
     c->launches += 2;
   }

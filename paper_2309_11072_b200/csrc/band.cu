@@ -95,7 +95,10 @@ int run_chains(Ctx* c, Band* b, int mode) {
   uint8_t* E = (uint8_t*)c->estat;
   ChainTab ct_dct = b->hc_dct.table(b->sc_dct, D, E, c->estat_tiles, 0, b->d_ticket, c->epoch, mode);
   ChainTab ct_pln = b->hc_pln.table(b->sc_pln, D, E, c->estat_tiles, b->hc_dct.ntiles(), b->d_ticket + 2, c->epoch, mode);
-  launch_entropy_dct(b->d_desc, ct_dct, b->st);
+  if (ensure(&c->plane_scratch, &c->plane_scratch_cap,
+             std::max(dct_scratch_bytes(ct_dct), plane_scratch_bytes(ct_pln, b->W)), true))
+    return HDLL_B200_E_CUDA;
+  launch_entropy_dct(b->d_desc, ct_dct, c->plane_scratch, b->st);
   launch_entropy_fixup(ct_dct, b->st);
   if (ensure(&c->plane_scratch, &c->plane_scratch_cap, plane_scratch_bytes(ct_pln, b->W), true))
     return HDLL_B200_E_CUDA;

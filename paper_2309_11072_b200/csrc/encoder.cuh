@@ -230,7 +230,9 @@ void launch_bitcat(uint8_t* dst, const uint8_t* const* src, const unsigned long 
                    int npieces, unsigned long long max_bits, cudaStream_t);
 void launch_estimate(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
 void launch_crc(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
-void launch_entropy_dct(const ImgDesc*, const ChainTab&, cudaStream_t);
+// both coders keep per-warp scratch in one device buffer (they run one after the other)
+size_t dct_scratch_bytes(const ChainTab&);
+void launch_entropy_dct(const ImgDesc*, const ChainTab&, void* scratch, cudaStream_t);
 size_t plane_scratch_bytes(const ChainTab&, int max_w);
 void launch_entropy_plane(const ImgDesc*, const ChainTab&, int max_w, void* scratch, cudaStream_t);
 void launch_entropy_fixup(const ChainTab&, cudaStream_t);

@@ -219,6 +219,37 @@ struct LaneBits {
   }
 };
 
+// A lane's code bits before its position in the stream is known: MSB-first
+// 32-bit words at w[j * 32] (lanes interleaved), copied into place by the emit
+// pass once the look-back has given the lane its bit offset.
+struct ScratchBits {
+  uint32_t* w;
+  int cap, n, nacc;
+  unsigned long long acc;
+  __device__ __forceinline__ void init(uint32_t* p, int c) {
+    w = p;
+    cap = c;
+    n = nacc = 0;
+    acc = 0;
+  }
+  __device__ __forceinline__ void put(uint32_t bits, int len) {  // len <= 32
+    acc = (acc << len) | (unsigned long long)bits;
+    nacc += len;
+    if (nacc >= 32) {
+      nacc -= 32;
+      if (n < cap) w[n * 32] = (uint32_t)(acc >> nacc);
+      n++;
+    }
+  }
+  __device__ __forceinline__ void flush() {
+    if (nacc) {
+      if (n < cap) w[n * 32] = (uint32_t)(acc << (32 - nacc));
+      n++;
+      nacc = 0;
+    }
+  }
+};
+
 // ---------------------------------------------------------------------------
 // Symbol sources.  A generator enumerates a lane's symbols in coder order as
 // f(index, ctx, value, raw_len, raw_bits), re-deriving them from the data on
@@ -228,7 +259,6 @@ struct LaneBits {
 // DC size (ctx 0) + raw bits, then per nonzero AC (zero run ctx 1, size ctx 2 +
 // raw bits), EOB = run 64 unless position 63 is coded.
 struct DctBlockGen {
-  static constexpr bool kStoresK = false;
   static constexpr bool kStaticCtx = true;  // every f() call names its context
   const int16_t* z;  // nullptr: idle lane
   unsigned long long nzm;
@@ -273,7 +303,7 @@ struct LaneState {
 // ---------------------------------------------------------------------------
 template <int NL, int NC, class Gen>
 __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long g, int base, const Gen& gen,
-                         const int* cnt_in, const LaneState& ls, unsigned* status) {
+                         const int* cnt_in, const LaneState& ls, unsigned* status, uint32_t* scr, int scr_cap) {
   const int lane = threadIdx.x & 31;
 #ifdef HDLL_EXP_NO_LB  // timing experiment only: no look-backs (wrong output)
   const bool chain_start = true;
@@ -444,7 +474,7 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
     publish(ct, g, 1, 2);
   }
 
-  // ---- 3. code lengths (k of every symbol is kept for the emit pass when the generator can) ----
+  // ---- 3. codes: every symbol's Rice code (and raw bits) into the lane's scratch words ----
   int a_start[NL];
 #pragma unroll
   for (int c = 0; c < NL; c++) {
@@ -453,27 +483,34 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
     ls.nn[c * 32 + lane] = n0[c];
   }
   long long nbits = 0;
+  ScratchBits sb;
+  sb.init(scr, scr_cap);
   if constexpr (Gen::kStaticCtx) {
     int ra[NL], rnn[NL];
 #pragma unroll
     for (int c = 0; c < NL; c++) ra[c] = a_start[c], rnn[c] = n0[c];
-    gen.for_each([&](int, int c, int v, int xl, uint32_t) {
+    gen.for_each([&](int, int c, int v, int xl, uint32_t xb) {
       const int k = kfast(ra[c], rnn[c]);
-      nbits += rice_len(v, k) + xl;
+      const int rl = rice_len(v, k);
+      nbits += rl + xl;
+      sb.put(rice_bits(v, k), rl);
+      if (xl) sb.put(xb, xl);
       ra[c] += v;  // _update_state
       rnn[c] += 1;
       if (rnn[c] >= kStateReset) {
         ra[c] >>= 1;
         rnn[c] >>= 1;
       }
-      return k;
     });
   } else {
-    auto len_step = [&](int, int c, int v, int xl, uint32_t) {
+    gen.for_each([&](int, int c, int v, int xl, uint32_t xb) {
       const int o = c * 32 + lane;
       int a = ls.a[o], nb = ls.nn[o];
       const int k = kfast(a, nb);
-      nbits += rice_len(v, k) + xl;
+      const int rl = rice_len(v, k);
+      nbits += rl + xl;
+      sb.put(rice_bits(v, k), rl);
+      if (xl) sb.put(xb, xl);
       a += v;  // _update_state
       nb += 1;
       if (nb >= kStateReset) {
@@ -482,11 +519,10 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
       }
       ls.a[o] = a;
       ls.nn[o] = nb;
-      return k;
-    };
-    if constexpr (Gen::kStoresK) gen.for_each_setk(len_step);  // k kept for the emit pass
-    else gen.for_each(len_step);
+    });
   }
+  sb.flush();
+  if (sb.n > scr_cap) atomicOr(status, kErrCapacity);
   long long tbits;
   const long long loff = warp_excl_sum(nbits, &tbits);
   long long toff = 0;
@@ -525,26 +561,13 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
   LaneBits lb;
   lb.init(toff + loff);
 #ifndef HDLL_EXP_NO_EMIT
-  if constexpr (Gen::kStoresK) {
-    gen.for_each_k([&](int v, int k, int xl, uint32_t xb) {
-      lb.put(sink, rice_bits(v, k), rice_len(v, k));
-      if (xl) lb.put(sink, xb, xl);
-    });
-  } else {  // the emit pass re-runs each context's state to recover k
-    int ra[NL], rnn[NL];
-#pragma unroll
-    for (int c = 0; c < NL; c++) ra[c] = a_start[c], rnn[c] = n0[c];
-    gen.for_each([&](int, int c, int v, int xl, uint32_t xb) {
-      const int k = kfast(ra[c], rnn[c]);
-      ra[c] += v;
-      rnn[c] += 1;
-      if (rnn[c] >= kStateReset) {
-        ra[c] >>= 1;
-        rnn[c] >>= 1;
-      }
-      lb.put(sink, rice_bits(v, k), rice_len(v, k));
-      if (xl) lb.put(sink, xb, xl);
-    });
+  {  // the scratch words, shifted into place
+    const int nw = min(sb.n, scr_cap);
+    for (int j = 0; j < nw; j++) {
+      const uint32_t wd = scr[j * 32];
+      const int len = j < nw - 1 ? 32 : (int)(nbits - 32LL * (nw - 1));
+      lb.put(sink, len == 32 ? wd : wd >> (32 - len), len);
+    }
   }
 #endif
   // Lane partial words.  A lane that starts mid-word owes its first word to the
@@ -612,7 +635,6 @@ __device__ __forceinline__ LaneState carve_state(uint8_t* p, int nl) {
 // leave: either free, or inside a run of L samples so far (the run's chunks
 // go out where it ends, _kernels.py:183-198, so no symbol moves between lanes).
 struct PlaneRowGen {
-  static constexpr bool kStoresK = false;
   static constexpr bool kStaticCtx = false;
   const uint8_t* cur;   // the lane's row; nullptr: idle lane
   const uint8_t* prev;  // the row above; nullptr on row 0
@@ -840,7 +862,6 @@ struct SymChunk {  // 8 u16 symbols, shifted in at the top
 };
 
 struct PlaneBufGen {
-  static constexpr bool kStoresK = true;
   static constexpr bool kStaticCtx = false;
   uint4* slab;  // this lane's chunk 0
   int n;        // symbols
@@ -856,42 +877,16 @@ struct PlaneBufGen {
       }
     }
   }
-  template <class F>
-  __device__ __forceinline__ void for_each_setk(F&& f) const {  // f returns k
-    for (int q0 = 0; q0 < n; q0 += 8) {
-      SymChunk ch, out;
-      ch.load(slab[(q0 >> 3) * 32]);
-      const int m = min(8, n - q0);
-      for (int j = 0; j < m; j++) {
-        const uint32_t sy = ch.pop();
-        const int k = f(q0 + j, (int)((sy >> 8) & 7), (int)(sy & 0xFF), 0, 0u);
-        out.push((sy & 0x7FFu) | ((uint32_t)k << 11));
-      }
-      if (m < 8) out.align(m);
-      slab[(q0 >> 3) * 32] = out.word();
-    }
-  }
-  template <class F>
-  __device__ __forceinline__ void for_each_k(F&& f) const {  // f(value, k, raw_len, raw_bits)
-    for (int q0 = 0; q0 < n; q0 += 8) {
-      SymChunk ch;
-      ch.load(slab[(q0 >> 3) * 32]);
-      const int m = min(8, n - q0);
-      for (int j = 0; j < m; j++) {
-        const uint32_t sy = ch.pop();
-        f((int)(sy & 0xFF), (int)(sy >> 11), 0, 0u);
-      }
-    }
-  }
 };
 
 // grid-persistent, 4 warps per CTA, each warp's context state in shared memory
 __global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict__ descs, ChainTab ct, uint4* symbuf,
-                                                       int cap_chunks) {
+                                                       int cap_chunks, uint32_t* wordbuf) {
   __shared__ __align__(16) uint8_t smem_pl[4 * lane_state_bytes(5)];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const LaneState ls = carve_state(smem_pl + warp * lane_state_bytes(5), 5);
   uint4* slab = symbuf + ((long long)blockIdx.x * 4 + warp) * cap_chunks * 32 + lane;
+  uint32_t* scr = wordbuf + ((long long)blockIdx.x * 4 + warp) * cap_chunks * 8 * 32 + lane;  // <= 1 word per symbol
   int chain;
   long long tin, g;
   while (next_tile(ct, &chain, &tin, &g)) {
@@ -947,7 +942,7 @@ __global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict
 #ifdef HDLL_EXP_COUNT_ONLY  // timing experiment: the generation pass alone
     if (cnt[0] == -1) atomicOr(d.status, 1u);
 #else
-    run_tile<5, 5>(ct, chain, tin, g, 0, PlaneBufGen{slab, n}, cnt, ls, d.status);
+    run_tile<5, 5>(ct, chain, tin, g, 0, PlaneBufGen{slab, n}, cnt, ls, d.status, scr, cap_chunks * 8);
 #endif
     __syncwarp();
   }
@@ -956,10 +951,14 @@ __global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict
 // ---------------------------------------------------------------------------
 // DCT coder: tile = 32 blocks of one component, lane = block
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_entropy_dct(const ImgDesc* __restrict__ descs, ChainTab ct) {
+// a block's code: <= 544 bytes (dct_chain_cap) = 136 words
+constexpr int kDctScrWords = 136;
+
+__global__ void __launch_bounds__(128) k_entropy_dct(const ImgDesc* __restrict__ descs, ChainTab ct, uint32_t* wordbuf) {
   __shared__ __align__(16) uint8_t smem_dct[4 * lane_state_bytes(3)];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const LaneState ls = carve_state(smem_dct + warp * lane_state_bytes(3), 3);
+  uint32_t* scr = wordbuf + ((long long)blockIdx.x * 4 + warp) * kDctScrWords * 32 + lane;
   int chain;
   long long tin, g;
   while (next_tile(ct, &chain, &tin, &g)) {
@@ -1000,7 +999,7 @@ __global__ void __launch_bounds__(128) k_entropy_dct(const ImgDesc* __restrict__
       cnt[1] = nnz + ((nzm >> 63) ? 0 : 1);  // runs + EOB (absent when position 63 is coded)
       cnt[2] = nnz;
     }
-    run_tile<3, 6>(ct, chain, tin, g, ci == 0 ? 0 : 3, gen, cnt, ls, d.status);
+    run_tile<3, 6>(ct, chain, tin, g, ci == 0 ? 0 : 3, gen, cnt, ls, d.status, scr, kDctScrWords);
     __syncwarp();
   }
 }
@@ -1076,14 +1075,22 @@ static int num_sms() {
   return sms;
 }
 
-void launch_entropy_dct(const ImgDesc* d_descs, const ChainTab& ct, cudaStream_t st) {
-  if (ct.ntiles <= 0) return;
+static long long dct_grid(const ChainTab& ct) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_entropy_dct, 128, 0);
   long long blocks = (long long)num_sms() * (per_sm > 0 ? per_sm : 1);
-  long long need = (ct.ntiles + 3) / 4;
-  if (blocks > need) blocks = need;
-  k_entropy_dct<<<(unsigned)blocks, 128, 0, st>>>(d_descs, ct);
+  const long long need = (ct.ntiles + 3) / 4;
+  return blocks < need ? blocks : need;
+}
+
+size_t dct_scratch_bytes(const ChainTab& ct) {
+  if (ct.ntiles <= 0) return 0;
+  return (size_t)dct_grid(ct) * 4 * 32 * kDctScrWords * sizeof(uint32_t);
+}
+
+void launch_entropy_dct(const ImgDesc* d_descs, const ChainTab& ct, void* scratch, cudaStream_t st) {
+  if (ct.ntiles <= 0) return;
+  k_entropy_dct<<<(unsigned)dct_grid(ct), 128, 0, st>>>(d_descs, ct, (uint32_t*)scratch);
 }
 
 static long long plane_grid(const ChainTab& ct) {
@@ -1102,15 +1109,21 @@ static int plane_cap_chunks(int max_w, int segw) {
   return (2 * ws + max_w / 255 + 16) / 8 + 1;
 }
 
+// per warp: the symbol slab (16 B per 8 symbols) and the code words (<= 4 B per symbol)
+static size_t plane_warp_bytes(int cap_chunks) { return (size_t)32 * cap_chunks * (sizeof(uint4) + 8 * sizeof(uint32_t)); }
+
 size_t plane_scratch_bytes(const ChainTab& ct, int max_w) {
   if (ct.ntiles <= 0) return 0;
-  return (size_t)plane_grid(ct) * 4 * 32 * plane_cap_chunks(max_w, ct.plane_segw) * sizeof(uint4);
+  return (size_t)plane_grid(ct) * 4 * plane_warp_bytes(plane_cap_chunks(max_w, ct.plane_segw));
 }
 
 void launch_entropy_plane(const ImgDesc* d_descs, const ChainTab& ct, int max_w, void* scratch, cudaStream_t st) {
   if (ct.ntiles <= 0) return;
-  k_entropy_plane<<<(unsigned)plane_grid(ct), 128, 0, st>>>(d_descs, ct, (uint4*)scratch,
-                                                             plane_cap_chunks(max_w, ct.plane_segw));
+  const long long grid = plane_grid(ct);
+  const int cc = plane_cap_chunks(max_w, ct.plane_segw);
+  uint4* slabs = (uint4*)scratch;
+  uint32_t* words = (uint32_t*)(slabs + grid * 4 * 32 * cc);
+  k_entropy_plane<<<(unsigned)grid, 128, 0, st>>>(d_descs, ct, slabs, cc, words);
 }
 
 void launch_entropy_fixup(const ChainTab& ct, cudaStream_t st) {
