@@ -548,15 +548,20 @@ def encode_device(preps, rgbe_ptrs, out_ptrs, out_caps, lens_ptr: int, stream_ha
 class HostPipeline:
     """Host-to-host batched encode with transfers overlapped with compute.
 
-    The batch is cut into chunks encoded back to back on one compute stream;
-    chunk i+1's host->device copy and chunk i-1's device->host copy of its
-    streams run on two copy streams meanwhile.  Three rotating buffer slots keep
-    a slot from being refilled before its streams have been read back.  Inputs
-    are pinned host tensors; streams land in pinned host buffers.  This is the
-    `e2e` path of bench.py.
+    The images (the batch, `repeats` times over for a continuous stream) are
+    cut into chunks encoded back to back on one compute stream; chunk i+1's
+    host->device copy and chunk i-1's device->host copy of its streams run on
+    two copy streams meanwhile.  Three rotating buffer slots keep a slot from
+    being refilled before its streams have been read back.  The first and the
+    last chunk are half-size: the pipeline waits for the first chunk's upload
+    and for the last chunk's download with nothing to overlap them, and PCIe
+    (55 GB/s per direction) outruns the encoder, so a half-size first chunk
+    still uploads the next full one in time.  Inputs are pinned host tensors;
+    streams land in pinned host buffers.  This is the `e2e` path of bench.py.
     """
 
     NSLOT = 3
+    ALIGN = 256
 
     def __init__(self, preps, device: int = 0, chunk: int = 8, ctx=None):
         import torch
@@ -566,24 +571,48 @@ class HostPipeline:
         self.device = device
         self.preps = preps
         self.chunk = max(1, chunk)
-        self.chunks = [list(range(i, min(len(preps), i + self.chunk))) for i in range(0, len(preps), self.chunk)]
         self.ctx = ctx if ctx is not None else _native.Context(device)
         self.s_comp = torch.cuda.Stream(self.dev)
         self.s_h2d = torch.cuda.Stream(self.dev)
         self.s_d2h = torch.cuda.Stream(self.dev)
-        mx = max(len(c) for c in self.chunks)
         self.caps = [stream_capacity(p) for p in preps]
-        # buffer k of a slot holds the k-th image of whichever chunk lands there
-        in_k = [max(preps[c[k]].pixels.nbytes for c in self.chunks if k < len(c)) for k in range(mx)]
-        cap_k = [max(self.caps[c[k]] for c in self.chunks if k < len(c)) for k in range(mx)]
-        n = self.NSLOT
-        self.d_in = [[torch.empty(in_k[k], dtype=torch.uint8, device=self.dev) for k in range(mx)] for _ in range(n)]
-        self.d_out = [[torch.empty(cap_k[k], dtype=torch.uint8, device=self.dev) for k in range(mx)] for _ in range(n)]
-        self.d_len = [torch.zeros(mx, dtype=torch.int64, device=self.dev) for _ in range(n)]
-        self.h_len = [torch.zeros(mx, dtype=torch.int64).pin_memory() for _ in range(n)]
-        self.slot_free = [torch.cuda.Event() for _ in range(n)]
+        n, c = len(preps), min(self.chunk, len(preps))
+        al = lambda v: (v + self.ALIGN - 1) // self.ALIGN * self.ALIGN
+        # a slot holds any `chunk` consecutive images of the cyclic sequence
+        ins = [al(p.pixels.nbytes) for p in preps]
+        outs = [al(cp) for cp in self.caps]
+        in_mx = max(sum(ins[(i + k) % n] for k in range(c)) for i in range(n))
+        out_mx = max(sum(outs[(i + k) % n] for k in range(c)) for i in range(n))
+        ns = self.NSLOT
+        self.d_in = [torch.empty(in_mx, dtype=torch.uint8, device=self.dev) for _ in range(ns)]
+        self.d_out = [torch.empty(out_mx, dtype=torch.uint8, device=self.dev) for _ in range(ns)]
+        self.d_len = [torch.zeros(c, dtype=torch.int64, device=self.dev) for _ in range(ns)]
+        self.h_len = [torch.zeros(c, dtype=torch.int64).pin_memory() for _ in range(ns)]
+        self._ins, self._outs = ins, outs
+        self.slot_free = [torch.cuda.Event() for _ in range(ns)]
         for e in self.slot_free:
             e.record(torch.cuda.current_stream(self.dev))
+
+    def _chunks(self, repeats: int):
+        seq = list(range(len(self.preps))) * max(1, repeats)
+        c = min(self.chunk, len(self.preps))
+        if len(seq) <= c:
+            return [seq]
+        bounds = [0, c // 2] if c >= 2 else [0]
+        while bounds[-1] + c < len(seq):
+            bounds.append(bounds[-1] + c)
+        bounds.append(len(seq))
+        return [seq[a:b] for a, b in zip(bounds, bounds[1:]) if b > a]
+
+    def _layout(self, idx):
+        """byte offsets of the chunk's images in a slot's input / output buffers"""
+        oi, oo, ri, ro = [], [], 0, 0
+        for i in idx:
+            oi.append(ri)
+            oo.append(ro)
+            ri += self._ins[i]
+            ro += self._outs[i]
+        return oi, oo
 
     def run(self, h_in, h_out, repeats: int = 1):
         """h_in[i]: pinned uint8 tensor of image i's RGBE bytes; h_out[i]: pinned
@@ -594,15 +623,17 @@ class HostPipeline:
         lens = [0] * len(self.preps)
         pending = []
         ns = self.NSLOT
-        chunks = self.chunks * max(1, repeats)
+        chunks = self._chunks(repeats)
+        layouts = [self._layout(c) for c in chunks]
 
         def upload(ci):
             s = ci % ns
             self.s_h2d.wait_event(self.slot_free[s])
+            oi = layouts[ci][0]
             with torch.cuda.stream(self.s_h2d):
                 for k, i in enumerate(chunks[ci]):
                     nb = self.preps[i].pixels.nbytes
-                    self.d_in[s][k][:nb].copy_(h_in[i][:nb], non_blocking=True)
+                    self.d_in[s][oi[k]:oi[k] + nb].copy_(h_in[i][:nb], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(self.s_h2d)
             return ev
@@ -613,14 +644,16 @@ class HostPipeline:
             if ci + 1 < len(chunks):
                 up[ci + 1] = upload(ci + 1)  # next chunk's upload overlaps this chunk's encode
             self.s_comp.wait_event(up.pop(ci))
-            encode_device([self.preps[i] for i in idx], [self.d_in[s][k].data_ptr() for k in range(len(idx))],
-                          [self.d_out[s][k].data_ptr() for k in range(len(idx))], [self.caps[i] for i in idx],
-                          self.d_len[s].data_ptr(), self.s_comp.cuda_stream, self.device, self.ctx)
+            oi, oo = layouts[ci]
+            bi, bo = self.d_in[s].data_ptr(), self.d_out[s].data_ptr()
+            encode_device([self.preps[i] for i in idx], [bi + o for o in oi], [bo + o for o in oo],
+                          [self.caps[i] for i in idx], self.d_len[s].data_ptr(), self.s_comp.cuda_stream,
+                          self.device, self.ctx)
             with torch.cuda.stream(self.s_comp):
                 self.h_len[s][: len(idx)].copy_(self.d_len[s][: len(idx)], non_blocking=True)
             done = torch.cuda.Event()
             done.record(self.s_comp)
-            pending.append((idx, s, done))
+            pending.append((idx, s, oo, done))
             if len(pending) == 2:  # read back the previous chunk while this one computes
                 self._drain(pending.pop(0), h_out, lens)
         while pending:
@@ -631,12 +664,12 @@ class HostPipeline:
 
     def _drain(self, item, h_out, lens):
         torch = self.torch
-        idx, s, done = item
+        idx, s, oo, done = item
         done.synchronize()  # the chunk's lengths are on the host now
         self.s_d2h.wait_event(done)
         with torch.cuda.stream(self.s_d2h):
             for k, i in enumerate(idx):
                 n = int(self.h_len[s][k])
                 lens[i] = n
-                h_out[i][:n].copy_(self.d_out[s][k][:n], non_blocking=True)
+                h_out[i][:n].copy_(self.d_out[s][oo[k]:oo[k] + n], non_blocking=True)
         self.slot_free[s].record(self.s_d2h)

@@ -26,9 +26,17 @@ def enc(*a, **k):
 container.encode_device = enc
 t0 = time.perf_counter()
 base = torch.cuda.Event(enable_timing=True); base.record()
-pipe.run(h_in, h_out)
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+pipe.run(h_in, h_out, repeats=reps)
 torch.cuda.synchronize()
 wall = (time.perf_counter() - t0) * 1e3
-print(f"wall {wall:.1f} ms")
+print(f"wall {wall:.1f} ms for {reps} x {nimg} images ({nimg * reps * w * h / wall / 1e3:.0f} Mpix/s)")
+prev = None
+busy = 0.0
 for name, e0, e1 in evs:
-    print(name, f"{base.elapsed_time(e0):7.2f} -> {base.elapsed_time(e1):7.2f}")
+    a, b = base.elapsed_time(e0), base.elapsed_time(e1)
+    busy += b - a
+    gap = "" if prev is None else f"  gap {a - prev:6.2f}"
+    print(name, f"{a:7.2f} -> {b:7.2f} ({b - a:6.2f}){gap}")
+    prev = b
+print(f"compute busy {busy:.1f} ms of {wall:.1f}")
