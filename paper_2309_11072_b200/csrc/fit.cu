@@ -100,7 +100,7 @@ struct ScatterSmem {
   unsigned wcnt[8][256];
   unsigned loc_off[257];
   unsigned g_off[256];
-  double xs[3][kSortTile];
+  uint16_t src[kSortTile];  // slot -> sample of the tile
   uint8_t ys[3][kSortTile];
   uint8_t es[kSortTile];
 };
@@ -183,11 +183,8 @@ __global__ void __launch_bounds__(256) k_sort_scatter(const ImgDesc* __restrict_
       peers = __match_any_sync(act, e);
       const unsigned slot = sm.wcnt[w][e] + __popc(peers & lt);
 #pragma unroll
-      for (int c = 0; c < 3; c++) {
-        sm.xs[c][slot] =
-            real ? d.sstar[(long long)c * d.n + pb + p] : (double)d.s_planes[(long long)c * d.n + pb + p];
-        sm.ys[c][slot] = (uint8_t)((q >> (8 * c)) & 0xFF);
-      }
+      for (int c = 0; c < 3; c++) sm.ys[c][slot] = (uint8_t)((q >> (8 * c)) & 0xFF);
+      sm.src[slot] = (uint16_t)k;
       sm.es[slot] = (uint8_t)e;
     }
     __syncwarp();
@@ -198,9 +195,11 @@ __global__ void __launch_bounds__(256) k_sort_scatter(const ImgDesc* __restrict_
   for (int q = threadIdx.x; q < tn; q += blockDim.x) {
     const unsigned e = sm.es[q];
     const long long gpos = (long long)sm.g_off[e] + (q - sm.loc_off[e]);
+    const long long p = t0 + sm.src[q];  // a gather inside the tile's window (L1)
 #pragma unroll
     for (int c = 0; c < 3; c++) {
-      d.xs[(long long)c * m + gpos] = sm.xs[c][q];
+      d.xs[(long long)c * m + gpos] =
+          real ? d.sstar[(long long)c * d.n + pb + p] : (double)d.s_planes[(long long)c * d.n + pb + p];
       d.ys[(long long)c * m + gpos] = sm.ys[c][q];
     }
   }
