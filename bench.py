@@ -137,7 +137,13 @@ def run_b200(args):
 
     rank, world, local = dist_env()
     nimg = args.images
-    indices = [rank * nimg + i for i in range(nimg)]
+    if args.config == 4 and world > 1:  # the mixed stream: LPT on pixel count over all ranks' images
+        from paper_2309_11072_b200 import dist as D, synth
+        sizes = [h * w for h, w in synth.config4_sizes()[: world * nimg]]
+        indices = D.local_indices(sizes, rank, world)
+        nimg = len(indices)
+    else:
+        indices = [rank * nimg + i for i in range(nimg)]
     pix = generate(args.config, indices, args.scale)  # before any CUDA work (forked workers)
 
     torch.cuda.set_device(local)
@@ -274,7 +280,10 @@ def run_b200(args):
                                 f"c{args.config}: {nimg} mixed-size RGBE images per GPU ({npx / 1e6:.1f} Mpx), "
                                 "batch-sharded"),
                    "images_per_gpu": nimg, "width": w, "height": h, "quality": args.quality,
-                   "sigma": args.sigma, "slrme": True, "l2": "inputs (%.0f MB/GPU) exceed the 126 MB L2"
+                   "sigma": args.sigma, "slrme": True,
+                   "sharding": ("LPT on pixel count over all ranks' images (dist.lpt_assign)"
+                                if args.config == 4 and world > 1 else "contiguous image ranges per rank"),
+                   "l2": "inputs (%.0f MB/GPU) exceed the 126 MB L2"
                    % (h2d_bytes / 1e6), "blas_model": "skylakex/1 thread"},
         "roofline": {"bound": "hbm", "achieved": round(dom_achieved, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(dom_achieved / peak, 5), "traffic": traffic, "peak_source": peak_src,
