@@ -229,15 +229,17 @@ __device__ unsigned decode_plane_dev(const ImgDesc& d, int kind, uint8_t* rows /
   return 0;
 }
 
-// one thread per stream: thread 0 of image i the base layer, threads 1..4 its
-// planes (each with 2 rows of dynamic shared memory)
-__global__ void __launch_bounds__(32) k_decode_coders(const ImgDesc* __restrict__ descs, int with_planes, int max_w) {
+// one thread per stream, each in its own warp (lanes of one warp would take
+// turns on their divergent paths): warp 0 of image i's block decodes the base
+// layer, warps 1..4 its planes (each with 2 rows of dynamic shared memory)
+__global__ void __launch_bounds__(160) k_decode_coders(const ImgDesc* __restrict__ descs, int with_planes, int max_w) {
   extern __shared__ uint8_t dec_rows[];
   const ImgDesc& d = descs[blockIdx.x];
-  const int t = threadIdx.x;
+  if (threadIdx.x & 31) return;
+  const int t = threadIdx.x >> 5;
   unsigned st = 0;
   if (t == 0) st = decode_dct_image(d);
-  else if (t <= 4 && with_planes) st = decode_plane_dev(d, t, dec_rows + (long long)(t - 1) * 2 * max_w);
+  else if (with_planes) st = decode_plane_dev(d, t, dec_rows + (long long)(t - 1) * 2 * max_w);
   if (st) atomicOr(d.status, 1u << (kDecBadShift + t));
 }
 
@@ -283,7 +285,7 @@ __global__ void __launch_bounds__(256) k_decode_output(const ImgDesc* __restrict
 void launch_decode_coders(const ImgDesc* d_descs, int nimg, bool planes, int max_w, cudaStream_t st) {
   const size_t smem = planes ? (size_t)8 * max_w : 0;
   cudaFuncSetAttribute(k_decode_coders, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_decode_coders<<<nimg, 32, smem, st>>>(d_descs, planes ? 1 : 0, max_w);
+  k_decode_coders<<<nimg, planes ? 160 : 32, smem, st>>>(d_descs, planes ? 1 : 0, max_w);
 }
 
 void launch_decode_output(const ImgDesc* d_descs, int nimg, long long max_n, cudaStream_t st) {
