@@ -89,10 +89,11 @@ struct BitReader {
 };
 
 // _select_k (_kernels.py:114-119): smallest k <= 15 with (N << k) >= A, closed form
-__device__ __forceinline__ int select_k_dec(long long a, long long n) {
+// (A < 2^31: u < 24 << 15 per symbol, and A halves every 32 symbols)
+__device__ __forceinline__ int select_k_dec(int a, int n) {
   if (a <= n) return 0;
-  const int k0 = __clzll(n) - __clzll(a - 1);  // bitlen(a-1) - bitlen(n) >= 0
-  const int k = ((n << k0) >= a) ? k0 : k0 + 1;
+  const int k0 = __clz(n) - __clz(a - 1);  // bitlen(a-1) - bitlen(n) >= 0
+  const int k = (((long long)n << k0) >= a) ? k0 : k0 + 1;
   return k < kRiceMaxK ? k : kRiceMaxK;
 }
 
@@ -100,13 +101,13 @@ __device__ __forceinline__ int select_k_dec(long long a, long long n) {
 // the serial path); _update_state (_kernels.py:122-128)
 template <int NC>
 struct RiceState {
-  long long A[NC], N[NC];
+  int A[NC], N[NC];
   __device__ __forceinline__ void reset() {
 #pragma unroll
     for (int i = 0; i < NC; i++) A[i] = 4, N[i] = 1;
   }
   __device__ __forceinline__ int k(int c) const {
-    long long a = A[0], n = N[0];
+    int a = A[0], n = N[0];
 #pragma unroll
     for (int i = 1; i < NC; i++)
       if (c == i) a = A[i], n = N[i];
@@ -116,7 +117,7 @@ struct RiceState {
 #pragma unroll
     for (int i = 0; i < NC; i++)
       if (c == i) {
-        A[i] += u;
+        A[i] += (int)u;
         N[i] += 1;
         if (N[i] >= kStateReset) {
           A[i] >>= 1;
@@ -134,6 +135,7 @@ __device__ unsigned decode_dct_image(const ImgDesc& d) {
   br.init(d.pay[0], d.pay_bytes[0]);
   RiceState<6> rs;
   rs.reset();
+#pragma unroll  // the contexts become compile-time register indices
   for (int ci = 0; ci < 3; ci++) {
     const int base = ci == 0 ? 0 : 3;
     int16_t* zc = d.zz + (long long)ci * d.nblocks * 64;
