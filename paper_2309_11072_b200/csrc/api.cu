@@ -98,13 +98,25 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
     }
     hc_pln.segw = plane_segw_for(rows, mw);
   }
+  // A full encode codes each image's base layer as two chains: Y (contexts
+  // 0-2) and Cb, Cr (contexts 3-5).  No state crosses between them -- the
+  // reference's shared A/N arrays keep Y's and the chroma's contexts apart --
+  // so twice as many chains share the GPU, and the assembly appends the
+  // chroma bits to the Y bits.
+  const bool dct_split = mode == 0;
   for (int i = 0; i < n; i++) {
     const long long w = imgs[i].width, h = imgs[i].height;
     const long long nb = ((w + 7) / 8) * ((h + 7) / 8);
     for (int k = 0; k < 5; k++) {
       bool active = (mode == 0) || (mode == 1 && k == 1) || (mode == 2 && k == 0);
-      (k == 0 ? hc_dct : hc_pln).add(i, k, -1, 0, active ? (k == 0 ? nb : h) : 0, A + base[i] + lays[i].off_chain[k],
-                                     lays[i].chain_cap[k], (int)w);
+      uint8_t* out = A + base[i] + lays[i].off_chain[k];
+      if (k == 0 && dct_split) {
+        const long long ycap = dct_y_cap(nb);
+        hc_dct.add(i, 0, 0, 0, nb, out, ycap, (int)w);
+        hc_dct.add(i, 0, -2, 0, nb, out + ycap, lays[i].chain_cap[0] - ycap, (int)w);
+        continue;
+      }
+      (k == 0 ? hc_dct : hc_pln).add(i, k, -1, 0, active ? (k == 0 ? nb : h) : 0, out, lays[i].chain_cap[k], (int)w);
     }
   }
   hc_dct.schedule();
@@ -237,6 +249,8 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
     AsmTab at;
     at.dct_out = ct_dct.out;
     at.dct_bits = ct_dct.bits;
+    at.dct_stride = dct_split ? 2 : 1;
+    at.dct_split = dct_split;
     at.plane_out = ct_pln.out;
     at.plane_bits = ct_pln.bits;
     launch_assemble(dd, n, at, max_out, st);

@@ -23,6 +23,35 @@ __device__ __forceinline__ void put_le32(uint8_t* p, uint32_t v) {
   p[3] = v >> 24;
 }
 
+__device__ __forceinline__ uint32_t be_word(const uint8_t* p, long long k) {
+  return __byte_perm(reinterpret_cast<const uint32_t*>(p)[k], 0, 0x0123);
+}
+
+// 32 bits of an MSB-first stream of `nbits` bits from bit `b` (>= 0) on; bits
+// past the end read as 0
+__device__ __forceinline__ uint32_t bits_at(const uint8_t* p, long long nbits, long long b) {
+  if (b >= nbits) return 0u;
+  const long long k = b >> 5;
+  const int sh = (int)(b & 31);
+  uint32_t v = be_word(p, k) << sh;
+  if (sh && (k + 1) * 32 < nbits) v |= be_word(p, k + 1) >> (32 - sh);
+  const long long valid = nbits - b;
+  if (valid < 32) v &= ~0u << (32 - valid);
+  return v;
+}
+
+// Little-endian word k (stream bytes 4k .. 4k+3) of the base-layer body when
+// it is two chains: Y's bits, then Cb, Cr's bits straight after them.
+__device__ __forceinline__ uint32_t split_word(const uint8_t* y, long long ybits, const uint8_t* c, long long cbits,
+                                               long long k) {
+  const long long o = 32 * k;
+  uint32_t v;
+  if (o + 32 <= ybits) v = be_word(y, k);
+  else if (o >= ybits) v = bits_at(c, cbits, o - ybits);
+  else v = bits_at(y, ybits, o) | (bits_at(c, cbits, 0) >> (int)(ybits - o));
+  return __byte_perm(v, 0, 0x0123);
+}
+
 __global__ void __launch_bounds__(256) k_assemble(const ImgDesc* __restrict__ descs, AsmTab at) {
   const ImgDesc& d = descs[blockIdx.y];
   __shared__ Layout L;
@@ -48,7 +77,9 @@ __global__ void __launch_bounds__(256) k_assemble(const ImgDesc* __restrict__ de
     L.post = o;
     o += d.hdr_post_len;
     for (int k = 0; k < 5; k++) {
-      unsigned long long bits = k == 0 ? at.dct_bits[img] : at.plane_bits[img * 4 + k - 1];
+      const unsigned long long bits =
+          k == 0 ? at.dct_bits[img * at.dct_stride] + (at.dct_split ? at.dct_bits[img * at.dct_stride + 1] : 0ULL)
+                 : at.plane_bits[img * 4 + k - 1];
       L.body_len[k] = 8 + (long long)((bits + 7) / 8);
       L.pay[k] = o;
       o += 9 + L.body_len[k];
@@ -70,8 +101,34 @@ __global__ void __launch_bounds__(256) k_assemble(const ImgDesc* __restrict__ de
   const long long nthreads = (long long)gridDim.x * blockDim.x;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   for (int k = 0; k < 5; k++) {
-    const uint8_t* src = k == 0 ? at.dct_out[img] : at.plane_out[img * 4 + k - 1];
+    const uint8_t* src = k == 0 ? at.dct_out[img * at.dct_stride] : at.plane_out[img * 4 + k - 1];
     const long long dst0 = L.pay[k] + 17, len = L.body_len[k] - 8;
+    if (k == 0 && at.dct_split) {  // Y chain + Cb, Cr chain, bit-contiguous
+      const uint8_t* cs = at.dct_out[img * at.dct_stride + 1];
+      const long long yb = (long long)at.dct_bits[img * at.dct_stride];
+      const long long cb = (long long)at.dct_bits[img * at.dct_stride + 1];
+      const long long head = min(len, (16 - ((long long)(reinterpret_cast<uintptr_t>(d.out) + dst0) & 15)) & 15);
+      for (long long i = tid; i < head; i += nthreads)
+        if (dst0 + i < total) d.out[dst0 + i] = (uint8_t)(split_word(src, yb, cs, cb, i >> 2) >> (8 * (i & 3)));
+      const long long nvec = (len - head) / 16;
+      for (long long v = tid; v < nvec; v += nthreads) {
+        const long long so = head + v * 16;
+        const long long k0 = so >> 2;
+        const int sh = (int)(so & 3);
+        uint32_t w[5];
+#pragma unroll
+        for (int q = 0; q < 5; q++) w[q] = (q < 4 || sh) ? split_word(src, yb, cs, cb, k0 + q) : 0u;
+        uint4 o;
+        o.x = __funnelshift_r(w[0], w[1], 8 * sh);
+        o.y = __funnelshift_r(w[1], w[2], 8 * sh);
+        o.z = __funnelshift_r(w[2], w[3], 8 * sh);
+        o.w = __funnelshift_r(w[3], w[4], 8 * sh);
+        if (dst0 + so + 16 <= total) *reinterpret_cast<uint4*>(d.out + dst0 + so) = o;
+      }
+      for (long long i = head + nvec * 16 + tid; i < len; i += nthreads)
+        if (dst0 + i < total) d.out[dst0 + i] = (uint8_t)(split_word(src, yb, cs, cb, i >> 2) >> (8 * (i & 3)));
+      continue;
+    }
     // head bytes up to a 16-byte aligned destination, then aligned 16-byte chunks
     const long long head = min(len, (16 - ((long long)(reinterpret_cast<uintptr_t>(d.out) + dst0) & 15)) & 15);
     for (long long i = tid; i < head; i += nthreads)
@@ -151,10 +208,6 @@ __global__ void __launch_bounds__(256) k_assemble(const ImgDesc* __restrict__ de
 // are OR-ed into dst at bit dst_bit[p].  Words shared with a neighbouring
 // piece (a piece's first and last) use atomicOr; dst starts zeroed.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t be_word(const uint8_t* p, long long k) {
-  return __byte_perm(reinterpret_cast<const uint32_t*>(p)[k], 0, 0x0123);
-}
-
 __global__ void __launch_bounds__(256) k_bitcat(uint8_t* dst, const uint8_t* const* src,
                                                 const unsigned long long* dst_bit, const unsigned long long* nbits) {
   const int piece = blockIdx.y;

@@ -158,7 +158,7 @@ struct ChainTab {
   const long long* tile_base;  // [nchains+1] global tile index of each chain's tile 0
   const int* img;              // image of the chain
   const int* kind;             // 0 = DCT stream, 1..4 = plane (E, R, G, B)
-  const int* comp;             // DCT: the one component of the chain, or -1 for Y, Cb, Cr in turn
+  const int* comp;             // DCT: the one component of the chain, -1 for Y, Cb, Cr in turn, -2 for Cb, Cr
   const long long* first;      // first coded unit in the image arrays (DCT block / plane row)
   const long long* units;      // coded units (DCT: blocks per component; plane: rows)
   uint8_t* const* out;         // chain byte stream (4-byte aligned)
@@ -194,8 +194,13 @@ struct ChainTab {
 };
 
 struct AsmTab {
-  uint8_t* const* dct_out;                   // [nimg] base-layer DCT byte streams
-  const unsigned long long* dct_bits;        // [nimg] their bit totals
+  // base-layer DCT byte streams and bit totals: image i's at [i * dct_stride];
+  // with dct_split its stream is that chain (Y) followed, bit-contiguously, by
+  // chain [i * dct_stride + 1] (Cb, Cr)
+  uint8_t* const* dct_out;
+  const unsigned long long* dct_bits;
+  int dct_stride = 1;
+  bool dct_split = false;
   uint8_t* const* plane_out;                 // [nimg*4] E, R, G, B plane byte streams
   const unsigned long long* plane_bits;      // [nimg*4]
 };

@@ -965,8 +965,8 @@ __global__ void __launch_bounds__(128) k_entropy_dct(const ImgDesc* __restrict__
     const ImgDesc& d = descs[ct.img[chain]];
     const long long units = ct.units[chain];
     const long long tpc = (units + 31) / 32;
-    const int comp = ct.comp[chain];
-    const int ci = comp >= 0 ? comp : (int)(tin / tpc);
+    const int comp = ct.comp[chain];  // >= 0: that component; -1: Y, Cb, Cr; -2: Cb, Cr
+    const int ci = comp >= 0 ? comp : (comp == -2 ? 1 : 0) + (int)(tin / tpc);
     const long long tl = comp >= 0 ? tin : tin % tpc;
     const long long bi = ct.first[chain] + tl * 32 + lane;  // block index in the image arrays
     DctBlockGen gen{nullptr, 0ULL, 0u};

@@ -47,7 +47,9 @@ inline void quant_tables(int quality, double* out128) {
   }
 }
 
-inline long long dct_chain_cap(long long nblocks) { return (3 * nblocks * 544 + 64 + 15) / 16 * 16; }
+// a block's code <= 544 bytes; the buffer holds the Y chain, then the Cb, Cr chain
+inline long long dct_y_cap(long long nblocks) { return (nblocks * 544 + 64 + 15) / 16 * 16; }
+inline long long dct_chain_cap(long long nblocks) { return dct_y_cap(nblocks) + (2 * nblocks * 544 + 64 + 15) / 16 * 16; }
 inline long long plane_chain_cap(long long n) { return (n * 8 + 64 + 15) / 16 * 16; }
 inline long long max_seg_nodes(long long n) { return 3 * (2 * (n / kNodeTarget) + 2 * 256 + 2); }
 
@@ -227,7 +229,7 @@ struct HostChains {
       in_a.push_back(4);  // AdaptiveRiceState: A = 4 (_kernels.py:114-128)
     }
     const long long per = k == 0 ? kDctTileBlocks : plane_tile_rows(width, segw);
-    const long long tiles = (k == 0 && cp < 0 ? 3 : 1) * ((nunits + per - 1) / per);
+    const long long tiles = (k == 0 && cp < 0 ? (cp == -2 ? 2 : 3) : 1) * ((nunits + per - 1) / per);
     tile_base.push_back(tile_base.back() + tiles);
   }
   int nchains() const { return (int)img.size(); }
