@@ -167,22 +167,25 @@ __global__ void __launch_bounds__(256) k_prefilter_cols(const ImgDesc* __restric
   const uint8_t* col = S + gx;
   const long long W = d.w;
   const uint8_t* rp = col + (inner ? (long long)(y0 - R) * W : 0);
-  auto row_at = [&](int i) -> double {  // input row y0 - R + i of the column
-    if (inner) {
-      const double v = (double)__ldg(rp);
-      rp += W;
-      return v;
-    }
-    return (double)__ldg(col + (long long)reflect_idx((long long)y0 - R + i, d.h) * W);
-  };
+  // all kCR + 2R input bytes of the column in flight at once (the pass is
+  // otherwise bound by one dependent load latency per output row)
+  uint8_t colv[kCR + 2 * R];
+  if (inner) {
+#pragma unroll
+    for (int i = 0; i < kCR + 2 * R; i++) colv[i] = __ldg(rp + (long long)i * W);
+  } else {
+#pragma unroll
+    for (int i = 0; i < kCR + 2 * R; i++)
+      colv[i] = __ldg(col + (long long)reflect_idx((long long)y0 - R + i, d.h) * W);
+  }
   double win[2 * R + 1];
 #pragma unroll
-  for (int i = 0; i < 2 * R; i++) win[i + 1] = row_at(i);
+  for (int i = 0; i < 2 * R; i++) win[i + 1] = (double)colv[i];
 #pragma unroll
   for (int oy = 0; oy < kCR; oy++) {
 #pragma unroll
     for (int i = 0; i < 2 * R; i++) win[i] = win[i + 1];
-    win[2 * R] = row_at(oy + 2 * R);
+    win[2 * R] = (double)colv[oy + 2 * R];
     double o = win[R] * fw[0];
 #pragma unroll
     for (int j = R; j >= 1; j--) o += (win[R - j] + win[R + j]) * fw[j];
