@@ -639,6 +639,18 @@ __device__ __forceinline__ LaneState carve_state(uint8_t* p, int nl) {
 // other than the first enters in the automaton state the previous segments
 // leave: either free, or inside a run of L samples so far (the run's chunks
 // go out where it ends, _kernels.py:183-198, so no symbol moves between lanes).
+// What the coding of a segment entered free tells about entering it inside a
+// run: the first sample that differs from its left neighbour (E false) ends any
+// run, and both entries code it as a regular sample and leave it outside a run,
+// so from there on they emit the same symbols.
+struct RowTrack {
+  bool brk;    // some sample has E false
+  int cov;     // samples before it (all E true)
+  int brk_i;   // symbols of the free coding up to and including it
+  bool out_in; // exit state of the free coding
+  int out_L;
+};
+
 struct PlaneRowGen {
   static constexpr bool kStaticCtx = false;
   const uint8_t* cur;   // the lane's row; nullptr: idle lane
@@ -647,6 +659,7 @@ struct PlaneRowGen {
   bool last;            // x1 == width: a run open at x1 ends with the row
   bool inrun0;          // entry state
   int L0;               // samples of the entering run so far
+  RowTrack* trk;        // nullptr, or filled in (entered free)
   // f(index, ctx, value, 0, 0) in coder order.  _neighbors (_kernels.py:131-143):
   // a = left (above at x = 0, 128 at the origin), b = above (else a),
   // c = above-left (else b).
@@ -658,6 +671,8 @@ struct PlaneRowGen {
     int c = x0 > 0 ? (prev ? prev[x0 - 1] : a) : a;  // above-left (the above sample at x = 0)
     bool inrun = inrun0;
     int L = L0;
+    int nsamp = 0;
+    if (trk) trk->brk = false;
     auto run_chunks = [&]() {  // chunks of <= 255; a chunk of 255 continues
       for (;;) {
         const int ch = L >= 255 ? 255 : L;
@@ -693,6 +708,12 @@ struct PlaneRowGen {
         if (r > 127) r -= 256;
         f(i++, ctx, r >= 0 ? 2 * r : -2 * r - 1, 0, 0u);
       }
+      if (trk && !E && !trk->brk) {
+        trk->brk = true;
+        trk->cov = nsamp;
+        trk->brk_i = i;
+      }
+      nsamp++;
       c = b;
       a = xv;
     };
@@ -718,6 +739,11 @@ struct PlaneRowGen {
       }
     }
     for (; x < x1; x++) sample(__ldg(cur + x), __ldg(pv + x));
+    if (trk) {
+      trk->out_in = inrun;
+      trk->out_L = L;
+      if (!trk->brk) trk->cov = nsamp;
+    }
     if (inrun && last) run_chunks();  // a run reaching the row end
   }
 };
@@ -766,46 +792,6 @@ __device__ __forceinline__ SegFn segfn_then(const SegFn& f, const SegFn& g) {  /
   return h;
 }
 
-// one sweep of the segment for both entry states
-__device__ SegFn segment_fn(const uint8_t* cur, const uint8_t* prev, int x0, int x1) {
-  int a = x0 > 0 ? cur[x0 - 1] : (prev ? __ldg(prev) : 128);
-  int c = x0 > 0 ? (prev ? prev[x0 - 1] : a) : a;
-  bool fin = false, rin = true, carried = true;
-  int fL = 0, rL = 0, cov = 0;
-  for (int x = x0; x < x1; x++) {
-    const int xv = __ldg(cur + x);
-    const int b = prev ? __ldg(prev + x) : a;
-    const int cc = prev ? c : a;
-    const bool E = xv == a, F = a == b && b == cc;
-    // entered free
-    if (!fin && F) fin = true, fL = 0;
-    if (fin) {
-      if (E) fL++;
-      else fin = false;
-    }
-    // entered inside a run
-    if (carried) {
-      if (E) cov++;
-      else carried = false, rin = false;
-    } else {
-      if (!rin && F) rin = true, rL = 0;
-      if (rin) {
-        if (E) rL++;
-        else rin = false;
-      }
-    }
-    c = b;
-    a = xv;
-  }
-  SegFn f;
-  f.f_in = fin;
-  f.f_L = fL;
-  f.full = carried;
-  f.cov = cov;
-  f.r_in = carried ? true : rin;
-  f.r_L = carried ? 0 : rL;
-  return f;
-}
 
 __device__ __forceinline__ SegFn shfl_up_segfn(const SegFn& f, int d) {
   const unsigned bits = (unsigned)f.f_in | ((unsigned)f.full << 1) | ((unsigned)f.r_in << 2);
@@ -866,23 +852,48 @@ struct SymChunk {  // 8 u16 symbols, shifted in at the top
   }
 };
 
+// A lane's symbols: the slab's [start, n), after (for a segment entered inside
+// a run) the run's chunks of run_len samples and the symbol `head` (>= 0) of the
+// sample that ended it.
 struct PlaneBufGen {
   static constexpr bool kStaticCtx = false;
   uint4* slab;  // this lane's chunk 0
-  int n;        // symbols
+  int n;        // symbols in the slab
+  int start;    // first slab symbol coded
+  int run_len;  // < 0: no chunks
+  int head;     // < 0: none
   template <class F>
   __device__ __forceinline__ void for_each(F&& f) const {
-    for (int q0 = 0; q0 < n; q0 += 8) {
+    int i = 0;
+    if (run_len >= 0) {
+      int L = run_len;
+      for (;;) {
+        const int ch = L >= 255 ? 255 : L;
+        f(i++, kRunCtx, ch, 0, 0u);
+        L -= ch;
+        if (ch < 255) break;
+      }
+    }
+    if (head >= 0) f(i++, (head >> 8) & 7, head & 0xFF, 0, 0u);
+    for (int q0 = start & ~7; q0 < n; q0 += 8) {
       SymChunk ch;
       ch.load(slab[(q0 >> 3) * 32]);
       const int m = min(8, n - q0);
       for (int j = 0; j < m; j++) {
         const uint32_t sy = ch.pop();
-        f(q0 + j, (int)((sy >> 8) & 7), (int)(sy & 0xFF), 0, 0u);
+        if (q0 + j >= start) f(i++, (int)((sy >> 8) & 7), (int)(sy & 0xFF), 0, 0u);
       }
     }
   }
 };
+
+// symbol q of a lane's slab
+__device__ __forceinline__ uint32_t slab_symbol(const uint4* slab, int q) {
+  const uint4 w = slab[(q >> 3) * 32];
+  const int j = q & 7;
+  const uint32_t wd = j < 2 ? w.x : (j < 4 ? w.y : (j < 6 ? w.z : w.w));
+  return (j & 1) ? (wd >> 16) : (wd & 0xFFFFu);
+}
 
 // grid-persistent, 4 warps per CTA, each warp's context state in shared memory
 __global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict__ descs, ChainTab ct, uint4* symbuf,
@@ -906,22 +917,20 @@ __global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict
     const long long y = ct.first[chain] + (live ? r : 0);  // row in the image arrays
     const uint8_t* cur = src + y * d.w;
     const uint8_t* prev = y > 0 ? cur - d.w : nullptr;
-    // entry state of the segment: segmented scan of the segments' functions
-    bool in0 = false;
-    int L0 = 0;
-    if (S > 1) {
-      SegFn f = live ? segment_fn(cur, prev, x0, x1) : segfn_identity();
-      for (int dd = 1; dd < S; dd <<= 1) {
-        const SegFn o = shfl_up_segfn(f, dd);
-        if (sg >= dd) f = segfn_then(o, f);
-      }
-      const SegFn ex = shfl_up_segfn(f, 1);
-      if (sg > 0) segfn_apply(ex, in0, L0);
-    }
+    // Every segment is coded entered free; a segment that continues a run
+    // from the previous ones (segmented scan of the segments' automaton
+    // functions, derived from the same pass) then swaps the free coding's
+    // symbols up to its first run-ending sample for the run's chunks.
+    RowTrack trk;
+    trk.brk = false;
+    trk.cov = 0;
+    trk.brk_i = 0;
+    trk.out_in = false;
+    trk.out_L = 0;
     int cnt[5] = {0, 0, 0, 0, 0};
     int n = 0;
     if (live) {
-      PlaneRowGen gen{cur, prev, x0, x1, x1 == d.w, in0, L0};
+      PlaneRowGen gen{cur, prev, x0, x1, x1 == d.w, false, 0, S > 1 ? &trk : nullptr};
       // counts per context (two 32-bit fields per word for the regular contexts)
       unsigned long long p01 = 0, p23 = 0;
       int c4 = 0;
@@ -944,10 +953,43 @@ __global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict
       cnt[3] = (int)(p23 >> 32);
       cnt[4] = c4;
     }
+    PlaneBufGen gen{slab, n, 0, -1, -1};
+    if (S > 1) {
+      SegFn f = segfn_identity();
+      if (live) {
+        f.f_in = trk.out_in;
+        f.f_L = trk.out_L;
+        f.full = !trk.brk;
+        f.cov = trk.cov;
+        f.r_in = trk.out_in;
+        f.r_L = trk.out_L;
+      }
+      for (int dd = 1; dd < S; dd <<= 1) {
+        const SegFn o = shfl_up_segfn(f, dd);
+        if (sg >= dd) f = segfn_then(o, f);
+      }
+      const SegFn ex = shfl_up_segfn(f, 1);
+      bool in0 = false;
+      int L0 = 0;
+      if (sg > 0) segfn_apply(ex, in0, L0);
+      if (live && in0) {  // entered inside a run of L0 samples
+        const int run = L0 + trk.cov;
+        const int upto = trk.brk ? trk.brk_i : n;  // free symbols replaced
+        for (int q = 0; q < upto; q++) cnt[(slab_symbol(slab, q) >> 8) & 7]--;
+        const bool chunks = trk.brk || x1 == d.w;  // the run ends here (or with the row)
+        if (chunks) cnt[kRunCtx] += run / 255 + 1;
+        gen.start = upto;
+        gen.run_len = chunks ? run : -1;
+        if (trk.brk) {
+          gen.head = (int)slab_symbol(slab, trk.brk_i - 1);
+          cnt[(gen.head >> 8) & 7]++;
+        }
+      }
+    }
 #ifdef HDLL_EXP_COUNT_ONLY  // timing experiment: the generation pass alone
     if (cnt[0] == -1) atomicOr(d.status, 1u);
 #else
-    run_tile<5, 5>(ct, chain, tin, g, 0, PlaneBufGen{slab, n}, cnt, ls, d.status, scr, cap_chunks * 8);
+    run_tile<5, 5>(ct, chain, tin, g, 0, gen, cnt, ls, d.status, scr, cap_chunks * 8);
 #endif
     __syncwarp();
   }

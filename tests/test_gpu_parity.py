@@ -208,12 +208,16 @@ def test_errors(gpu):
 # whose automaton entry state comes from a scan (runs carried across them)
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("w,h,kind", [(4100, 24, "scene"), (9000, 12, "flat"), (6000, 10, "stripes"),
-                                      (2049, 16, "scene"), (65536 + 8, 2, "flat")])
+                                      (2049, 16, "scene"), (65536 + 8, 2, "flat"), (9000, 6, "const")])
 def test_wide_rows_match_oracle(w, h, kind, gpu):
     from paper_2309_11072_b200 import synth
     rng = np.random.default_rng(w + h)
     if kind == "scene":
         px = np.tile(synth.make_config(0, 1), (1, -(-w // 768), 1))[:h, :w].copy()
+    elif kind == "const":  # every segment inside one run: only the row end emits its chunks
+        px = np.zeros((h, w, 4), np.uint8)
+        px[...] = (140, 130, 120, 128)
+        px[h // 2:] = (7, 7, 7, 100)
     elif kind == "flat":  # long constant runs crossing every segment boundary, a few breaks
         px = np.zeros((h, w, 4), np.uint8)
         px[...] = (140, 130, 120, 128)
