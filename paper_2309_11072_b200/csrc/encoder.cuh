@@ -140,12 +140,12 @@ __host__ __device__ inline int plane_row_segments(int w, int segw) {
 inline int plane_tile_rows(int w, int segw) { return kPlaneTileRows / plane_row_segments(w, segw); }
 
 // target segment width for a launch coding `rows` plane rows in all: about
-// eight waves of tiles over the GPU's warps, segments of >= 256 samples
+// sixteen waves of tiles over the GPU's warps, segments of >= 256 samples
 inline int plane_segw_for(long long rows, int max_w) {
-  // ~8 waves of tiles over the resident warps (148 SMs x 28): a tile takes
+  // ~16 waves of tiles over the resident warps (148 SMs x 28): a tile takes
   // ~2 ms / S, and with ~2 waves the last, partial wave idles most of the GPU
-  // (config 1: S = 4 measured 0.3 ms faster than S = 1; S = 2 slower)
-  const long long want_tiles = 8LL * 148 * 28;
+  // (config 1: S = 8 measured 0.8 ms faster than S = 1; 2 and 4 in between)
+  const long long want_tiles = 16LL * 148 * 28;
   long long s = 1;
   while (s < 32 && rows * s / kPlaneTileRows < want_tiles) s <<= 1;
   int segw = (int)((max_w + s - 1) / s);
