@@ -192,6 +192,28 @@ __global__ void __launch_bounds__(256) k_sort_scatter(const ImgDesc* __restrict_
     __syncwarp();
   }
   __syncthreads();
+  if (tn == kSortTile && real) {  // full tile: every gather in flight before the stores
+    constexpr int kR = kSortTile / 256;
+    double xv[kR][3];
+#pragma unroll
+    for (int r = 0; r < kR; r++) {
+      const long long p = t0 + sm.src[threadIdx.x + 256 * r];
+#pragma unroll
+      for (int c = 0; c < 3; c++) xv[r][c] = d.sstar[(long long)c * d.n + pb + p];
+    }
+#pragma unroll
+    for (int r = 0; r < kR; r++) {
+      const int q = threadIdx.x + 256 * r;
+      const unsigned e = sm.es[q];
+      const long long gpos = (long long)sm.g_off[e] + (q - sm.loc_off[e]);
+#pragma unroll
+      for (int c = 0; c < 3; c++) {
+        d.xs[(long long)c * m + gpos] = xv[r][c];
+        d.ys[(long long)c * m + gpos] = sm.ys[c][q];
+      }
+    }
+    return;
+  }
   for (int q = threadIdx.x; q < tn; q += blockDim.x) {
     const unsigned e = sm.es[q];
     const long long gpos = (long long)sm.g_off[e] + (q - sm.loc_off[e]);
