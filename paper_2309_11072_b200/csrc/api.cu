@@ -207,7 +207,7 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   mark(kStTonemap);
   if (mode != 1) {
     launch_base_layer(dd, n, max_base_tiles, max_n, st);
-    c->launches += 2;
+    c->launches += 3;
   }
   mark(kStBase);
   if (mode == 0 && any_real) {

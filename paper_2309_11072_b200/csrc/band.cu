@@ -278,7 +278,7 @@ int hdll_b200_band_layers(hdll_b200_ctx* ctx, const double* h_nodes_all, uint64_
   CK(cudaMemcpyAsync(d.maxlw, &maxlw, 8, cudaMemcpyHostToDevice, b->st));
   launch_tonemap_scalars(b->d_desc, 1, b->st);
   launch_base_layer(b->d_desc, 1, (d.nbx + 15) / 16 * d.nby, d.n, b->st);
-  c->launches += 2;
+  c->launches += 3;
   if (d.slrme && d.sigma_milli) {
     launch_prefilter(b->d_desc, 1, d.w, d.h, d.radius, b->st);
     c->launches += 2;

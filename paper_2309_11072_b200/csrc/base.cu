@@ -62,28 +62,47 @@ __device__ __noinline__ uint8_t quantize_pow_exact(double m, double g) {
   return (uint8_t)rha(255.0 * clampd(v, 0.0, 1.0));
 }
 
-__device__ __forceinline__ uint8_t quantize_pow(double m, double g, float g32, unsigned* amb) {
+// For 1 / gamma <= 4 the fp32 pass uses the MUFU approximations (lg2 / ex2
+// .approx: ~2^-22 relative): |err(255 m^g)| stays below 4e-4, well inside kAmb.
+constexpr float kApproxMaxG = 4.0f;
+
+__device__ __forceinline__ float lg2_approx(float x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// the byte, or -1 when the fp32 value is too close to a rounding boundary
+__device__ __forceinline__ int quantize_pow_fast(double m, float g32, bool approx) {
   if (m >= 1.0) return 255;  // m^g >= 1 clips to 1
   if (m <= 0.0) return 0;
-  const float y = 255.0f * exp2f(g32 * log2f(__double2float_rn(m)));
+  const float mf = __double2float_rn(m);
+  const float y = 255.0f * (approx ? ex2_approx(g32 * lg2_approx(mf)) : exp2f(g32 * log2f(mf)));
   const float yf = y + 0.5f;
   const float fl = floorf(yf), fr = yf - fl;
-  if (fr > kAmb && fr < 1.0f - kAmb) return (uint8_t)fl;
-  (*amb)++;
-  return quantize_pow_exact(m, g);
+  if (fr > kAmb && fr < 1.0f - kAmb) return (int)fl;
+  return -1;
 }
 
 // tone_map pass B for one pixel -> 3 SDR bytes (fp64 chain of the reference,
-// tonemap.py:102-110; the gamma step through quantize_pow)
+// tonemap.py:102-110; the gamma step through quantize_pow_fast, and with
+// `exact` the fp64 pow for whatever the fast pass cannot certify).  Returns
+// false when a byte is undecided (exact == false only).
 struct TmoConst {
-  float g32;  // 1 / gamma
+  float g32;    // 1 / gamma
+  bool approx;  // g32 <= kApproxMaxG
 };
 
-__device__ __forceinline__ void sdr_pixel(const ImgDesc& d, uint32_t q, double log_avg, double white,
-                                          const TmoConst& tc, bool allzero, uint8_t* out3, unsigned* amb) {
+__device__ __forceinline__ bool sdr_pixel(const ImgDesc& d, uint32_t q, double log_avg, double white,
+                                          const TmoConst& tc, bool allzero, uint8_t* out3, bool exact) {
   if (allzero || q == 0u) {
     out3[0] = out3[1] = out3[2] = 0;
-    return;
+    return true;
   }
   const double sc = rgbe_scale_b(q >> 24);
   double f[3];
@@ -94,8 +113,18 @@ __device__ __forceinline__ void sdr_pixel(const ImgDesc& d, uint32_t q, double l
   const double scaled = d.key * lw / log_avg;
   const double disp = scaled * (1.0 + scaled / (white * white)) / (1.0 + scaled);
   const double ratio = lw > 0 ? disp / lw : 0.0;
+  bool ok = true;
 #pragma unroll
-  for (int c = 0; c < 3; c++) out3[c] = quantize_pow(fmax(f[c] * ratio, 0.0), d.inv_gamma, tc.g32, amb);
+  for (int c = 0; c < 3; c++) {
+    const double m = fmax(f[c] * ratio, 0.0);
+    int v = quantize_pow_fast(m, tc.g32, tc.approx);
+    if (v < 0) {
+      if (exact) v = quantize_pow_exact(m, d.inv_gamma);
+      else ok = false;
+    }
+    out3[c] = (uint8_t)v;
+  }
+  return ok;
 }
 
 // Pass 1, per pixel: tone-map pass B (or the given SDR in the lossy-coder
@@ -119,7 +148,7 @@ __global__ void __launch_bounds__(256) k_sdr_ycc(const ImgDesc* __restrict__ des
   const bool allzero = d.sdr_in ? false : d.scalars[3] != 0.0;
   TmoConst tc;
   tc.g32 = (float)d.inv_gamma;
-  unsigned amb = 0;  // samples the fp32 pow could not certify
+  tc.approx = tc.g32 <= kApproxMaxG;
   const long long nq = (d.n + 3) / 4;
   uint8_t* Yp = d.ycc;
   int8_t* Cb = reinterpret_cast<int8_t*>(d.ycc + d.n);
@@ -154,7 +183,16 @@ __global__ void __launch_bounds__(256) k_sdr_ycc(const ImgDesc* __restrict__ des
         s3[0] = d.sdr_in[3 * p], s3[1] = d.sdr_in[3 * p + 1], s3[2] = d.sdr_in[3 * p + 2];
       } else {
         const uint32_t q = k == 0 ? qs[0] : (k == 1 ? qs[1] : (k == 2 ? qs[2] : qs[3]));
-        sdr_pixel(d, q, log_avg, white, tc, allzero, s3, &amb);
+        if (!sdr_pixel(d, q, log_avg, white, tc, allzero, s3, false)) {
+          // a byte the fp32 pass cannot certify (~0.3 % of samples): the pixel
+          // goes to k_sdr_fix instead of holding its warp through an fp64 pow
+          const unsigned slot = atomicAdd(d.amb, 1u);
+          if (slot < d.amb_cap) {
+            d.amb_list[slot] = (unsigned)p;
+            continue;
+          }
+          sdr_pixel(d, q, log_avg, white, tc, allzero, s3, true);  // list full: here
+        }
         if (d.want_trace) {
           d.sdr[3 * p] = s3[0];
           d.sdr[3 * p + 1] = s3[1];
@@ -171,7 +209,29 @@ __global__ void __launch_bounds__(256) k_sdr_ycc(const ImgDesc* __restrict__ des
       if (hc) atomicAdd(&d.bin_count[threadIdx.x], hc);
     }
   }
-  if (amb) atomicAdd(d.amb, amb);
+}
+
+// the deferred pixels of k_sdr_ycc, with the fp64 pow where needed
+__global__ void __launch_bounds__(256) k_sdr_fix(const ImgDesc* __restrict__ descs) {
+  const ImgDesc& d = descs[blockIdx.y];
+  if (d.sdr_in) return;
+  const unsigned cnt = min(*d.amb, d.amb_cap);
+  TmoConst tc;
+  tc.g32 = (float)d.inv_gamma;
+  tc.approx = tc.g32 <= kApproxMaxG;
+  const double log_avg = d.scalars[1], white = d.scalars[2];
+  const bool allzero = d.scalars[3] != 0.0;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+    const long long p = d.amb_list[i];
+    uint8_t s3[3];
+    sdr_pixel(d, reinterpret_cast<const uint32_t*>(d.rgbe)[p], log_avg, white, tc, allzero, s3, true);
+    if (d.want_trace) {
+      d.sdr[3 * p] = s3[0];
+      d.sdr[3 * p + 1] = s3[1];
+      d.sdr[3 * p + 2] = s3[2];
+    }
+    ycc_bytes(s3, d.ycc + p, reinterpret_cast<int8_t*>(d.ycc + d.n) + p, reinterpret_cast<int8_t*>(d.ycc + 2 * d.n) + p);
+  }
 }
 
 // Pass 2: the 8x8 DCT round trip of one tile = 8 pixel rows x 128 columns
@@ -366,6 +426,7 @@ void launch_base_layer(const ImgDesc* d_descs, int nimg, int max_tiles, long lon
   if (gx > 148 * 8) gx = 148 * 8;
   if (gx < 1) gx = 1;
   k_sdr_ycc<<<dim3(gx, nimg), 256, 0, st>>>(d_descs);
+  k_sdr_fix<<<dim3(8, nimg), 256, 0, st>>>(d_descs);
   size_t smem = sizeof(double) * 3 * 8 * kRowStride;
   cudaFuncSetAttribute(k_base_layer<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  // per device
   k_base_layer<false><<<dim3(max_tiles, nimg), 128, smem, st>>>(d_descs);

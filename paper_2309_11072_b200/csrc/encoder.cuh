@@ -108,7 +108,9 @@ struct ImgDesc {
   const uint8_t* hdr_post;    // u32 length + header text block
   int hdr_post_len;
   unsigned* status;           // error bits
-  unsigned* amb;              // tone-map samples decided by the fp64 pow (diagnostic)
+  unsigned* amb;              // pixels k_sdr_ycc deferred to k_sdr_fix (their fp32 pow is undecided)
+  unsigned* amb_list;         // [amb_cap] their indices
+  unsigned amb_cap;
 };
 
 constexpr int kMaxBlasThreads = 64;

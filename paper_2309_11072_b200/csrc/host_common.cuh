@@ -57,7 +57,7 @@ struct ImgLayout {
   size_t off_qt, off_taps, off_pre, off_post;
   size_t off_tmnodes, off_scalars;
   size_t off_sdr, off_ycc, off_s, off_zz;
-  size_t off_sstar, off_sstar_tmp, off_e, off_res, off_mstar;
+  size_t off_sstar, off_sstar_tmp, off_e, off_res, off_mstar, off_amb;
   size_t off_tile_hist, off_xs, off_ys, off_bin_start, off_seg_nodes, off_seg_level, off_seg_node_off, off_dot, off_a32,
       off_b32;
   size_t off_crc, off_crc_part;
@@ -146,6 +146,10 @@ inline int ensure(void** p, size_t* cap, size_t need, bool device, bool zero = f
   return 0;
 }
 
+// tone-map pixels k_sdr_ycc may defer to k_sdr_fix (~0.3 % occur; beyond the
+// cap they are decided in place)
+inline long long amb_cap(long long n) { return n / 32 + 1024; }
+
 inline ImgLayout plan(const hdll_b200_image& im, bool trace) {
   ImgLayout L{};
   const long long w = im.width, h = im.height, n = w * h;
@@ -171,6 +175,7 @@ inline ImgLayout plan(const hdll_b200_image& im, bool trace) {
   L.off_sstar = real ? take(sizeof(double) * 3 * n) : 0;
   L.off_sstar_tmp = real ? take(sizeof(double) * 3 * n) : 0;
   L.off_e = take(n + 16);
+  L.off_amb = take(sizeof(unsigned) * (size_t)amb_cap(n));
   L.off_res = take(3 * n + 16);
   L.off_mstar = trace ? take(3 * n) : 0;
   const long long sort_tiles = (n + kSortTile - 1) / kSortTile;
@@ -398,6 +403,8 @@ inline void fill_desc(ImgDesc& d, const hdll_b200_image& im, const ImgLayout& L,
   d.maxlw = (unsigned long long*)(B + L.off_zero);
   d.status = (unsigned*)(B + L.off_zero + 8);
   d.amb = (unsigned*)(B + L.off_zero + 12);
+  d.amb_list = (unsigned*)(B + L.off_amb);
+  d.amb_cap = (unsigned)amb_cap(d.n);
   d.bin_count = (unsigned*)(B + L.off_zero + 16);
   d.sum_y = (long long*)(B + L.off_zero + 16 + 1024);
   d.full_n = d.n;

@@ -18,7 +18,7 @@ idx = {w: hdr.index(w) for w in want if w in hdr}
 SCALE = {"byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3, "Gbyte": 1.0, "ns": 1e-6, "us": 1e-3, "usecond": 1e-3,
          "ms": 1.0, "msecond": 1.0, "nsecond": 1e-6}
 STAGE = {"k_lum_log": "tonemap", "k_tm_nodes": "tonemap", "k_tm_scalars": "tonemap", "k_base_layer": "base",
-         "k_sdr_ycc": "base", "k_prefilter_cols": "prefilter",
+         "k_sdr_ycc": "base", "k_sdr_fix": "base", "k_prefilter_cols": "prefilter",
          "k_prefilter_fused": "prefilter", "k_prefilter_v": "prefilter", "k_prefilter_h": "prefilter",
          "k_sort_hist": "fit", "k_sort_scan": "fit", "k_sort_scatter": "fit", "k_seg_setup": "fit", "k_seg_nodes": "fit",
          "k_seg_dot": "fit", "k_seg_reduce_coef": "fit", "k_estimate": "estimate", "k_crc_chunks": "crc",
