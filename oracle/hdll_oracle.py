@@ -283,7 +283,7 @@ def encode(pixels: np.ndarray, quality: int = 85, sigma: float = 1.0, slrme: boo
     if not 1 <= quality <= 100:
         raise ValueError("quality must be in [1, 100]")
     sigma_milli = int(round(sigma * 1000.0))
-    tmo = dict(key=0.18, white_point=None, gamma=2.2, epsilon=1e-6, **(tmo or {}))
+    tmo = {**dict(key=0.18, white_point=None, gamma=2.2, epsilon=1e-6), **(tmo or {})}
     mants = [pixels[..., c].copy() for c in range(3)]
     e_plane = pixels[..., 3].copy()
 

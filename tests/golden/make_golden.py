@@ -47,7 +47,7 @@ def main() -> int:
     sys.path.insert(0, str(scratch / "pkg" / "src"))
     from threadpoolctl import threadpool_info, threadpool_limits
 
-    from hdll import RadianceImage, container, corpus
+    from hdll import RadianceImage, TmoParams, container, corpus
     from hdll.radiance_io import read_hdr_file
 
     from paper_2309_11072_b200 import synth
@@ -63,9 +63,12 @@ def main() -> int:
         h, w = px.shape[:2]
         img = RadianceImage(w, h, px, list(header_vars), orientation)
         trace: dict = {}
+        rkw = dict(kw)
+        if "tmo" in rkw:  # stored as a plain dict (JSON); the reference takes TmoParams
+            rkw["tmo"] = TmoParams(**rkw["tmo"])
         with threadpool_limits(limits=blas_threads, user_api="blas"):
             try:
-                stream = container.encode(img, trace=trace, **kw)
+                stream = container.encode(img, trace=trace, **rkw)
                 blob = container.serialize(stream)
                 err = None
             except Exception as ex:  # error parity cases
@@ -134,6 +137,11 @@ def main() -> int:
     runs[5, 510:] = (12, 20, 30, 120)
     runs[7, ::2] = (200, 200, 200, 140)
     run("long_runs", runs, [])
+    # tone-map parameters (tonemap.py:22-37): gamma on both sides of the GPU's
+    # MUFU cut-over (1 / gamma = 4), explicit white point, key, epsilon
+    for i, tmo in enumerate([dict(gamma=1.0), dict(gamma=0.2, key=0.36), dict(white_point=2.5, gamma=2.4),
+                             dict(gamma=0.05, epsilon=1e-4), dict(key=0.05, white_point=0.5)]):
+        run(f"tmo_{i}", synth.make_config(0, 200 + i, scale=0.09), [("FORMAT", "32-bit_rle_rgbe")], tmo=tmo)
     # error parity
     run("err_sigma", rng.integers(0, 256, (4, 4, 4), dtype=np.uint8), [], sigma=70.0)
     run("err_quality", rng.integers(0, 256, (4, 4, 4), dtype=np.uint8), [], quality=0)

@@ -132,6 +132,8 @@ def test_encode_matches_reference_golden(case, gpu):
     px = golden_pixels(case, inputs)
     img = _image(gpu, px, case["header_vars"], case["orientation"])
     kw = dict(case["kwargs"])
+    if "tmo" in kw:
+        kw["tmo"] = gpu.TmoParams(**kw["tmo"])
     if case["error"]:
         with pytest.raises(ValueError):
             gpu.encode(img, blas_kernel=max(case["blas_kernel"], 0), blas_threads=case["blas_threads"], **kw)
@@ -235,4 +237,20 @@ def test_wide_rows_match_oracle(w, h, kind, gpu):
     img = _image(gpu, px, [("FORMAT", "32-bit_rle_rgbe")])
     got = gpu.serialize(gpu.encode(img))
     want = O.encode(px, header_vars=[("FORMAT", "32-bit_rle_rgbe")])
+    assert got == want
+
+
+# ---------------------------------------------------------------------------
+# tone-map parameters: the fp32 gamma pass uses MUFU approximations up to
+# 1 / gamma = 4 and the accurate fp32 functions beyond; both defer undecided
+# bytes to the fp64 pow (tonemap.py:80-118)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("tmo", [dict(gamma=1.0), dict(gamma=0.2, key=0.36), dict(white_point=2.5, gamma=2.4),
+                                 dict(gamma=0.05, epsilon=1e-4)])
+def test_tmo_params_match_oracle(tmo, gpu):
+    from paper_2309_11072_b200 import synth
+    px = synth.make_config(0, 3, scale=0.25)
+    img = _image(gpu, px, [("FORMAT", "32-bit_rle_rgbe")])
+    got = gpu.serialize(gpu.encode(img, tmo=gpu.TmoParams(**tmo)))
+    want = O.encode(px, tmo=tmo, header_vars=[("FORMAT", "32-bit_rle_rgbe")])
     assert got == want
