@@ -77,6 +77,15 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return r;
 }
 
+// 1 / x from the MUFU approximation and one Newton step (relative error
+// ~2^-40; x normal and finite)
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = __fma_rn(-x, r, 1.0);
+  return __fma_rn(r, e, r);
+}
+
 // the byte, or -1 when the fp32 value is too close to a rounding boundary
 __device__ __forceinline__ int quantize_pow_fast(double m, float g32, bool approx) {
   if (m >= 1.0) return 255;  // m^g >= 1 clips to 1
@@ -110,9 +119,16 @@ __device__ __forceinline__ bool sdr_pixel(const ImgDesc& d, uint32_t q, double l
   f[1] = ((double)((q >> 8) & 0xFF) + 0.5) * sc;
   f[2] = ((double)((q >> 16) & 0xFF) + 0.5) * sc;
   const double lw = 0.2126 * f[0] + 0.7152 * f[1] + 0.0722 * f[2];
-  const double scaled = d.key * lw / log_avg;
-  const double disp = scaled * (1.0 + scaled / (white * white)) / (1.0 + scaled);
-  const double ratio = lw > 0 ? disp / lw : 0.0;
+  double ratio;
+  if (exact) {  // the reference's fp64 chain, every division correctly rounded
+    const double scaled = d.key * lw / log_avg;
+    const double disp = scaled * (1.0 + scaled / (white * white)) / (1.0 + scaled);
+    ratio = lw > 0 ? disp / lw : 0.0;
+  } else {  // divisions as refined reciprocals (~2^-40): far inside the kAmb window
+    const double scaled = d.key * lw * rcp_nr(log_avg);
+    const double disp = scaled * (1.0 + scaled * rcp_nr(white * white)) * rcp_nr(1.0 + scaled);
+    ratio = lw > 0 ? disp * rcp_nr(lw) : 0.0;
+  }
   bool ok = true;
 #pragma unroll
   for (int c = 0; c < 3; c++) {
