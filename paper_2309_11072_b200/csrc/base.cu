@@ -158,6 +158,16 @@ __device__ __forceinline__ void ycc_bytes(const uint8_t* s3, uint8_t* y, int8_t*
   *cr = (int8_t)clampd(rha(v), -128.0, 127.0);
 }
 
+// _rgb_to_ycc of one pixel as Y | Cb << 8 | Cr << 16.  (An exact-integer form
+// with a tie fallback was measured slower: the fp64 pipe has room here, the
+// integer pipes do not.)
+__device__ __forceinline__ uint32_t ycc_word(const uint8_t* s3) {
+  uint8_t Y;
+  int8_t Cb, Cr;
+  ycc_bytes(s3, &Y, &Cb, &Cr);
+  return (uint32_t)Y | ((uint32_t)(uint8_t)Cb << 8) | ((uint32_t)(uint8_t)Cr << 16);
+}
+
 __global__ void __launch_bounds__(256) k_sdr_ycc(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
   const double log_avg = d.sdr_in ? 1.0 : d.scalars[1], white = d.sdr_in ? 1.0 : d.scalars[2];
@@ -167,19 +177,24 @@ __global__ void __launch_bounds__(256) k_sdr_ycc(const ImgDesc* __restrict__ des
   tc.approx = tc.g32 <= kApproxMaxG;
   const long long nq = (d.n + 3) / 4;
   uint8_t* Yp = d.ycc;
-  int8_t* Cb = reinterpret_cast<int8_t*>(d.ycc + d.n);
-  int8_t* Cr = reinterpret_cast<int8_t*>(d.ycc + 2 * d.n);
+  uint8_t* Cb = d.ycc + d.n;
+  uint8_t* Cr = d.ycc + 2 * d.n;
+  const bool aligned = (d.n & 3) == 0;  // the planes' 4-pixel groups are 4-byte aligned
   // The fit's exponent histogram per 1024-pixel sort tile (fit.cu k_sort_hist)
   // rides along: one pass of this grid-stride loop is exactly one sort tile.
-  __shared__ unsigned hist[256];
+  // Two buffers, one barrier per pass: a thread clears its entry of the next
+  // pass's buffer before the barrier that ends this pass's counting.
+  __shared__ unsigned hist[2][256];
   const bool fuse_hist = d.hist_fused != 0;
   static_assert(kSortTile == 4 * 256, "one k_sdr_ycc block iteration covers one sort tile");
+  if (fuse_hist) {
+    hist[0][threadIdx.x] = 0;
+    __syncthreads();
+  }
+  int buf = 0;
   for (long long qb = (long long)blockIdx.x * blockDim.x; qb < nq; qb += (long long)gridDim.x * blockDim.x) {
     const long long qi = qb + threadIdx.x;
-    if (fuse_hist) {  // (block-uniform branch: every thread reaches both barriers)
-      hist[threadIdx.x] = 0;
-      __syncthreads();
-    }
+    if (fuse_hist) hist[buf ^ 1][threadIdx.x] = 0;
     const long long p0 = qi * 4;
     const int cnt = qi < nq ? (int)min(4LL, d.n - p0) : 0;
     uint32_t qs[4] = {0u, 0u, 0u, 0u};
@@ -191,38 +206,56 @@ __global__ void __launch_bounds__(256) k_sdr_ycc(const ImgDesc* __restrict__ des
         for (int k = 0; k < cnt; k++) qs[k] = reinterpret_cast<const uint32_t*>(d.rgbe)[p0 + k];
       }
     }
-#pragma unroll 1
-    for (int k = 0; k < cnt; k++) {
+    uint32_t yw = 0, cbw = 0, crw = 0;  // the 4 pixels' bytes (a deferred pixel's are written by k_sdr_fix)
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      if (k >= cnt) break;
       const long long p = p0 + k;
       uint8_t s3[3];
+      bool have = true;
       if (d.sdr_in) {
         s3[0] = d.sdr_in[3 * p], s3[1] = d.sdr_in[3 * p + 1], s3[2] = d.sdr_in[3 * p + 2];
-      } else {
-        const uint32_t q = k == 0 ? qs[0] : (k == 1 ? qs[1] : (k == 2 ? qs[2] : qs[3]));
-        if (!sdr_pixel(d, q, log_avg, white, tc, allzero, s3, false)) {
-          // a byte the fp32 pass cannot certify (~0.3 % of samples): the pixel
-          // goes to k_sdr_fix instead of holding its warp through an fp64 pow
-          const unsigned slot = atomicAdd(d.amb, 1u);
-          if (slot < d.amb_cap) {
-            d.amb_list[slot] = (unsigned)p;
-            continue;
-          }
-          sdr_pixel(d, q, log_avg, white, tc, allzero, s3, true);  // list full: here
+      } else if (!sdr_pixel(d, qs[k], log_avg, white, tc, allzero, s3, false)) {
+        // a byte the fp32 pass cannot certify (~0.3 % of samples): the pixel
+        // goes to k_sdr_fix instead of holding its warp through an fp64 pow
+        const unsigned slot = atomicAdd(d.amb, 1u);
+        if (slot < d.amb_cap) {
+          d.amb_list[slot] = (unsigned)p;
+          have = false;
+        } else {
+          sdr_pixel(d, qs[k], log_avg, white, tc, allzero, s3, true);  // list full: here
         }
-        if (d.want_trace) {
+      }
+      if (have) {
+        if (d.want_trace && !d.sdr_in) {
           d.sdr[3 * p] = s3[0];
           d.sdr[3 * p + 1] = s3[1];
           d.sdr[3 * p + 2] = s3[2];
         }
+        const uint32_t w = ycc_word(s3);
+        yw |= (w & 0xFFu) << (8 * k);
+        cbw |= ((w >> 8) & 0xFFu) << (8 * k);
+        crw |= ((w >> 16) & 0xFFu) << (8 * k);
       }
-      ycc_bytes(s3, Yp + p, Cb + p, Cr + p);
+    }
+    if (cnt == 4 && aligned) {
+      reinterpret_cast<uint32_t*>(Yp)[qi] = yw;
+      reinterpret_cast<uint32_t*>(Cb)[qi] = cbw;
+      reinterpret_cast<uint32_t*>(Cr)[qi] = crw;
+    } else {
+      for (int k = 0; k < cnt; k++) {
+        Yp[p0 + k] = (uint8_t)(yw >> (8 * k));
+        Cb[p0 + k] = (uint8_t)(cbw >> (8 * k));
+        Cr[p0 + k] = (uint8_t)(crw >> (8 * k));
+      }
     }
     if (fuse_hist) {
-      for (int k = 0; k < cnt; k++) atomicAdd(&hist[qs[k] >> 24], 1u);
+      for (int k = 0; k < cnt; k++) atomicAdd(&hist[buf][qs[k] >> 24], 1u);
       __syncthreads();
-      const unsigned hc = hist[threadIdx.x];
+      const unsigned hc = hist[buf][threadIdx.x];
       d.tile_hist[(long long)threadIdx.x * d.sort_tiles + qb / 256] = hc;
       if (hc) atomicAdd(&d.bin_count[threadIdx.x], hc);
+      buf ^= 1;
     }
   }
 }

@@ -895,8 +895,19 @@ __device__ __forceinline__ uint32_t slab_symbol(const uint4* slab, int q) {
   return (j & 1) ? (wd >> 16) : (wd & 0xFFFFu);
 }
 
+#ifdef HDLL_PLANE_MINB  // experiment builds: resident CTAs per SM asked of ptxas
+#define HDLL_PLANE_LB 128, HDLL_PLANE_MINB
+#else
+#define HDLL_PLANE_LB 128, 8  // 64 registers, 8 CTAs per SM (-0.12 ms against 72 registers, 7 CTAs)
+#endif
+#ifdef HDLL_DCT_MINB
+#define HDLL_DCT_LB 128, HDLL_DCT_MINB
+#else
+#define HDLL_DCT_LB 128
+#endif
+
 // grid-persistent, 4 warps per CTA, each warp's context state in shared memory
-__global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict__ descs, ChainTab ct, uint4* symbuf,
+__global__ void __launch_bounds__(HDLL_PLANE_LB) k_entropy_plane(const ImgDesc* __restrict__ descs, ChainTab ct, uint4* symbuf,
                                                        int cap_chunks, uint32_t* wordbuf) {
   __shared__ __align__(16) uint8_t smem_pl[4 * lane_state_bytes(5)];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1001,7 +1012,7 @@ __global__ void __launch_bounds__(128) k_entropy_plane(const ImgDesc* __restrict
 // a block's code: <= 544 bytes (dct_chain_cap) = 136 words
 constexpr int kDctScrWords = 136;
 
-__global__ void __launch_bounds__(128) k_entropy_dct(const ImgDesc* __restrict__ descs, ChainTab ct, uint32_t* wordbuf) {
+__global__ void __launch_bounds__(HDLL_DCT_LB) k_entropy_dct(const ImgDesc* __restrict__ descs, ChainTab ct, uint32_t* wordbuf) {
   __shared__ __align__(16) uint8_t smem_dct[4 * lane_state_bytes(3)];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const LaneState ls = carve_state(smem_dct + warp * lane_state_bytes(3), 3);

@@ -9,7 +9,14 @@ from paper_2309_11072_b200 import _native, container
 nimg = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 cfg = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 8
-pix = bench.generate(cfg, list(range(nimg)))
+import os
+cache = f"/tmp/hdll_gen_{cfg}_{nimg}.npy"  # speed-up for repeated A/B runs only
+if os.path.exists(cache):
+    pix = list(np.load(cache))
+else:
+    pix = bench.generate(cfg, list(range(nimg)))
+    if len({p.shape for p in pix}) == 1:
+        np.save(cache, np.stack(pix))
 h, w = pix[0].shape[:2]
 preps = [container.prepare(P.RadianceImage(w, h, p, [("FORMAT", "32-bit_rle_rgbe")])) for p in pix]
 dev = torch.device("cuda", 0)
