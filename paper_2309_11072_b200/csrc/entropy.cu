@@ -651,77 +651,132 @@ struct RowTrack {
   int out_L;
 };
 
-struct PlaneRowGen {
-  static constexpr bool kStaticCtx = false;
-  const uint8_t* cur;   // the lane's row; nullptr: idle lane
-  const uint8_t* prev;  // the row above; nullptr on row 0
-  int x0, x1;           // the segment
-  bool last;            // x1 == width: a run open at x1 ends with the row
-  bool inrun0;          // entry state
-  int L0;               // samples of the entering run so far
-  RowTrack* trk;        // nullptr, or filled in (entered free)
-  // f(index, ctx, value, 0, 0) in coder order.  _neighbors (_kernels.py:131-143):
-  // a = left (above at x = 0, 128 at the origin), b = above (else a),
-  // c = above-left (else b).
-  template <class F>
-  __device__ __forceinline__ void for_each(F&& f) const {
-    if (!cur) return;
-    int i = 0;
-    int a = x0 > 0 ? cur[x0 - 1] : (prev ? __ldg(prev) : 128);
-    int c = x0 > 0 ? (prev ? prev[x0 - 1] : a) : a;  // above-left (the above sample at x = 0)
-    bool inrun = inrun0;
-    int L = L0;
-    int nsamp = 0;
-    if (trk) trk->brk = false;
-    auto run_chunks = [&]() {  // chunks of <= 255; a chunk of 255 continues
-      for (;;) {
-        const int ch = L >= 255 ? 255 : L;
-        f(i++, kRunCtx, ch, 0, 0u);
-        L -= ch;
-        if (ch < 255) break;
+// The count pass keeps each row's symbols (u16: ctx << 8 | value)
+// in a global scratch slab of the warp, interleaved by lane in 16-byte chunks
+// (chunk q of lane l at slab[q * 32 + l]), so the later passes read 8 symbols
+// per coalesced 128-bit access instead of re-deriving them.
+struct SymChunk {  // 8 u16 symbols, shifted in at the top
+  unsigned long long lo = 0, hi = 0;
+  __device__ __forceinline__ void push(uint32_t s) {
+    lo = (lo >> 16) | (hi << 48);
+    hi = (hi >> 16) | ((unsigned long long)s << 48);
+  }
+  __device__ __forceinline__ uint32_t pop() {  // lowest symbol first
+    const uint32_t s = (uint32_t)(lo & 0xFFFFu);
+    lo = (lo >> 16) | (hi << 48);
+    hi >>= 16;
+    return s;
+  }
+  __device__ __forceinline__ void align(int m) {  // m < 8 pushed: move them to the bottom
+    const int sh = 16 * (8 - m);
+    if (sh < 64) {
+      lo = (lo >> sh) | (hi << (64 - sh));
+      hi >>= sh;
+    } else {
+      lo = hi >> (sh - 64);
+      hi = 0;
+    }
+  }
+  __device__ __forceinline__ uint4 word() const {
+    return make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32));
+  }
+  __device__ __forceinline__ void load(const uint4& w) {
+    lo = (unsigned long long)w.x | ((unsigned long long)w.y << 32);
+    hi = (unsigned long long)w.z | ((unsigned long long)w.w << 32);
+  }
+};
+
+// The count pass of one segment entered free (_kernels.py:169-216 from a free
+// state): every symbol (ctx << 8 | value) into the lane's slab, symbols per
+// context, and the RowTrack facts.  _neighbors (_kernels.py:131-143): a = left
+// (above at x = 0, 128 at the origin), b = above (else a), c = above-left (else b).
+// Samples go four to a 32-bit word with the byte loop unrolled; the regular
+// contexts' counts are 8-bit fields of one word, folded out every 16 samples.
+// ctx of the activity g = |a - c| + |c - b| (_activity_ctx, _kernels.py:157-166):
+// 2-bit fields of kCtxTab indexed by min(g, 9): 0 -> 0, 1-2 -> 1, 3-8 -> 2, 9+ -> 3
+constexpr uint32_t kCtxTab = (1u << 2) | (1u << 4) | (2u << 6) | (2u << 8) | (2u << 10) | (2u << 12) | (2u << 14) |
+                             (2u << 16) | (3u << 18);
+
+struct SegGen {
+  int a, c;           // left and above-left neighbours of the next sample
+  bool inrun;
+  int L;
+  int i;              // symbols so far
+  SymChunk ch;
+  uint4* sp;          // the slab chunk being filled
+  uint32_t cpk;       // regular contexts' counts, 8 bits each (< 256 between folds)
+  int cnt[5];
+  // RowTrack
+  bool brk;
+  int cov, brk_i, nsamp;
+
+  __device__ __forceinline__ void put(int ctx, int v) {
+    ch.push((uint32_t)((ctx << 8) | v));
+    if ((i & 7) == 7) {
+      *sp = ch.word();
+      sp += 32;
+    }
+    i++;
+  }
+  __device__ __forceinline__ void fold() {
+    cnt[0] += cpk & 0xFF;
+    cnt[1] += (cpk >> 8) & 0xFF;
+    cnt[2] += (cpk >> 16) & 0xFF;
+    cnt[3] += cpk >> 24;
+    cpk = 0;
+  }
+  __device__ __forceinline__ void run_chunks() {  // chunks of <= 255; a chunk of 255 continues
+    for (;;) {
+      const int chn = L >= 255 ? 255 : L;
+      put(kRunCtx, chn);
+      cnt[kRunCtx]++;
+      L -= chn;
+      if (chn < 255) break;
+    }
+  }
+  // one sample (hp: a row above exists; track: record the first break)
+  __device__ __forceinline__ void sample(int xv, int braw, bool hp, bool track) {
+    const int b = hp ? braw : a;
+    const int cc = hp ? c : a;
+    const bool E = xv == a;
+    if (!inrun && a == b && b == cc) {  // run mode (not forced, a == b == c)
+      inrun = true;
+      L = 0;
+    }
+    if (inrun && E) {
+      L++;
+    } else {
+      if (inrun) {  // the run ends: its chunks, then this sample is forced regular
+        run_chunks();
+        inrun = false;
       }
-    };
-    auto sample = [&](int xv, int braw) {
-      const int b = prev ? braw : a;
-      const int cc = prev ? c : a;
-      const bool E = xv == a;
-      if (!inrun && a == b && b == cc) {  // run mode (not forced, a == b == c)
-        inrun = true;
-        L = 0;
-      }
-      bool regular = true;
-      if (inrun) {
-        if (E) {
-          L++;
-          regular = false;
-        } else {  // the run ends: its chunks, then this sample is forced regular
-          run_chunks();
-          inrun = false;
-        }
-      }
-      if (regular) {  // MED prediction, activity context, folded residual (_kernels.py:146-166)
-        const int mx = max(a, b), mn = min(a, b);
-        const int pred = cc >= mx ? mn : (cc <= mn ? mx : a + b - cc);
-        const int gg = abs(a - cc) + abs(cc - b);
-        const int ctx = gg == 0 ? 0 : (gg <= 2 ? 1 : (gg <= 8 ? 2 : 3));
-        int r = (xv - pred) & 255;
-        if (r > 127) r -= 256;
-        f(i++, ctx, r >= 0 ? 2 * r : -2 * r - 1, 0, 0u);
-      }
-      if (trk && !E && !trk->brk) {
-        trk->brk = true;
-        trk->cov = nsamp;
-        trk->brk_i = i;
-      }
-      nsamp++;
-      c = b;
-      a = xv;
-    };
-    // 16 samples per 128-bit load when the rows are aligned: one L1 wavefront
-    // per lane per 16 samples instead of one per sample (x0 is a multiple of 16)
-    const uint8_t* pv = prev ? prev : cur;
+      // MED = median(a, b, a + b - c) (_med, _kernels.py:146-154), folded residual
+      const int mx = max(a, b), mn = min(a, b);
+      const int pred = max(mn, min(mx, a + b - cc));
+      const int gg = min(abs(a - cc) + abs(cc - b), 9);
+      const int ctx = (int)((kCtxTab >> (2 * gg)) & 3u);
+      cpk += 1u << (8 * ctx);
+      const int t = (xv - pred) << 24;  // r = (x - pred) mod 256 as a signed byte, << 24
+      put(ctx, (t >> 23) ^ (t >> 31));   // r >= 0 ? 2r : -2r - 1
+    }
+    if (track && !E && !brk) {
+      brk = true;
+      cov = nsamp;
+      brk_i = i;
+    }
+    nsamp++;
+    c = b;
+    a = xv;
+  }
+  // [x0, x1) of row `cur` (prev: the row above, or nullptr); with `track` the
+  // RowTrack facts are recorded
+  __device__ __forceinline__ void run(const uint8_t* cur, const uint8_t* prev, int x0, int x1, bool track) {
+    const bool hp = prev != nullptr;
+    const uint8_t* pv = hp ? prev : cur;
     int x = x0;
+    // 16 samples per 128-bit load when the rows are aligned (x0 is a multiple of 16)
     if (((reinterpret_cast<uintptr_t>(cur + x0) | reinterpret_cast<uintptr_t>(pv + x0)) & 15) == 0) {
+#pragma unroll 1
       for (; x + 16 <= x1; x += 16) {
         const uint4 c4 = __ldg(reinterpret_cast<const uint4*>(cur + x));
         const uint4 p4 = __ldg(reinterpret_cast<const uint4*>(pv + x));
@@ -731,20 +786,19 @@ struct PlaneRowGen {
           uint32_t pw = q == 0 ? p4.x : (q == 1 ? p4.y : (q == 2 ? p4.z : p4.w));
 #pragma unroll 1
           for (int k = 0; k < 4; k++) {
-            sample((int)(cw & 0xFF), (int)(pw & 0xFF));
+            sample((int)(cw & 0xFF), (int)(pw & 0xFF), hp, track);
             cw >>= 8;
             pw >>= 8;
           }
         }
+        fold();
       }
     }
-    for (; x < x1; x++) sample(__ldg(cur + x), __ldg(pv + x));
-    if (trk) {
-      trk->out_in = inrun;
-      trk->out_L = L;
-      if (!trk->brk) trk->cov = nsamp;
+#pragma unroll 1
+    for (; x < x1; x++) {
+      sample(__ldg(cur + x), __ldg(pv + x), hp, track);
+      fold();
     }
-    if (inrun && last) run_chunks();  // a run reaching the row end
   }
 };
 
@@ -816,41 +870,13 @@ __host__ __device__ __forceinline__ int plane_seg_width(int w, int segw) {  // m
   return ((w + s - 1) / s + 15) / 16 * 16;
 }
 
-// The count pass keeps each row's symbols (u16: k << 11 | ctx << 8 | value)
-// in a global scratch slab of the warp, interleaved by lane in 16-byte chunks
-// (chunk q of lane l at slab[q * 32 + l]), so the later passes read 8 symbols
-// per coalesced 128-bit access instead of re-deriving them; the length pass
-// stores each symbol's Rice parameter k for the emit pass.
-struct SymChunk {  // 8 u16 symbols, shifted in at the top
-  unsigned long long lo = 0, hi = 0;
-  __device__ __forceinline__ void push(uint32_t s) {
-    lo = (lo >> 16) | (hi << 48);
-    hi = (hi >> 16) | ((unsigned long long)s << 48);
-  }
-  __device__ __forceinline__ uint32_t pop() {  // lowest symbol first
-    const uint32_t s = (uint32_t)(lo & 0xFFFFu);
-    lo = (lo >> 16) | (hi << 48);
-    hi >>= 16;
-    return s;
-  }
-  __device__ __forceinline__ void align(int m) {  // m < 8 pushed: move them to the bottom
-    const int sh = 16 * (8 - m);
-    if (sh < 64) {
-      lo = (lo >> sh) | (hi << (64 - sh));
-      hi >>= sh;
-    } else {
-      lo = hi >> (sh - 64);
-      hi = 0;
-    }
-  }
-  __device__ __forceinline__ uint4 word() const {
-    return make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32));
-  }
-  __device__ __forceinline__ void load(const uint4& w) {
-    lo = (unsigned long long)w.x | ((unsigned long long)w.y << 32);
-    hi = (unsigned long long)w.z | ((unsigned long long)w.w << 32);
-  }
-};
+// symbol q of a lane's slab
+__device__ __forceinline__ uint32_t slab_symbol(const uint4* slab, int q) {
+  const uint4 w = slab[(q >> 3) * 32];
+  const int j = q & 7;
+  const uint32_t wd = j < 2 ? w.x : (j < 4 ? w.y : (j < 6 ? w.z : w.w));
+  return (j & 1) ? (wd >> 16) : (wd & 0xFFFFu);
+}
 
 // A lane's symbols: the slab's [start, n), after (for a segment entered inside
 // a run) the run's chunks of run_len samples and the symbol `head` (>= 0) of the
@@ -887,13 +913,6 @@ struct PlaneBufGen {
   }
 };
 
-// symbol q of a lane's slab
-__device__ __forceinline__ uint32_t slab_symbol(const uint4* slab, int q) {
-  const uint4 w = slab[(q >> 3) * 32];
-  const int j = q & 7;
-  const uint32_t wd = j < 2 ? w.x : (j < 4 ? w.y : (j < 6 ? w.z : w.w));
-  return (j & 1) ? (wd >> 16) : (wd & 0xFFFFu);
-}
 
 #ifdef HDLL_PLANE_MINB  // experiment builds: resident CTAs per SM asked of ptxas
 #define HDLL_PLANE_LB 128, HDLL_PLANE_MINB
@@ -941,28 +960,33 @@ __global__ void __launch_bounds__(HDLL_PLANE_LB) k_entropy_plane(const ImgDesc* 
     int cnt[5] = {0, 0, 0, 0, 0};
     int n = 0;
     if (live) {
-      PlaneRowGen gen{cur, prev, x0, x1, x1 == d.w, false, 0, S > 1 ? &trk : nullptr};
-      // counts per context (two 32-bit fields per word for the regular contexts)
-      unsigned long long p01 = 0, p23 = 0;
-      int c4 = 0;
-      SymChunk ch;
-      gen.for_each([&](int i, int c, int v, int, uint32_t) {
-        if (c == kRunCtx) c4++;
-        else if (c < 2) p01 += 1ULL << (32 * c);
-        else p23 += 1ULL << (32 * (c - 2));
-        ch.push((uint32_t)((c << 8) | v));
-        if ((i & 7) == 7) slab[(i >> 3) * 32] = ch.word();
-        n = i + 1;
-      });
+      SegGen sg_;
+      sg_.a = x0 > 0 ? cur[x0 - 1] : (prev ? __ldg(prev) : 128);
+      sg_.c = x0 > 0 ? (prev ? prev[x0 - 1] : sg_.a) : sg_.a;  // above-left (the above sample at x = 0)
+      sg_.inrun = false;
+      sg_.L = 0;
+      sg_.i = 0;
+      sg_.sp = slab;
+      sg_.cpk = 0;
+#pragma unroll
+      for (int c = 0; c < 5; c++) sg_.cnt[c] = 0;
+      sg_.brk = false;
+      sg_.cov = sg_.brk_i = sg_.nsamp = 0;
+      const bool track = S > 1;
+      sg_.run(cur, prev, x0, x1, track);
+      trk.brk = sg_.brk;
+      trk.cov = sg_.brk ? sg_.cov : x1 - x0;
+      trk.brk_i = sg_.brk_i;
+      trk.out_in = sg_.inrun;
+      trk.out_L = sg_.L;
+      if (sg_.inrun && x1 == d.w) sg_.run_chunks();  // a run reaching the row end
+      n = sg_.i;
       if (n & 7) {
-        ch.align(n & 7);
-        slab[(n >> 3) * 32] = ch.word();
+        sg_.ch.align(n & 7);
+        *sg_.sp = sg_.ch.word();
       }
-      cnt[0] = (int)(p01 & 0xFFFFFFFFu);
-      cnt[1] = (int)(p01 >> 32);
-      cnt[2] = (int)(p23 & 0xFFFFFFFFu);
-      cnt[3] = (int)(p23 >> 32);
-      cnt[4] = c4;
+#pragma unroll
+      for (int c = 0; c < 5; c++) cnt[c] = sg_.cnt[c];
     }
     PlaneBufGen gen{slab, n, 0, -1, -1};
     if (S > 1) {
