@@ -199,7 +199,7 @@ __device__ __forceinline__ uint32_t rice_bits(int u, int k) {
   int q = u >> k;
   if (q < kRiceEscapeQ) {
     // q ones, a zero, k remainder bits
-    uint32_t ones = (q == 0) ? 0u : (((1u << q) - 1u) << (k + 1));
+    const uint32_t ones = ((1u << q) - 1u) << (k + 1);  // q + 1 + k <= 32 for u <= 255
     return ones | ((uint32_t)u & ((1u << k) - 1u));
   }
   return (((1u << kRiceEscapeQ) - 1u) << 8) | ((uint32_t)u & 0xFFu);

@@ -508,23 +508,23 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
       }
     });
   } else {
+    // (A, N) of a context packed as A | N << 16 in one shared word (A < 2^15)
+#pragma unroll
+    for (int c = 0; c < NL; c++) ls.a[c * 32 + lane] = a_start[c] | (n0[c] << 16);
+    int nb32 = 0;
     gen.for_each([&](int, int c, int v, int xl, uint32_t xb) {
       const int o = c * 32 + lane;
-      int a = ls.a[o], nb = ls.nn[o];
-      const int k = kfast(a, nb);
+      int st = ls.a[o];
+      const int k = kfast(st & 0xFFFF, st >> 16);
       const int rl = rice_len(v, k);
-      nbits += rl + xl;
+      nb32 += rl + xl;
       sb.put(rice_bits(v, k), rl);
       if (xl) sb.put(xb, xl);
-      a += v;  // _update_state
-      nb += 1;
-      if (nb >= kStateReset) {
-        a >>= 1;
-        nb >>= 1;
-      }
-      ls.a[o] = a;
-      ls.nn[o] = nb;
+      st += v + (1 << 16);  // _update_state: A += u, N += 1; at N = 64 both halve
+      if (st >= (kStateReset << 16)) st = (st >> 1) & ~0x8000;
+      ls.a[o] = st;
     });
+    nbits = nb32;
   }
   sb.flush();
   if (sb.n > scr_cap) atomicOr(status, kErrCapacity);
