@@ -177,6 +177,7 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
     any_real |= (d.slrme && d.sigma_milli != 0);
     any_slrme |= d.slrme != 0;
   }
+  const long long crc_units = crc_assign_units(ds.data(), n);
   memcpy(H + t_descs, ds.data(), sizeof(ImgDesc) * n);
   memset(H + t_ticket, 0, 16);
   for (int i = 0; i < n; i++) zero_ptrs[i] = A + base[i] + lays[i].off_zero;
@@ -225,7 +226,7 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
     c->launches += 1;
   }
   mark(kStEstimate);
-  launch_crc(dd, n, max_n, st);
+  launch_crc(dd, n, crc_units, st);
   c->launches += 2;
   mark(kStCrc);
   if (ct_dct.ntiles > 0) {
@@ -354,6 +355,7 @@ int run_decode(Ctx* c, const hdll_b200_decode_image* imgs, int n, uint8_t* const
     any_real |= d.slrme && d.sigma_milli;
     all_sdr &= di.sdr_only != 0;
   }
+  const long long crc_units = crc_assign_units(ds.data(), n);
   memcpy(H + t_descs, ds.data(), sizeof(ImgDesc) * n);
   CK(cudaMemcpyAsync(D, H, so, cudaMemcpyHostToDevice, st));
   for (int i = 0; i < n; i++) {
@@ -370,7 +372,7 @@ int run_decode(Ctx* c, const hdll_b200_decode_image* imgs, int n, uint8_t* const
     c->launches += 1;
   }
   launch_decode_output(dd, n, max_n, st);
-  launch_crc(dd, n, max_n, st);
+  launch_crc(dd, n, crc_units, st);
   c->launches += 3;
   CK(cudaGetLastError());
   CK(cudaEventRecord(c->slot_ev[slot], st));

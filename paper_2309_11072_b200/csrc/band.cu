@@ -51,6 +51,7 @@ struct Band {
   void* asmb = nullptr;  // rank-0 assembly
   size_t asmb_cap = 0;
   ImgDesc* d_desc = nullptr;
+  long long crc_units = 0;
   double* d_nodes = nullptr;
   uint8_t* piece_ptr[kPieces] = {};
   HostChains hc_dct, hc_pln;
@@ -250,6 +251,7 @@ int hdll_b200_band_begin(hdll_b200_ctx* ctx, const hdll_b200_image* img, const h
   d.hist_fused = 0;  // the band's fit rows are a sub-range: k_sort_hist counts them
   d.crc_p0 = d.fit_p0;
   d.crc_np = d.fit_m;
+  b->crc_units = crc_assign_units(&d, 1);
   b->d_desc = (ImgDesc*)(D + t_desc);
   b->d_nodes = d.tm_nodes;
   b->d_ticket = (int*)(D + t_ticket);
@@ -455,7 +457,7 @@ int hdll_b200_band_code(hdll_b200_ctx* ctx, const float* h_a32, const float* h_b
   CK(cudaMemcpyAsync(d.a32, h_a32, 4 * 768, cudaMemcpyHostToDevice, b->st));
   CK(cudaMemcpyAsync(d.b32, h_b32, 4 * 768, cudaMemcpyHostToDevice, b->st));
   launch_estimate(b->d_desc, 1, d.n, b->st);
-  launch_crc(b->d_desc, 1, d.n, b->st);
+  launch_crc(b->d_desc, 1, b->crc_units, b->st);
   c->launches += 3;
   CK(cudaMemcpyAsync(h_crc, d.crc, 4 * 5, cudaMemcpyDeviceToHost, b->st));
   if (int rc = run_chains(c, b, 1)) return rc;

@@ -4,8 +4,9 @@
 // produce: the decoded interleaved RGB image for the base layer
 // (codec_core.py:533) and the raw plane for each lossless payload (:313).
 // Parallel form: every chunk (1 KiB of a plane, 256 pixels of the interleaved
-// image) is CRC'd by one warp (slice-by-4 tables in shared memory, one piece
-// per lane, pieces merged in-warp), then chunks are merged with zlib's
+// image) is CRC'd by one thread, slice-by-4 with each lane reading its own
+// copy of the tables held in its own shared-memory bank (no bank conflicts:
+// 128 KB, one 1024-thread CTA per SM), then chunks are merged with zlib's
 // crc32_combine algebra: crc(A||B) = x^(8|B|) * crc(A) + crc(B) over GF(2) mod P.
 #include <cstring>
 
@@ -13,7 +14,7 @@
 
 namespace hdll {
 
-__constant__ uint32_t c_crc_tab[4][256];
+__device__ uint32_t c_crc_tab[4][256];  // global, not __constant__: staged with divergent indices
 __constant__ uint32_t c_x2n[32];  // x^(2^k) mod P, zlib x2n_table
 
 __device__ __forceinline__ uint32_t x2nmodp(unsigned long long n, unsigned k) {
@@ -32,112 +33,120 @@ __device__ __forceinline__ uint32_t crc_combine(uint32_t a, uint32_t b, unsigned
 
 // job j of an image: 0 = decoded RGB interleaved (from S planes), 1 = E, 2..4 = residuals
 // (over desc pixels [crc_p0, crc_p0 + crc_np): the whole image, or a row band's own rows)
-__device__ __forceinline__ long long crc_job_len(const ImgDesc& d, int j) { return j == 0 ? 3 * d.crc_np : d.crc_np; }
+__host__ __device__ __forceinline__ long long crc_job_len(const ImgDesc& d, int j) { return j == 0 ? 3 * d.crc_np : d.crc_np; }
 
-// A chunk is the bytes of one warp: 32 lanes x kCrcLaneBytes[j] contiguous
-// bytes (8 whole pixels = 24 bytes for the interleaved job, 32 bytes of a
-// plane).  Lanes CRC their pieces, then the warp merges them in log2(32)
-// steps with crc(A||B) = x^(8|B|) crc(A) + crc(B); multiplying by the fixed
-// x^(8 P 2^k) is a GF(2)-linear map applied through four 256-entry tables.
-constexpr int kCrcLaneBytesRgb = kCrcChunkRgb / 32, kCrcLaneBytesPlane = kCrcChunk / 32;
-__host__ __device__ __forceinline__ long long crc_lane_bytes(int j) { return j == 0 ? kCrcLaneBytesRgb : kCrcLaneBytesPlane; }
-__host__ __device__ __forceinline__ long long crc_chunk_bytes(int j) { return 32 * crc_lane_bytes(j); }
+__host__ __device__ __forceinline__ long long crc_chunk_bytes(int j) { return j == 0 ? kCrcChunkRgb : kCrcChunk; }
 
-__device__ uint32_t c_shift_tab[2][5][4][256];  // [rgb / plane][k][byte][value]: times x^(8 P 2^k)
-
-__device__ __forceinline__ uint32_t crc_bytes(const uint32_t (*tab)[256], uint32_t c, const uint8_t* p, int n) {
-  for (int i = 0; i < n; i++) c = tab[0][(c ^ p[i]) & 0xFF] ^ (c >> 8);
-  return c;
+__host__ __device__ __forceinline__ long long crc_job_chunks(const ImgDesc& d, int j) {
+  return (crc_job_len(d, j) + crc_chunk_bytes(j) - 1) / crc_chunk_bytes(j);
 }
 
-__global__ void __launch_bounds__(256) k_crc_chunks(const ImgDesc* __restrict__ descs) {
-  const ImgDesc& d = descs[blockIdx.y];
-  const int job = blockIdx.z;
-  if (!((d.crc_mask >> job) & 1)) return;
-  __shared__ uint32_t tab[4][256];
-  __shared__ uint32_t sht[5][4][256];
-  const int kind = job == 0 ? 0 : 1;
-  for (int i = threadIdx.x; i < 1024; i += blockDim.x) (&tab[0][0])[i] = (&c_crc_tab[0][0])[i];
-  for (int i = threadIdx.x; i < 5 * 1024; i += blockDim.x) (&sht[0][0][0])[i] = (&c_shift_tab[kind][0][0][0])[i];
+long long crc_assign_units(ImgDesc* ds, int n) {
+  long long u = 0;
+  for (int i = 0; i < n; i++) {
+    ds[i].crc_u0 = u;
+    for (int j = 0; j < 5; j++)
+      if ((ds[i].crc_mask >> j) & 1) u += crc_job_chunks(ds[i], j);
+  }
+  return u;
+}
+
+constexpr int kCrcThreads = 1024;
+constexpr size_t kCrcTabSmem = 4 * 256 * 32 * sizeof(uint32_t);  // [table][entry][lane]
+
+// slice-by-4 on a lane's private tables (T = tabs + lane, entry stride 32 words)
+__device__ __forceinline__ uint32_t crc_slice4(const uint32_t* T, uint32_t c, uint32_t w) {
+  w ^= c;
+  return T[(3 * 256 + (w & 0xFF)) * 32] ^ T[(2 * 256 + ((w >> 8) & 0xFF)) * 32] ^ T[(256 + ((w >> 16) & 0xFF)) * 32] ^
+         T[(w >> 24) * 32];
+}
+__device__ __forceinline__ uint32_t crc_byte(const uint32_t* T, uint32_t c, uint32_t b) {
+  return T[((c ^ b) & 0xFF) * 32] ^ (c >> 8);
+}
+
+// One work unit = one chunk of one job of one image, numbered through the
+// batch (crc_u0); lane l of a warp takes unit 32 k + l, so whatever the image
+// sizes every thread gets about the same number of bytes.
+__global__ void __launch_bounds__(kCrcThreads, 1) k_crc_chunks(const ImgDesc* __restrict__ descs, int nimg, long long units) {
+  extern __shared__ uint32_t tabs[];
+  for (int i = threadIdx.x; i < 4 * 256 * 32; i += blockDim.x) tabs[i] = (&c_crc_tab[0][0])[i >> 5];
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const long long len = crc_job_len(d, job);
-  const long long csz = crc_chunk_bytes(job), lb = crc_lane_bytes(job);
-  const long long nch = (len + csz - 1) / csz;
-  const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
-  auto slice4 = [&](uint32_t c, uint32_t w) {
-    w ^= c;
-    return tab[3][w & 0xFF] ^ tab[2][(w >> 8) & 0xFF] ^ tab[1][(w >> 16) & 0xFF] ^ tab[0][w >> 24];
-  };
-  const uint8_t* R = d.s_planes + d.crc_p0;
-  const uint8_t* G = d.s_planes + d.n + d.crc_p0;
-  const uint8_t* B = d.s_planes + 2 * d.n + d.crc_p0;
-  const uint8_t* src = job == 0 ? nullptr : (job == 1 ? d.e_plane : d.res_planes + (long long)(job - 2) * d.n) + d.crc_p0;
-  for (long long chunk = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); chunk < nch; chunk += wstride) {
-    const long long b0 = chunk * csz;
-    if (b0 + csz > len) {  // the job's last, partial chunk: one lane, byte by byte
-      if (lane == 0) {
-        uint32_t c = 0xFFFFFFFFu;
-        if (job == 0) {
-          for (long long p = b0 / 3; p < len / 3; p++) {
-            const uint8_t px[3] = {R[p], G[p], B[p]};
-            c = crc_bytes(tab, c, px, 3);
-          }
-        } else {
-          c = crc_bytes(tab, c, src + b0, (int)(len - b0));
-        }
-        d.crc_part[d.crc_part_off[job] + chunk] = c ^ 0xFFFFFFFFu;
-      }
-      continue;
+  const uint32_t* T = tabs + lane;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long ub = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; ub < units; ub += nw * 32) {
+    const long long u = ub + lane;
+    if (u >= units) break;
+    int lo = 0, hi = nimg;  // the image holding unit u: last crc_u0 <= u
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (descs[mid].crc_u0 <= u) lo = mid; else hi = mid;
     }
+    const ImgDesc& d = descs[lo];
+    long long chunk = u - d.crc_u0;
+    int job = 0;
+    for (; job < 5; job++) {
+      if (!((d.crc_mask >> job) & 1)) continue;
+      const long long nch = crc_job_chunks(d, job);
+      if (chunk < nch) break;
+      chunk -= nch;
+    }
+    if (job == 5) continue;  // (not reached: units are exact)
+    const long long len = crc_job_len(d, job), csz = crc_chunk_bytes(job);
+    const long long b0 = chunk * csz, nb = min(csz, len - b0);
     uint32_t c = 0xFFFFFFFFu;
-    const long long o = b0 + lane * lb;
-    if (job == 0) {  // 8 pixels: 3 plane words each, interleaved r g b
-      const long long p = o / 3;
-      uint32_t r[2], g[2], bb[2];
+    if (job == 0) {  // interleaved r g b of pixels [p0, p0 + nb / 3)
+      const uint8_t* R = d.s_planes + d.crc_p0;
+      const uint8_t* G = R + d.n;
+      const uint8_t* B = G + d.n;
+      const long long p0 = b0 / 3, np = nb / 3;
+      long long p = p0;
+      if (((reinterpret_cast<uintptr_t>(R + p0) | reinterpret_cast<uintptr_t>(G + p0) | reinterpret_cast<uintptr_t>(B + p0)) & 15) == 0) {
+#pragma unroll 1
+        for (; p + 16 <= p0 + np; p += 16) {
+          const uint4 r4 = *reinterpret_cast<const uint4*>(R + p), g4 = *reinterpret_cast<const uint4*>(G + p),
+                      b4 = *reinterpret_cast<const uint4*>(B + p);
+          const uint32_t rr[4] = {r4.x, r4.y, r4.z, r4.w}, gg[4] = {g4.x, g4.y, g4.z, g4.w}, bb[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
-      for (int h = 0; h < 2; h++) {
-        memcpy(&r[h], R + p + 4 * h, 4);
-        memcpy(&g[h], G + p + 4 * h, 4);
-        memcpy(&bb[h], B + p + 4 * h, 4);
+          for (int h = 0; h < 4; h++) {
+            const uint32_t r = rr[h], g = gg[h], b = bb[h];
+            // little-endian words of the byte stream r0 g0 b0 r1 | g1 b1 r2 g2 | b2 r3 g3 b3
+            c = crc_slice4(T, c, __byte_perm(__byte_perm(r, g, 0x1040), b, 0x3410));
+            c = crc_slice4(T, c, __byte_perm(__byte_perm(g, b, 0x2051), r, 0x3610));
+            c = crc_slice4(T, c, __byte_perm(__byte_perm(b, r, 0x3072), g, 0x3710));
+          }
+        }
       }
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const uint32_t r4 = r[h], g4 = g[h], b4 = bb[h];
-        // little-endian words of the byte stream r0 g0 b0 r1 | g1 b1 r2 g2 | b2 r3 g3 b3
-        c = slice4(c, (r4 & 0xFF) | ((g4 & 0xFF) << 8) | ((b4 & 0xFF) << 16) | (((r4 >> 8) & 0xFF) << 24));
-        c = slice4(c, ((g4 >> 8) & 0xFF) | (((b4 >> 8) & 0xFF) << 8) | (((r4 >> 16) & 0xFF) << 16) |
-                          (((g4 >> 16) & 0xFF) << 24));
-        c = slice4(c, ((b4 >> 16) & 0xFF) | ((r4 >> 24) << 8) | ((g4 >> 24) << 16) | ((b4 >> 24) << 24));
+      for (; p < p0 + np; p++) {
+        c = crc_byte(T, c, R[p]);
+        c = crc_byte(T, c, G[p]);
+        c = crc_byte(T, c, B[p]);
       }
     } else {
-      uint32_t w[8];
-      const uint8_t* q = src + o;
+      const uint8_t* q = (job == 1 ? d.e_plane : d.res_planes + (long long)(job - 2) * d.n) + d.crc_p0 + b0;
+      long long k = 0;
       if ((reinterpret_cast<uintptr_t>(q) & 15) == 0) {
-        const uint4 v0 = *reinterpret_cast<const uint4*>(q), v1 = *reinterpret_cast<const uint4*>(q + 16);
-        w[0] = v0.x, w[1] = v0.y, w[2] = v0.z, w[3] = v0.w, w[4] = v1.x, w[5] = v1.y, w[6] = v1.z, w[7] = v1.w;
-      } else {
-#pragma unroll
-        for (int k = 0; k < 8; k++) memcpy(&w[k], q + 4 * k, 4);
+#pragma unroll 2
+        for (; k + 16 <= nb; k += 16) {
+          const uint4 v = *reinterpret_cast<const uint4*>(q + k);
+          c = crc_slice4(T, c, v.x);
+          c = crc_slice4(T, c, v.y);
+          c = crc_slice4(T, c, v.z);
+          c = crc_slice4(T, c, v.w);
+        }
       }
-#pragma unroll
-      for (int k = 0; k < 8; k++) c = slice4(c, w[k]);
+      for (; k < nb; k++) c = crc_byte(T, c, q[k]);
     }
-    c ^= 0xFFFFFFFFu;
-    // merge: at step k, lanes 2^(k+1) i hold the CRC of 2^k pieces, their right
-    // neighbours the next 2^k pieces
-#pragma unroll
-    for (int k = 0; k < 5; k++) {
-      const uint32_t right = __shfl_down_sync(0xffffffffu, c, 1 << k);
-      if ((lane & ((2 << k) - 1)) == 0)
-        c = sht[k][0][c & 0xFF] ^ sht[k][1][(c >> 8) & 0xFF] ^ sht[k][2][(c >> 16) & 0xFF] ^ sht[k][3][c >> 24] ^ right;
-    }
-    if (lane == 0) d.crc_part[d.crc_part_off[job] + chunk] = c;
+    d.crc_part[d.crc_part_off[job] + chunk] = c ^ 0xFFFFFFFFu;
   }
 }
 
-// one CTA (1024 threads) per (image, job): sequential runs then a tree
-__global__ void __launch_bounds__(1024) k_crc_combine(const ImgDesc* __restrict__ descs) {
+// One CTA (256 threads) per (image, job): each thread folds a run of `per`
+// chunk CRCs (whole chunks through byte tables of x^(8 csz)), then a tree over
+// the threads, whose regular right halves (per csz 2^s bytes) shift by a
+// per-level constant.
+constexpr int kCrcCombineThreads = 256;
+__global__ void __launch_bounds__(kCrcCombineThreads) k_crc_combine(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
   const int job = blockIdx.x;
   if (!((d.crc_mask >> job) & 1)) return;
@@ -145,31 +154,50 @@ __global__ void __launch_bounds__(1024) k_crc_combine(const ImgDesc* __restrict_
   const long long csz = crc_chunk_bytes(job);
   const long long nch = (len + csz - 1) / csz;
   const uint32_t* part = d.crc_part + d.crc_part_off[job];
-  const int nt = blockDim.x, t = threadIdx.x;
-  __shared__ uint32_t scrc[1024];
-  __shared__ unsigned long long slen[1024];
+  constexpr int nt = kCrcCombineThreads;
+  constexpr int kLevels = 8;  // log2(nt)
+  const int t = threadIdx.x;
+  __shared__ uint32_t scrc[nt];
+  __shared__ unsigned long long slen[nt];
+  __shared__ uint32_t xch[4][256];    // times x^(8 csz) (one whole chunk), as byte tables
+  __shared__ uint32_t xlev[kLevels];  // times x^(8 per csz 2^s)
+  __shared__ uint32_t xfull_s;
   const long long per = (nch + nt - 1) / nt;
+  if (t < kLevels) xlev[t] = x2nmodp((unsigned long long)(per * csz) << t, 3);
+  if (t == kLevels) xfull_s = x2nmodp((unsigned long long)csz, 3);
+  __syncthreads();
+  {
+    const uint32_t xfull = xfull_s;
+    for (int i = t; i < 1024; i += nt) xch[i >> 8][i & 255] = crc_multmodp(xfull, (uint32_t)(i & 255) << (8 * (i >> 8)));
+  }
+  __syncthreads();
   const long long c0 = (long long)t * per, c1 = min(nch, c0 + per);
   uint32_t acc = 0;
   unsigned long long alen = 0;
   if (c0 < c1) {
-    const uint32_t xfull = x2nmodp((unsigned long long)csz, 3);
     acc = part[c0];
     alen = (unsigned long long)min(csz, len - c0 * csz);
     for (long long k = c0 + 1; k < c1; k++) {
       unsigned long long l = (unsigned long long)min(csz, len - k * csz);
-      uint32_t xp = (l == (unsigned long long)csz) ? xfull : x2nmodp(l, 3);
-      acc = crc_multmodp(xp, acc) ^ part[k];
+      if (l == (unsigned long long)csz)
+        acc = xch[0][acc & 0xFF] ^ xch[1][(acc >> 8) & 0xFF] ^ xch[2][(acc >> 16) & 0xFF] ^ xch[3][acc >> 24] ^ part[k];
+      else
+        acc = crc_multmodp(x2nmodp(l, 3), acc) ^ part[k];
       alen += l;
     }
   }
   scrc[t] = acc;
   slen[t] = alen;
   __syncthreads();
-  for (int s = 1; s < nt; s <<= 1) {
-    if ((t % (2 * s)) == 0 && slen[t + s] > 0) {
-      scrc[t] = slen[t] ? crc_combine(scrc[t], scrc[t + s], slen[t + s]) : scrc[t + s];
-      slen[t] += slen[t + s];
+#pragma unroll 1
+  for (int lv = 0; lv < kLevels; lv++) {
+    const int sd = 1 << lv;
+    if ((t & (2 * sd - 1)) == 0 && slen[t + sd] > 0) {
+      const unsigned long long lr = slen[t + sd];
+      if (!slen[t]) scrc[t] = scrc[t + sd];
+      else if (lr == ((unsigned long long)(per * csz) << lv)) scrc[t] = crc_multmodp(xlev[lv], scrc[t]) ^ scrc[t + sd];
+      else scrc[t] = crc_combine(scrc[t], scrc[t + sd], lr);
+      slen[t] += lr;
     }
     __syncthreads();
   }
@@ -191,34 +219,24 @@ void upload_crc_constants() {
   for (int n = 1; n < 32; n++) x2n[n] = p = crc_multmodp(p, p);
   cudaMemcpyToSymbol(c_crc_tab, tab, sizeof(tab));
   cudaMemcpyToSymbol(c_x2n, x2n, sizeof(x2n));
-  // shift tables: x^(8 len) mod P for len = P 2^k, as byte-indexed linear maps
-  static uint32_t sh[2][5][4][256];
-  for (int kind = 0; kind < 2; kind++)
-    for (int k = 0; k < 5; k++) {
-      unsigned long long n = (unsigned long long)(kind == 0 ? kCrcLaneBytesRgb : kCrcLaneBytesPlane) << k;
-      uint32_t x = 1u << 31;  // x^0; x^(8 n) by square-and-multiply over x2n
-      unsigned kk = 3;
-      while (n) {
-        if (n & 1) x = crc_multmodp(x2n[kk & 31], x);
-        n >>= 1;
-        kk++;
-      }
-      for (int b = 0; b < 4; b++)
-        for (uint32_t v = 0; v < 256; v++) sh[kind][k][b][v] = crc_multmodp(x, v << (8 * b));
-    }
-  cudaMemcpyToSymbol(c_shift_tab, sh, sizeof(sh));
 }
 
-void launch_crc(const ImgDesc* d_descs, int nimg, long long max_n, cudaStream_t st) {
-  long long max_chunks = (3 * max_n + crc_chunk_bytes(0) - 1) / crc_chunk_bytes(0);
-  // 8 warps per CTA looping over chunks: few CTAs per (image, job), since each
-  // first stages 24 KB of tables in shared memory
-  long long gx = (max_chunks + 63) / 64;
-  const long long cap = (148 * 8 + 5 * nimg - 1) / (5 * nimg);
-  if (gx > cap) gx = cap;
-  if (gx < 1) gx = 1;
-  k_crc_chunks<<<dim3((unsigned)gx, nimg, 5), 256, 0, st>>>(d_descs);
-  k_crc_combine<<<dim3(5, nimg), 1024, 0, st>>>(d_descs);
+void launch_crc(const ImgDesc* d_descs, int nimg, long long units, cudaStream_t st) {
+  if (units <= 0) return;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  cudaFuncSetAttribute(k_crc_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCrcTabSmem);  // per device
+  // one CTA per SM; no more warps than 32-unit groups
+  long long gx = sms;
+  const long long groups = (units + 31) / 32;
+  if (gx * (kCrcThreads / 32) > groups) gx = (groups + kCrcThreads / 32 - 1) / (kCrcThreads / 32);
+  k_crc_chunks<<<(unsigned)gx, kCrcThreads, kCrcTabSmem, st>>>(d_descs, nimg, units);
+  k_crc_combine<<<dim3(5, nimg), kCrcCombineThreads, 0, st>>>(d_descs);
 }
 
 }  // namespace hdll

@@ -91,6 +91,7 @@ struct ImgDesc {
   unsigned* crc_part;         // per-chunk partial crcs
   long long crc_chunks[5];
   long long crc_part_off[5];
+  long long crc_u0;           // first CRC work unit (chunk) of the image in the batch (crc_assign_units)
 
 
   // GPU decoder (decode.cu): coder bodies in, RGBE (or the SDR) out
@@ -239,7 +240,10 @@ void launch_fit_regroup(const ImgDesc* d, const RegroupTab&, cudaStream_t);
 void launch_bitcat(uint8_t* dst, const uint8_t* const* src, const unsigned long long* dst_bit, const unsigned long long* nbits,
                    int npieces, unsigned long long max_bits, cudaStream_t);
 void launch_estimate(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
-void launch_crc(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
+// CRC chunks of the batch's active jobs, numbered image by image: sets each
+// descriptor's crc_u0 (after crc_mask / crc_np are final) and returns the total
+long long crc_assign_units(ImgDesc* ds, int n);
+void launch_crc(const ImgDesc*, int nimg, long long units, cudaStream_t);
 // both coders keep per-warp scratch in one device buffer (they run one after the other)
 size_t dct_scratch_bytes(const ChainTab&);
 void launch_entropy_dct(const ImgDesc*, const ChainTab&, void* scratch, cudaStream_t);

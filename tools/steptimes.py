@@ -17,8 +17,7 @@ else:
     pix = bench.generate(cfg, list(range(nimg)))
     if len({p.shape for p in pix}) == 1:
         np.save(cache, np.stack(pix))
-h, w = pix[0].shape[:2]
-preps = [container.prepare(P.RadianceImage(w, h, p, [("FORMAT", "32-bit_rle_rgbe")])) for p in pix]
+preps = [container.prepare(P.RadianceImage(p.shape[1], p.shape[0], p, [("FORMAT", "32-bit_rle_rgbe")])) for p in pix]
 dev = torch.device("cuda", 0)
 d_in = [torch.from_numpy(p.pixels).to(dev) for p in preps]
 caps = [container.stream_capacity(p) for p in preps]
