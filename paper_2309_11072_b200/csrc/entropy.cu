@@ -568,7 +568,17 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
 #ifndef HDLL_EXP_NO_EMIT
   {  // the scratch words, shifted into place
     const int nw = min(sb.n, scr_cap);
-    for (int j = 0; j < nw; j++) {
+    int j = 0;
+    if constexpr (!Gen::kStaticCtx) {  // plane rows: whole words, four loads in flight before their
+      for (; j + 4 < nw; j += 4) {     // stores (-0.17 ms; the DCT's few words per block lose by it)
+        uint32_t w4[4];
+#pragma unroll
+        for (int h = 0; h < 4; h++) w4[h] = scr[(j + h) * 32];
+#pragma unroll
+        for (int h = 0; h < 4; h++) lb.put(sink, w4[h], 32);
+      }
+    }
+    for (; j < nw; j++) {
       const uint32_t wd = scr[j * 32];
       const int len = j < nw - 1 ? 32 : (int)(nbits - 32LL * (nw - 1));
       lb.put(sink, len == 32 ? wd : wd >> (32 - len), len);
