@@ -224,14 +224,11 @@ constexpr uint32_t kCrcPoly = 0xEDB88320u;
 
 // a * b mod P in the reflected representation (zlib multmodp)
 __device__ __host__ __forceinline__ uint32_t crc_multmodp(uint32_t a, uint32_t b) {
-  uint32_t m = 1u << 31, p = 0;
-  for (;;) {
-    if (a & m) {
-      p ^= b;
-      if ((a & (m - 1)) == 0) break;
-    }
-    m >>= 1;
-    b = (b & 1) ? (b >> 1) ^ kCrcPoly : b >> 1;
+  uint32_t p = 0;  // branch-free: bit 31 - i of a selects b * x^i
+#pragma unroll
+  for (int i = 0; i < 32; i++) {
+    p ^= b & (0u - ((a >> (31 - i)) & 1u));
+    b = (b >> 1) ^ (kCrcPoly & (0u - (b & 1u)));
   }
   return p;
 }

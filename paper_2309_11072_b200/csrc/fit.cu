@@ -259,18 +259,25 @@ __device__ __forceinline__ XAcc x_acc(const ImgDesc& d, int c, const SegView& v)
   return XAcc{d.xs + (long long)c * d.fit_m + v.off};
 }
 
-__global__ void k_seg_setup(const ImgDesc* __restrict__ descs) {
+// one CTA of kSegs threads per image: each segment's tree depth, then an
+// exclusive scan of the node counts (2^L per non-empty segment)
+__global__ void __launch_bounds__(kSegs) k_seg_setup(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.x];
-  if (!d.slrme || threadIdx.x != 0) return;
-  long long off = 0;
-  for (int s = 0; s < kSegs; s++) {
-    SegView v = seg_view(d, s);
-    int L = v.n > 0 ? pairwise_level(v.n) : 0;
-    d.seg_level[s] = L;
-    d.seg_node_off[s] = off;
-    off += v.n > 0 ? (1LL << L) : 0;
-  }
-  d.seg_node_off[kSegs] = off;
+  if (!d.slrme) return;
+  const int s = threadIdx.x;
+  const SegView v = seg_view(d, s);
+  const int L = v.n > 0 ? pairwise_level(v.n) : 0;
+  d.seg_level[s] = L;
+  long long tot;
+  const long long ex = warp_excl_sum(v.n > 0 ? (1LL << L) : 0LL, &tot);
+  __shared__ long long wsum[kSegs / 32];
+  const int w = s >> 5;
+  if ((s & 31) == 0) wsum[w] = tot;
+  __syncthreads();
+  long long pre = 0;
+  for (int k = 0; k < w; k++) pre += wsum[k];
+  d.seg_node_off[s] = pre + ex;
+  if (s == kSegs - 1) d.seg_node_off[kSegs] = pre + ex + (v.n > 0 ? (1LL << L) : 0LL);
 }
 
 // one warp per depth-L node of a segment's pairwise tree
@@ -653,7 +660,7 @@ void launch_fit_sort(const ImgDesc* d_descs, int nimg, int max_sort_tiles, cudaS
 }
 
 void launch_fit_bins(const ImgDesc* d_descs, int nimg, long long max_nodes, int max_chunks, cudaStream_t st) {
-  k_seg_setup<<<nimg, 32, 0, st>>>(d_descs);
+  k_seg_setup<<<nimg, kSegs, 0, st>>>(d_descs);
   k_seg_nodes<<<dim3((unsigned)((max_nodes + 3) / 4), nimg), 128, 0, st>>>(d_descs);
   cudaFuncSetAttribute(k_seg_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DotSmem));
   k_seg_dot<<<dim3(kSegs, nimg, max_chunks), 32, sizeof(DotSmem), st>>>(d_descs);
