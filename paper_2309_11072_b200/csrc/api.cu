@@ -151,7 +151,7 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
 
   long long max_n = 0, max_sort_tiles = 0, max_nodes = 0, max_out = 0;
   int max_w = 0, max_h = 0, max_radius = 0, max_level = 0, max_base_tiles = 0, max_chunks = 1;
-  bool any_real = false, any_slrme = false;
+  bool any_real = false, any_slrme = false, any_non3 = false, any_hist = false;
   for (int i = 0; i < n; i++) {
     const auto& im = imgs[i];
     const auto& p = im.params;
@@ -175,7 +175,9 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
     max_base_tiles = std::max(max_base_tiles, tiles_x * d.nby);
     if (mode == 0) max_out = std::max(max_out, d.out_cap);
     any_real |= (d.slrme && d.sigma_milli != 0);
+    any_non3 |= (d.slrme && d.sigma_milli != 0 && d.radius != 3);
     any_slrme |= d.slrme != 0;
+    any_hist |= (d.slrme && !d.fit_owner && !d.hist_fused);
   }
   const long long crc_units = crc_assign_units(ds.data(), n);
   memcpy(H + t_descs, ds.data(), sizeof(ImgDesc) * n);
@@ -212,13 +214,13 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   }
   mark(kStBase);
   if (mode == 0 && any_real) {
-    launch_prefilter(dd, n, max_w, max_h, max_radius, st);
-    c->launches += 2;
+    launch_prefilter(dd, n, max_w, max_h, max_radius, st, any_non3);
+    c->launches += any_non3 ? 2 : 1;
   }
   mark(kStPrefilter);
   if (mode == 0 && any_slrme) {
-    launch_fit(dd, n, (int)max_sort_tiles, max_nodes, max_chunks, st);
-    c->launches += 7;
+    launch_fit(dd, n, (int)max_sort_tiles, max_nodes, max_chunks, st, any_hist);
+    c->launches += any_hist ? 7 : 6;
   }
   mark(kStFit);
   if (mode == 0) {

@@ -223,9 +223,13 @@ void launch_hdr_sizes(const uint8_t* rgbe, int w, int h, long long* sizes, cudaS
 void launch_hdr_write(const uint8_t* rgbe, int w, int h, const long long* offs, uint8_t* out, cudaStream_t);
 void launch_hdr_expand(const uint8_t* data, const long long* starts, const uint8_t* newrle, int w, int h, uint8_t* rgbe,
                        cudaStream_t);
-void launch_prefilter(const ImgDesc*, int nimg, int max_w, int max_h, int max_radius, cudaStream_t);
-void launch_fit(const ImgDesc*, int nimg, int max_sort_tiles, long long max_nodes, int max_chunks, cudaStream_t);
-void launch_fit_sort(const ImgDesc*, int nimg, int max_sort_tiles, cudaStream_t);
+// any_non3: some image of the batch filters with a radius other than 3 (else the
+// general kernels are not launched at all)
+void launch_prefilter(const ImgDesc*, int nimg, int max_w, int max_h, int max_radius, cudaStream_t, bool any_non3 = true);
+// any_hist: some image needs k_sort_hist (its histogram is not fused into k_sdr_ycc)
+void launch_fit(const ImgDesc*, int nimg, int max_sort_tiles, long long max_nodes, int max_chunks, cudaStream_t,
+                bool any_hist = true);
+void launch_fit_sort(const ImgDesc*, int nimg, int max_sort_tiles, cudaStream_t, bool any_hist = true);
 void launch_fit_bins(const ImgDesc*, int nimg, long long max_nodes, int max_chunks, cudaStream_t);
 struct RegroupTab {
   int nsrc;

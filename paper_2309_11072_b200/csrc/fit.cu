@@ -73,6 +73,8 @@ __global__ void __launch_bounds__(256) k_sort_scan(const ImgDesc* __restrict__ d
       if (e == 255) d.bin_start[256] = below + d.bin_count[255];
     }
   }
+  // an empty bin's tile offsets are never read (k_sort_scatter places no sample in it)
+  if (d.bin_count[e] == 0) return;
   const long long T = d.sort_tiles;
   unsigned* row = d.tile_hist + (long long)e * T;
   const long long per = (T + 255) / 256;
@@ -652,8 +654,8 @@ __global__ void __launch_bounds__(256) k_seg_reduce_coef(const ImgDesc* __restri
   if (!isfinite(a32) || !isfinite(b32)) atomicOr(d.status, kErrNonFinite);
 }
 
-void launch_fit_sort(const ImgDesc* d_descs, int nimg, int max_sort_tiles, cudaStream_t st) {
-  k_sort_hist<<<dim3(max_sort_tiles, nimg), 256, 0, st>>>(d_descs);
+void launch_fit_sort(const ImgDesc* d_descs, int nimg, int max_sort_tiles, cudaStream_t st, bool any_hist) {
+  if (any_hist) k_sort_hist<<<dim3(max_sort_tiles, nimg), 256, 0, st>>>(d_descs);
   k_sort_scan<<<dim3(256, nimg), 256, 0, st>>>(d_descs);
   cudaFuncSetAttribute(k_sort_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ScatterSmem));
   k_sort_scatter<<<dim3(max_sort_tiles, nimg), 256, sizeof(ScatterSmem), st>>>(d_descs);
@@ -668,8 +670,8 @@ void launch_fit_bins(const ImgDesc* d_descs, int nimg, long long max_nodes, int 
 }
 
 void launch_fit(const ImgDesc* d_descs, int nimg, int max_sort_tiles, long long max_nodes, int max_chunks,
-                cudaStream_t st) {
-  launch_fit_sort(d_descs, nimg, max_sort_tiles, st);
+                cudaStream_t st, bool any_hist) {
+  launch_fit_sort(d_descs, nimg, max_sort_tiles, st, any_hist);
   launch_fit_bins(d_descs, nimg, max_nodes, max_chunks, st);
 }
 

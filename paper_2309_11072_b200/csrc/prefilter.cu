@@ -207,11 +207,13 @@ __global__ void __launch_bounds__(256) k_prefilter_cols(const ImgDesc* __restric
   }
 }
 
-void launch_prefilter(const ImgDesc* d_descs, int nimg, int max_w, int max_h, int max_radius, cudaStream_t st) {
+void launch_prefilter(const ImgDesc* d_descs, int nimg, int max_w, int max_h, int max_radius, cudaStream_t st,
+                      bool any_non3) {
   if (max_radius >= 3) {  // the images of radius 3 (sigma 1, the default); the others return at once
     const int tiles = ((max_w + 249) / 250) * ((max_h + kCR - 1) / kCR);
     k_prefilter_cols<3><<<dim3(tiles, 1, nimg * 3), 256, 0, st>>>(d_descs);
   }
+  if (!any_non3) return;
   if (max_radius <= kFusedMaxR) {  // (images of other radii; radius-3 ones return at once)
     const int tiles = ((max_w + kTW - 1) / kTW) * ((max_h + kTH - 1) / kTH);
     k_prefilter_fused<<<dim3(tiles, 1, nimg * 3), 256, 0, st>>>(d_descs);
