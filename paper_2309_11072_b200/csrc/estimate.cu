@@ -5,6 +5,8 @@
 // r = (M - M*) & 255 (container.py:187-190); slrme=False uses M* = S
 // (container.py:182-185).  The E plane is split_planes' 4th byte
 // (radiance_io.py:328-338).  4 pixels per thread through one 128-bit load.
+#include <algorithm>
+
 #include "encoder.cuh"
 
 namespace hdll {
@@ -99,10 +101,14 @@ __global__ void __launch_bounds__(256) k_estimate(const ImgDesc* __restrict__ de
 
 void launch_estimate(const ImgDesc* d_descs, int nimg, long long max_n, cudaStream_t st) {
   long long nq = (max_n + 3) / 4;
-  int gx = (int)((nq + 255) / 256);
-  if (gx > 148 * 8) gx = 148 * 8;
+  // about four waves of CTAs over the whole batch: each CTA stages the 6 KB
+  // coefficient table once and then loops (one pass per CTA was 1.7 per
+  // thread on config 1, the table loads and barrier a large share of it)
+  const long long cap = std::max(1LL, (long long)148 * 8 * 4 / nimg);
+  long long gx = (nq + 255) / 256;
+  if (gx > cap) gx = cap;
   if (gx < 1) gx = 1;
-  k_estimate<<<dim3(gx, nimg), 256, 0, st>>>(d_descs);
+  k_estimate<<<dim3((unsigned)gx, nimg), 256, 0, st>>>(d_descs);
 }
 
 }  // namespace hdll
