@@ -129,6 +129,27 @@ def dist_env():
     return rank, world, local
 
 
+STAGE_KERNEL = {"tonemap": "hdll::k_tm_nodes", "base": "hdll::k_base_layer", "prefilter": "hdll::k_prefilter_cols",
+                "fit": "hdll::k_sort_scatter", "estimate": "hdll::k_estimate", "crc": "hdll::k_crc_chunks",
+                "entropy_dct": "hdll::k_entropy_dct", "entropy_plane": "hdll::k_entropy_plane",
+                "assemble": "hdll::k_assemble"}
+
+
+def pipe_util(stage):
+    """The stage's main kernel's busiest execution pipe, % of that pipe's peak
+    (profiles/pipe_util.json, from the committed ncu --set full capture -- not
+    measured by this run)."""
+    f = ROOT / "profiles" / "pipe_util.json"
+    if not f.exists():
+        return None
+    k = STAGE_KERNEL.get(stage)
+    e = json.loads(f.read_text()).get(k)
+    if not e:
+        return None
+    return {"kernel": k, "pipe": e["pipe"], "pct_of_pipe_peak": e["pct"], "issue_active_pct": e["issue_pct"],
+            "source": "profiles/pipe_util.json (ncu --set full, profiles/r01/r01_full_raw.csv)"}
+
+
 def run_b200(args):
     import torch
 
@@ -267,7 +288,8 @@ def run_b200(args):
                "cores": min(sample, os.cpu_count() or 1),
                "kind": "port",
                "sample": f"{sample} of the {nimg} config-1 images, one per process (oracle/ C+numpy port, "
-                         f"bit-identical to the reference), wall {wall:.1f}s"}
+                         f"bit-identical to the reference), wall {wall:.1f}s on "
+                         f"{min(sample, os.cpu_count() or 1)} worker processes"}
         parity = all(bytes(d_out[i][: int(lens[i])].cpu().numpy()) == res[i][0] for i in range(sample))
 
     line = {
@@ -289,7 +311,8 @@ def run_b200(args):
                      "frac": round(dom_achieved / peak, 5), "traffic": traffic, "peak_source": peak_src,
                      "kernel": f"stage {dom} (k_entropy_plane + fix-up)" if dom == "entropy_plane" else f"stage {dom}",
                      "alg_bytes_per_launch": round(stage_alg[dom]), "launch_ms": round(stage_ms[dom], 4),
-                     "note": "integer/latency bound, not HBM bound (DESIGN.md section 4)"},
+                     "note": "integer/latency bound, not HBM bound (DESIGN.md section 4)",
+                     "busiest_pipe": pipe_util(dom)},
         "pipeline_roofline": {"achieved": round(achieved, 2), "unit": "GB/s", "frac": round(achieved / peak, 5),
                               "scope": "whole encode step (SURVEY 8d: 4 B/px RGBE + stream bytes)",
                               "bytes_per_px": round(alg_bytes / total_px, 3)},
@@ -466,7 +489,7 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--quality", type=int, default=85)
     ap.add_argument("--sigma", type=float, default=1.0)
-    ap.add_argument("--cpu-sample", type=int, default=4)
+    ap.add_argument("--cpu-sample", type=int, default=16)
     ap.add_argument("--chunk", type=int, default=64)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--tiled", action="store_true", help="config 3: tile-sharded path even on one rank")

@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(256) k_sort_scatter(const ImgDesc* __restrict_
     const unsigned off = pre + ex;
     sm.loc_off[e] = off;
     if (e == 255) sm.loc_off[256] = off + tot;
-    sm.g_off[e] = d.tile_hist[(long long)e * d.sort_tiles + tile];
+    sm.g_off[e] = tot ? d.tile_hist[(long long)e * d.sort_tiles + tile] : 0u;  // (bins of this tile only)
     unsigned run = off;
     for (int k = 0; k < 8; k++) {
       unsigned c = sm.wcnt[k][e];
