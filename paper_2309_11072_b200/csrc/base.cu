@@ -16,6 +16,8 @@
 // One CTA = 8 pixel rows x 128 columns (16 blocks) of one image, 128 threads.
 // All block transforms stay in shared memory; fp64 with no contraction and the
 // reference's summation order (s = 0.0; s += C * x for t = 0..7).
+#include <algorithm>
+
 #include "encoder.cuh"
 
 namespace hdll {
@@ -475,7 +477,9 @@ void launch_base_layer(const ImgDesc* d_descs, int nimg, int max_tiles, long lon
   if (gx > 148 * 8) gx = 148 * 8;
   if (gx < 1) gx = 1;
   k_sdr_ycc<<<dim3(gx, nimg), 256, 0, st>>>(d_descs);
-  k_sdr_fix<<<dim3(40, nimg), 256, 0, st>>>(d_descs);  // ~0.3 % of the pixels, each an fp64 pow
+  // ~0.3 % of the pixels, each an fp64 pow: about one CTA per 64 Ki pixels of the largest image
+  const long long fx = std::min(1184LL, std::max(40LL, max_n >> 16));
+  k_sdr_fix<<<dim3((unsigned)fx, nimg), 256, 0, st>>>(d_descs);
   size_t smem = sizeof(double) * 3 * 8 * kRowStride;
   cudaFuncSetAttribute(k_base_layer<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  // per device
   k_base_layer<false><<<dim3(max_tiles, nimg), 128, smem, st>>>(d_descs);

@@ -177,12 +177,24 @@ __global__ void __launch_bounds__(kCrcCombineThreads) k_crc_combine(const ImgDes
   if (c0 < c1) {
     acc = part[c0];
     alen = (unsigned long long)min(csz, len - c0 * csz);
-    for (long long k = c0 + 1; k < c1; k++) {
+    auto shift = [&](uint32_t a) {  // times x^(8 csz)
+      return xch[0][a & 0xFF] ^ xch[1][(a >> 8) & 0xFF] ^ xch[2][(a >> 16) & 0xFF] ^ xch[3][a >> 24];
+    };
+    // whole chunks (all but the job's last), eight partial CRCs loaded ahead of their merges
+    const long long cf = min(c1, nch - 1);
+    long long k = c0 + 1;
+    for (; k + 8 <= cf; k += 8) {
+      uint32_t p8[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) p8[u] = part[k + u];
+#pragma unroll
+      for (int u = 0; u < 8; u++) acc = shift(acc) ^ p8[u];
+      alen += 8ULL * (unsigned long long)csz;
+    }
+    for (; k < c1; k++) {
       unsigned long long l = (unsigned long long)min(csz, len - k * csz);
-      if (l == (unsigned long long)csz)
-        acc = xch[0][acc & 0xFF] ^ xch[1][(acc >> 8) & 0xFF] ^ xch[2][(acc >> 16) & 0xFF] ^ xch[3][acc >> 24] ^ part[k];
-      else
-        acc = crc_multmodp(x2nmodp(l, 3), acc) ^ part[k];
+      if (l == (unsigned long long)csz) acc = shift(acc) ^ part[k];
+      else acc = crc_multmodp(x2nmodp(l, 3), acc) ^ part[k];
       alen += l;
     }
   }
