@@ -142,3 +142,19 @@ def test_native_fails_loudly_without_device():
         pytest.skip("a GPU is present")
     with pytest.raises(RuntimeError):
         _native.Context(0)
+
+
+@pytest.mark.parametrize("nimg,chunk,repeats", [(64, 64, 10), (64, 64, 1), (64, 64, 3), (5, 2, 4), (9, 8, 7), (3, 8, 2),
+                                                (1, 1, 5), (17, 4, 3)])
+def test_host_pipeline_chunks_cover_the_stream_in_order(nimg, chunk, repeats):
+    """HostPipeline._chunks: every image of the repeated batch exactly once, in
+    order, no chunk above `chunk`, ramped (smaller) ends when the stream is long."""
+    h = container.HostPipeline.__new__(container.HostPipeline)
+    h.preps, h.chunk = [None] * nimg, chunk
+    chunks = h._chunks(repeats)
+    flat = [i for c in chunks for i in c]
+    assert flat == list(range(nimg)) * repeats
+    c = min(chunk, nimg)
+    assert all(1 <= len(k) <= c for k in chunks)
+    if nimg * repeats >= 3 * c and c >= 4:
+        assert len(chunks[0]) <= c // 4 and len(chunks[-1]) <= c // 2
