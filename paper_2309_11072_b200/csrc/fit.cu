@@ -515,13 +515,16 @@ __global__ void __launch_bounds__(32) k_seg_dot(const ImgDesc* __restrict__ desc
       const double* xs = &sm.x[st][mx];
       const uint8_t* ys = &sm.y[st][my];
       if (lane < nl) {
+        unsigned sy32 = 0;  // a block's byte sum fits 32 bits: one add per sample
 #pragma unroll 8
-        for (long long k = lane; k < len; k += nl) {
-          const double x = xs[k], y = (double)ys[k];
+        for (int k = lane; k < (int)len; k += nl) {
+          const unsigned yb = ys[k];
+          const double x = xs[k], y = (double)yb;
           axx = __fma_rn(x, x, axx);
           axy = __fma_rn(x, y, axy);
-          sy += ys[k];
+          sy32 += yb;
         }
+        sy += sy32;
       }
       __syncwarp();
     }
