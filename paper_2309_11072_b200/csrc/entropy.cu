@@ -34,7 +34,10 @@ namespace hdll {
 // (3 us measured best: config 1 -0.38 ms against 20 ns; 10 us and backoff
 // were slower).  A predecessor is always in flight, so waits are bounded by
 // one tile's work; kSpinLimit polls (seconds) only guard against a bug.
-constexpr unsigned kLookbackSleepNs = 3000;
+#ifndef HDLL_LB_SLEEP_NS
+#define HDLL_LB_SLEEP_NS 3000
+#endif
+constexpr unsigned kLookbackSleepNs = HDLL_LB_SLEEP_NS;
 constexpr long long kSpinLimit = 1LL << 20;
 
 // ---------------------------------------------------------------------------
