@@ -47,6 +47,7 @@ constexpr int kTileBlocks = 16;
 constexpr int kTileCols = kTileBlocks * 8;  // 128
 constexpr int kRowStride = kTileCols + 1;   // doubles; padding against bank conflicts
 
+
 __device__ __forceinline__ double rgbe_scale_b(unsigned e) {
   return __longlong_as_double((long long)((int)e - 136 + 1023) << 52);
 }
@@ -105,8 +106,9 @@ __device__ __forceinline__ int quantize_pow_fast(double m, float g32, bool appro
 // `exact` the fp64 pow for whatever the fast pass cannot certify).  Returns
 // false when a byte is undecided (exact == false only).
 struct TmoConst {
-  float g32;    // 1 / gamma
-  bool approx;  // g32 <= kApproxMaxG
+  float g32;     // 1 / gamma
+  bool approx;   // g32 <= kApproxMaxG
+  double inv_la, inv_w2;  // refined reciprocals of log_avg and white^2 (fast pass)
 };
 
 __device__ __forceinline__ bool sdr_pixel(const ImgDesc& d, uint32_t q, double log_avg, double white,
@@ -127,8 +129,8 @@ __device__ __forceinline__ bool sdr_pixel(const ImgDesc& d, uint32_t q, double l
     const double disp = scaled * (1.0 + scaled / (white * white)) / (1.0 + scaled);
     ratio = lw > 0 ? disp / lw : 0.0;
   } else {  // divisions as refined reciprocals (~2^-40): far inside the kAmb window
-    const double scaled = d.key * lw * rcp_nr(log_avg);
-    const double disp = scaled * (1.0 + scaled * rcp_nr(white * white)) * rcp_nr(1.0 + scaled);
+    const double scaled = d.key * lw * tc.inv_la;
+    const double disp = scaled * (1.0 + scaled * tc.inv_w2) * rcp_nr(1.0 + scaled);
     ratio = lw > 0 ? disp * rcp_nr(lw) : 0.0;
   }
   bool ok = true;
@@ -150,14 +152,18 @@ __device__ __forceinline__ bool sdr_pixel(const ImgDesc& d, uint32_t q, double l
 // stored as bytes (Y in [0, 255], Cb / Cr in [-128, 127]).  Four pixels per
 // thread; the transform kernel below reads them back per 8x8 block.  Split from
 // the transforms so each runs at its own register budget.
+// round_half_away(x) as an int: trunc(x + copysign(0.5, x)), the truncation by
+// the conversion itself (one XU op instead of a rounding and a conversion)
+__device__ __forceinline__ int rha_int(double x) { return (int)(x + copysign(0.5, x)); }
+
 __device__ __forceinline__ void ycc_bytes(const uint8_t* s3, uint8_t* y, int8_t* cb, int8_t* cr) {
   const double r = s3[0], g = s3[1], b = s3[2];
   const double Y = 0.299 * r + 0.587 * g + 0.114 * b;
   const double u = -0.168736 * r - 0.331264 * g + 0.5 * b;
   const double v = 0.5 * r - 0.418688 * g - 0.081312 * b;
-  *y = (uint8_t)clampd(rha(Y), 0.0, 255.0);
-  *cb = (int8_t)clampd(rha(u), -128.0, 127.0);
-  *cr = (int8_t)clampd(rha(v), -128.0, 127.0);
+  *y = (uint8_t)min(max(rha_int(Y), 0), 255);
+  *cb = (int8_t)min(max(rha_int(u), -128), 127);
+  *cr = (int8_t)min(max(rha_int(v), -128), 127);
 }
 
 // _rgb_to_ycc of one pixel as Y | Cb << 8 | Cr << 16.  (An exact-integer form
@@ -177,6 +183,8 @@ __global__ void __launch_bounds__(256) k_sdr_ycc(const ImgDesc* __restrict__ des
   TmoConst tc;
   tc.g32 = (float)d.inv_gamma;
   tc.approx = tc.g32 <= kApproxMaxG;
+  tc.inv_la = rcp_nr(log_avg);
+  tc.inv_w2 = rcp_nr(white * white);
   const long long nq = (d.n + 3) / 4;
   uint8_t* Yp = d.ycc;
   uint8_t* Cb = d.ycc + d.n;
@@ -271,6 +279,8 @@ __global__ void __launch_bounds__(256) k_sdr_fix(const ImgDesc* __restrict__ des
   tc.g32 = (float)d.inv_gamma;
   tc.approx = tc.g32 <= kApproxMaxG;
   const double log_avg = d.scalars[1], white = d.scalars[2];
+  tc.inv_la = rcp_nr(log_avg);
+  tc.inv_w2 = rcp_nr(white * white);
   const bool allzero = d.scalars[3] != 0.0;
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
     const long long p = d.amb_list[i];
