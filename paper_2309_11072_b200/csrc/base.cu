@@ -152,9 +152,6 @@ __device__ __forceinline__ bool sdr_pixel(const ImgDesc& d, uint32_t q, double l
 // stored as bytes (Y in [0, 255], Cb / Cr in [-128, 127]).  Four pixels per
 // thread; the transform kernel below reads them back per 8x8 block.  Split from
 // the transforms so each runs at its own register budget.
-// round_half_away(x) as an int: trunc(x + copysign(0.5, x)), the truncation by
-// the conversion itself (one XU op instead of a rounding and a conversion)
-__device__ __forceinline__ int rha_int(double x) { return (int)(x + copysign(0.5, x)); }
 
 __device__ __forceinline__ void ycc_bytes(const uint8_t* s3, uint8_t* y, int8_t* cb, int8_t* cr) {
   const double r = s3[0], g = s3[1], b = s3[2];
@@ -465,7 +462,7 @@ __global__ void __launch_bounds__(128, 8) k_base_layer(const ImgDesc* __restrict
     v[2] = Y + 1.772 * cb;
     long long pi = (long long)y * d.w + x;
 #pragma unroll
-    for (int c = 0; c < 3; c++) d.s_planes[c * d.n + pi] = (uint8_t)clampd(rha(v[c]), 0.0, 255.0);
+    for (int c = 0; c < 3; c++) d.s_planes[c * d.n + pi] = (uint8_t)min(max(rha_int(v[c]), 0), 255);
   }
 }
 

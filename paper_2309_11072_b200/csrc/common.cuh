@@ -27,6 +27,9 @@ enum : uint32_t {
 
 // round_half_away, _util.py:8-11: trunc(x + copysign(0.5, x))
 __device__ __forceinline__ double rha(double x) { return trunc(x + copysign(0.5, x)); }
+// round_half_away(x) as an int: the truncating conversion does the trunc (one
+// conversion instead of a rounding and a conversion; saturates out of range)
+__device__ __forceinline__ int rha_int(double x) { return (int)(x + copysign(0.5, x)); }
 
 __device__ __forceinline__ double clampd(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
 

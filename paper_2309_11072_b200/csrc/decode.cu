@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(256) k_decode_output(const ImgDesc* __restrict
         const float a = sa[c * 256 + e];
         if (isnan(a)) atomicOr(d.status, kDecNoEntry);  // absent entry (estimator.py:82-92 KeyError)
         const double est = (double)a * s + (double)sb[c * 256 + e];
-        ms = (unsigned)clampd(rha(est), 0.0, 255.0);
+        ms = (unsigned)min(max(rha_int(est), 0), 255);
       } else {
         ms = d.s_planes[(long long)c * d.n + p];
       }

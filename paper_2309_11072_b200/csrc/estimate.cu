@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256) k_estimate(const ImgDesc* __restrict__ de
           unsigned ms;
           if (d.slrme) {
             const double est = (double)sa[c * 256 + e] * sv[c][k] + (double)sb[c * 256 + e];
-            ms = (unsigned)clampd(rha(est), 0.0, 255.0);
+            ms = (unsigned)min(max(rha_int(est), 0), 255);
           } else {
             ms = (unsigned)sv[c][k];
           }
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256) k_estimate(const ImgDesc* __restrict__ de
         if (d.slrme) {
           double s = real ? d.sstar[(long long)c * d.n + p] : (double)d.s_planes[(long long)c * d.n + p];
           double est = (double)sa[c * 256 + e] * s + (double)sb[c * 256 + e];
-          ms = (unsigned)clampd(rha(est), 0.0, 255.0);
+          ms = (unsigned)min(max(rha_int(est), 0), 255);
         } else {
           ms = d.s_planes[(long long)c * d.n + p];
         }
