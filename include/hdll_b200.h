@@ -80,7 +80,9 @@ uint64_t hdll_b200_stream_capacity(uint32_t width, uint32_t height, uint32_t hdr
 int hdll_b200_encode_batch_device(hdll_b200_ctx *ctx, const hdll_b200_image *imgs, int n, uint8_t *const *d_out,
                                   const uint64_t *out_cap, uint64_t *d_out_len, void *stream);
 
-/* Wait for the last batch of this context and return its status. */
+/* Wait for the last batch of this context and return the worst status of
+ * every encode batch since the previous sync (device errors of earlier batches
+ * of a pipeline are accumulated on the device, not lost). */
 int hdll_b200_sync(hdll_b200_ctx *ctx);
 
 /* Host -> host convenience: H2D of the RGBE quads, encode, D2H of the stream. */
@@ -89,7 +91,9 @@ int hdll_b200_encode_host(hdll_b200_ctx *ctx, const hdll_b200_image *img, uint8_
 
 /* Per-stage trace of image `index` of the last batch (want_trace set):
  * which = 0 sdr (h,w,3), 1 decoded S (h,w,3 interleaved), 2 m_star (3 planes),
- * 3 residuals (3 planes).  nbytes must equal the array size. */
+ * 3 residuals (3 planes).  which | 16: the same arrays (1 and 3 only) of the
+ * last hdll_b200_decode_batch (the decode_hdr trace hook, container.py:269-271).
+ * nbytes must equal the array size. */
 int hdll_b200_trace(hdll_b200_ctx *ctx, int index, int which, uint8_t *h_dst, uint64_t nbytes);
 
 /* Lossless coder id 1 body (<II w,h> + bits) and the raw-plane CRC-32. */
@@ -121,7 +125,8 @@ const char *hdll_b200_status_string(int status);
 typedef struct hdll_b200_decode_image {
   uint32_t width, height;
   int32_t quality, slrme, sigma_milli, radius;
-  int32_t sdr_only;          /* 1: decode_sdr -- base layer only, output (h, w, 3) */
+  int32_t sdr_only;          /* 1: decode_sdr -- base layer only, output (h, w, 3);
+                                2: body[1] alone as a lossless plane (coder plugin decode), output (h, w) */
   const double *taps;        /* host, 2 * radius + 1 Gaussian taps (sigma_milli > 0) */
   const float *a32, *b32;    /* host [3][256] regression table, absent entries NaN */
   const uint8_t *body[5];    /* host: base, E, R, G, B coder bodies without their <II> w, h */

@@ -32,6 +32,8 @@ from .container import (
 )
 
 from .decode import decode_hdr, decode_hdr_batch, decode_sdr
+from .codec import (lossless_decode, lossless_encode, lossy_decode, lossy_encode, payload_coder_id,
+                    register_lossless_coder, register_lossy_coder)
 from .hdr_io import RadianceFormatError, parse_hdr, read_hdr_file, write_hdr, write_hdr_file
 
 __version__ = "0.1.0"

@@ -16,7 +16,7 @@ LIB_PATH = Path(os.environ["HDLL_B200_LIB"]) if os.environ.get("HDLL_B200_LIB") 
 
 OK, E_ARG, E_EMPTY, E_NONFINITE, E_CUDA, E_INTERNAL, E_CAPACITY = range(7)
 
-# every symbol include/hdll_b200.h declares (checked by tests/test_abi.py)
+# every symbol include/hdll_b200.h declares (checked by tests/test_host.py)
 EXPORTS = (
     "hdll_b200_ctx_create", "hdll_b200_ctx_destroy", "hdll_b200_stream_capacity",
     "hdll_b200_encode_batch_device", "hdll_b200_sync", "hdll_b200_encode_host", "hdll_b200_trace",
@@ -138,6 +138,9 @@ class Context:
 
     def __init__(self, device: int = 0):
         self.device = device
+        # held by host code that reads a batch's results (stage times, traces)
+        # after the call that launched it; each C call also locks the context
+        self.lock = threading.RLock()
         self.handle = ctypes.c_void_p()
         rc = lib().hdll_b200_ctx_create(ctypes.byref(self.handle), device)
         if rc != OK:
@@ -159,13 +162,15 @@ class Context:
 _contexts: dict[int, Context] = {}
 
 
+_ctx_lock = threading.Lock()
+
+
 def context(device: int = 0) -> Context:
-    with _lock:
+    """The device's shared context (created once; the C side serialises calls on it)."""
+    with _ctx_lock:
         ctx = _contexts.get(device)
-    if ctx is None:
-        ctx = Context(device)
-        with _lock:
-            _contexts[device] = ctx
+        if ctx is None:
+            ctx = _contexts[device] = Context(device)
     return ctx
 
 

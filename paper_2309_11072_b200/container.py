@@ -354,6 +354,29 @@ def gaussian_kernel(sigma: float) -> np.ndarray:
     return w / w.sum()
 
 
+# OpenBLAS core types whose ddot is the SKYLAKEX (0) or HASWELL (1) kernel: the
+# Cooper Lake / Sapphire Rapids builds include the SKYLAKEX kernel list, the Zen
+# builds the Haswell one
+BLAS_KERNELS = {"skylakex": 0, "cooperlake": 0, "sapphirerapids": 0, "haswell": 1, "zen": 1}
+
+
+def host_blas() -> dict:
+    """This host's numpy BLAS as threadpoolctl reports it: the parity parameters
+    a reference run here would have (architecture -> modelled kernel id or
+    None, thread count)."""
+    try:
+        from threadpoolctl import threadpool_info
+        info = [i for i in threadpool_info() if i.get("user_api") == "blas"]
+    except Exception:  # noqa: BLE001 -- reported, not fatal
+        info = []
+    if not info:
+        return {"architecture": None, "kernel": None, "threads": None, "internal_api": None}
+    arch = info[0].get("architecture")
+    return {"architecture": arch, "kernel": BLAS_KERNELS.get(str(arch).lower()),
+            "threads": info[0].get("num_threads"), "internal_api": info[0].get("internal_api"),
+            "version": info[0].get("version")}
+
+
 def _blas_defaults(blas_kernel, blas_threads):
     """Sum-order model of the reference's np.dot.  Defaults:
     OpenBLAS SKYLAKEX with 1 thread, overridable per call or by HDLL_BLAS_KERNEL
@@ -361,7 +384,7 @@ def _blas_defaults(blas_kernel, blas_threads):
     if blas_kernel is None:
         blas_kernel = os.environ.get("HDLL_BLAS_KERNEL", "skylakex")
     if isinstance(blas_kernel, str):
-        blas_kernel = {"skylakex": 0, "haswell": 1, "zen": 1}[blas_kernel.lower()]
+        blas_kernel = BLAS_KERNELS[blas_kernel.lower()]
     if blas_threads is None:
         blas_threads = int(os.environ.get("HDLL_BLAS_THREADS", "1"))
     return int(blas_kernel), max(1, int(blas_threads))
@@ -474,6 +497,26 @@ def _stage_times(ctx) -> dict:
     return dict(zip(STAGES, [float(v) for v in ms]))
 
 
+def reference_timings(dev: dict) -> dict:
+    """The reference's `timings` keys (container.py:163-222) from the device stage
+    times.  Stages the B200 path fuses away report 0.0: `split` (RGBE unpack
+    happens inside the tone-map and estimate kernels), `base_decode` (S is
+    rebuilt from the coefficients inside the base-layer kernel)
+    and `residual` (formed inside k_estimate)."""
+    return {
+        "split": 0.0,
+        "tonemap": dev["tonemap"],
+        "base_encode": dev["base"] + dev["entropy_dct"],
+        "base_decode": 0.0,
+        "prefilter": dev["prefilter"],
+        "fit": dev["fit"],
+        "estimate": dev["estimate"],
+        "residual": 0.0,
+        "enhancement_encode": dev["crc"] + dev["entropy_plane"],
+        "assemble": dev["assemble"],
+    }
+
+
 def encode(image, quality: int = 85, sigma: float = 1.0, slrme: bool = True, global_regression: bool = False,
            lossy_coder: int = 1, lossless_coder: int = 1, tmo: TmoParams | None = None,
            timings: dict | None = None, trace: dict | None = None, *, device: int = 0,
@@ -482,9 +525,11 @@ def encode(image, quality: int = 85, sigma: float = 1.0, slrme: bool = True, glo
 
     `image` is any object with width, height, pixels ((h, w, 4) uint8),
     header_vars and resolution_orientation (the reference's RadianceImage works).
-    `timings` receives per-stage device milliseconds plus host-side
-    `h2d_encode_d2h`; `trace` receives sdr, s, m_star, residuals and table like
-    the reference's trace hook (container.py:224-229)."""
+    `timings` accumulates (like container.py:114-118) the reference's stage keys
+    (`reference_timings`), the device stages (`STAGES`, prefixed `device_`) and
+    the host-side `h2d_encode_d2h`; `trace` receives sdr, s, m_star, residuals
+    and table like the reference's trace hook (container.py:224-229).  Safe to
+    call from several threads: calls on a device's context are serialised."""
     t0 = time.perf_counter()
     prep = _prepare(image, quality, sigma, slrme, global_regression, lossy_coder, lossless_coder, tmo,
                     blas_kernel, blas_threads, trace is not None)
@@ -493,14 +538,19 @@ def encode(image, quality: int = 85, sigma: float = 1.0, slrme: bool = True, glo
     out = np.empty(cap, np.uint8)
     olen = ctypes.c_uint64(0)
     im = _image_struct(prep, prep.pixels.ctypes.data)
-    _native.check(_native.lib().hdll_b200_encode_host(ctx.handle, ctypes.byref(im), out.ctypes.data, cap,
-                                                      ctypes.byref(olen)), "encode")
-    stream = deserialize(out[: olen.value].tobytes())
-    if timings is not None:
-        timings.update(_stage_times(ctx))
-        timings["h2d_encode_d2h"] = (time.perf_counter() - t0) * 1000.0
-    if trace is not None:
-        _collect_trace(ctx, 0, prep, stream, trace)
+    with ctx.lock:  # the stage times and traces below belong to this call's batch
+        _native.check(_native.lib().hdll_b200_encode_host(ctx.handle, ctypes.byref(im), out.ctypes.data, cap,
+                                                          ctypes.byref(olen)), "encode")
+        stream = deserialize(out[: olen.value].tobytes())
+        if timings is not None:
+            dev = _stage_times(ctx)
+            add = reference_timings(dev)
+            add.update({f"device_{k}": v for k, v in dev.items()})
+            add["h2d_encode_d2h"] = (time.perf_counter() - t0) * 1000.0
+            for k, v in add.items():
+                timings[k] = timings.get(k, 0.0) + v
+        if trace is not None:
+            _collect_trace(ctx, 0, prep, stream, trace)
     return stream
 
 
@@ -633,7 +683,8 @@ class HostPipeline:
 
     def run(self, h_in, h_out, repeats: int = 1):
         """h_in[i]: pinned uint8 tensor of image i's RGBE bytes; h_out[i]: pinned
-        uint8 tensor of capacity >= stream_capacity.  Returns the stream lengths.
+        uint8 tensor for its stream (stream_capacity bytes always suffice; a
+        smaller buffer that turns out too short raises).  Returns the stream lengths.
         `repeats` > 1 streams the batch that many times back to back (one
         continuous pipeline, as for a stream of images)."""
         torch = self.torch
@@ -688,5 +739,8 @@ class HostPipeline:
             for k, i in enumerate(idx):
                 n = int(self.h_len[s][k])
                 lens[i] = n
+                if n > h_out[i].numel():
+                    raise RuntimeError(f"host output buffer of image {i} holds {h_out[i].numel()} bytes, "
+                                       f"its stream has {n}")
                 h_out[i][:n].copy_(self.d_out[s][oo[k]:oo[k] + n], non_blocking=True)
         self.slot_free[s].record(self.s_d2h)

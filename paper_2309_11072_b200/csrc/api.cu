@@ -61,6 +61,9 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
               uint64_t* d_out_len, cudaStream_t st, int mode) {
   if (n <= 0) return HDLL_B200_E_ARG;
   CK(cudaSetDevice(c->device));
+  // the arena, tables and status area are reused: a batch on another stream
+  // waits for the previous batch on the device
+  if (c->done_ev && c->last_stream != st) CK(cudaStreamWaitEvent(st, c->done_ev, 0));
   c->launches = 0;
   const bool any_trace = mode == 0;
   std::vector<ImgLayout> lays(n);
@@ -256,6 +259,7 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
     at.dct_split = dct_split;
     at.plane_out = ct_pln.out;
     at.plane_bits = ct_pln.bits;
+    at.err_acc = c->err_acc;
     launch_assemble(dd, n, at, max_out, st);
     c->launches += 1;
   }
@@ -270,6 +274,12 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   c->bits_off_dct = sc_dct.bits;
   c->bits_off_pln = sc_pln.bits;
   return HDLL_B200_OK;
+}
+
+// which coder bodies a decode job reads: sdr_only 0 all five, 1 the base layer
+// (decode_sdr), 2 body 1 alone as a lossless plane (the plane coder plugin)
+inline bool dec_uses(const hdll_b200_decode_image& di, int k) {
+  return di.sdr_only == 0 || (di.sdr_only == 1 && k == 0) || (di.sdr_only == 2 && k == 1);
 }
 
 // GPU decode of a batch (decode.cu); synchronous.
@@ -289,6 +299,7 @@ int run_decode(Ctx* c, const hdll_b200_decode_image* imgs, int n, uint8_t* const
     if (di.width == 0 || di.height == 0) return HDLL_B200_E_EMPTY;
     if (di.quality < 1 || di.quality > 100 || di.sigma_milli < 0 || di.radius < 0) return HDLL_B200_E_ARG;
     if (!di.sdr_only && di.slrme && di.sigma_milli && (!di.taps || di.radius < 1)) return HDLL_B200_E_ARG;
+    if (di.sdr_only < 0 || di.sdr_only > 2) return HDLL_B200_E_ARG;
     hdll_b200_image& im = ims[i];
     memset(&im, 0, sizeof(im));
     im.width = di.width;
@@ -302,7 +313,7 @@ int run_decode(Ctx* c, const hdll_b200_decode_image* imgs, int n, uint8_t* const
     lays[i] = plan(im, false);
     base[i] = total;
     total += lays[i].total;
-    for (int k = 0; k < 5; k++) total = align_up(total + (di.sdr_only && k ? 0 : di.body_len[k]) + 16);
+    for (int k = 0; k < 5; k++) total = align_up(total + (dec_uses(di, k) ? di.body_len[k] : 0) + 16);
   }
   if (ensure(&c->arena, &c->arena_cap, total, true)) return HDLL_B200_E_CUDA;
   uint8_t* A = (uint8_t*)c->arena;
@@ -337,13 +348,13 @@ int run_decode(Ctx* c, const hdll_b200_decode_image* imgs, int n, uint8_t* const
     d.decode = 1;
     d.hist_fused = 0;
     d.slrme = di.sdr_only ? 0 : di.slrme;
-    d.crc_mask = di.sdr_only ? 0x1 : 0x1F;
+    d.crc_mask = di.sdr_only == 1 ? 0x1 : (di.sdr_only == 2 ? 0x2 : 0x1F);
     d.out_rgbe = d_out[i];
     d.a32 = (float*)(D + stage(di.a32, 4 * 768));
     d.b32 = (float*)(D + stage(di.b32, 4 * 768));
     size_t o = base[i] + lays[i].total;
     for (int k = 0; k < 5; k++) {
-      const size_t len = di.sdr_only && k ? 0 : di.body_len[k];
+      const size_t len = dec_uses(di, k) ? di.body_len[k] : 0;
       d.pay[k] = A + o;
       d.pay_bytes[k] = (long long)len;
       if (len) CK(cudaMemcpyAsync(A + o, di.body[k], len, cudaMemcpyHostToDevice, st));
@@ -355,7 +366,7 @@ int run_decode(Ctx* c, const hdll_b200_decode_image* imgs, int n, uint8_t* const
     max_radius = std::max(max_radius, d.radius);
     max_base_tiles = std::max(max_base_tiles, (d.nbx + 15) / 16 * d.nby);
     any_real |= d.slrme && d.sigma_milli;
-    all_sdr &= di.sdr_only != 0;
+    all_sdr &= di.sdr_only == 1;
   }
   const long long crc_units = crc_assign_units(ds.data(), n);
   memcpy(H + t_descs, ds.data(), sizeof(ImgDesc) * n);
@@ -379,6 +390,7 @@ int run_decode(Ctx* c, const hdll_b200_decode_image* imgs, int n, uint8_t* const
   CK(cudaGetLastError());
   CK(cudaEventRecord(c->slot_ev[slot], st));
   CK(cudaStreamSynchronize(st));
+  c->dec_descs = ds;
   for (int i = 0; i < n; i++) {
     unsigned s = 0, crc[5] = {0, 0, 0, 0, 0};
     CK(cudaMemcpy(&s, ds[i].status, 4, cudaMemcpyDeviceToHost));
@@ -393,6 +405,8 @@ int run_decode(Ctx* c, const hdll_b200_decode_image* imgs, int n, uint8_t* const
   return HDLL_B200_OK;
 }
 
+// status of the last batch and of every encode batch since the previous
+// check (the accumulated word is read and cleared)
 int check_status(Ctx* c) {
   CK(cudaEventSynchronize(c->done_ev));
   unsigned worst = 0;
@@ -401,7 +415,10 @@ int check_status(Ctx* c) {
     CK(cudaMemcpy(&s, d.status, sizeof(s), cudaMemcpyDeviceToHost));
     worst |= s;
   }
-  return map_status(worst);
+  unsigned acc = 0;
+  CK(cudaMemcpy(&acc, c->err_acc, sizeof(acc), cudaMemcpyDeviceToHost));
+  if (acc) CK(cudaMemset(c->err_acc, 0, sizeof(acc)));
+  return map_status(worst | acc);
 }
 
 }  // namespace
@@ -415,6 +432,10 @@ int hdll_b200_ctx_create(hdll_b200_ctx** out, int device) {
   CK(cudaSetDevice(device));
   Ctx* c = new Ctx();
   c->device = device;
+  if (cudaMalloc(&c->err_acc, 256) != cudaSuccess || cudaMemset(c->err_acc, 0, 256) != cudaSuccess) {
+    delete c;
+    return HDLL_B200_E_CUDA;
+  }
   upload_base_constants();
   upload_crc_constants();
   upload_fit_constants();
@@ -442,6 +463,7 @@ void hdll_b200_ctx_destroy(hdll_b200_ctx* ctx) {
   band_free(c);
   if (c->plane_scratch) cudaFree(c->plane_scratch);
   if (c->hdr_buf) cudaFree(c->hdr_buf);
+  if (c->err_acc) cudaFree(c->err_acc);
   if (c->done_ev) cudaEventDestroy(c->done_ev);
   for (int k = 0; k <= kStages; k++)
     if (c->stage_ev[k]) cudaEventDestroy(c->stage_ev[k]);
@@ -458,6 +480,7 @@ int hdll_b200_encode_batch_device(hdll_b200_ctx* ctx, const hdll_b200_image* img
                                   const uint64_t* out_cap, uint64_t* d_out_len, void* stream) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c || !imgs || !d_out || !out_cap || !d_out_len) return HDLL_B200_E_ARG;
+  CtxLock lock(c);
   for (int i = 0; i < n; i++)
     if (out_cap[i] < hdll_b200_stream_capacity(imgs[i].width, imgs[i].height, imgs[i].hdr_pre_len, imgs[i].hdr_post_len))
       return HDLL_B200_E_CAPACITY;
@@ -469,6 +492,7 @@ int hdll_b200_encode_batch_device(hdll_b200_ctx* ctx, const hdll_b200_image* img
 int hdll_b200_sync(hdll_b200_ctx* ctx) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c) return HDLL_B200_E_ARG;
+  CtxLock lock(c);
   if (c->last_status) return c->last_status;
   if (!c->done_ev) return HDLL_B200_OK;
   return check_status(c);
@@ -478,6 +502,7 @@ int hdll_b200_encode_host(hdll_b200_ctx* ctx, const hdll_b200_image* img, uint8_
                           uint64_t* out_len) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c || !img || !h_out || !out_len) return HDLL_B200_E_ARG;
+  CtxLock lock(c);
   if (img->width == 0 || img->height == 0) return HDLL_B200_E_EMPTY;
   CK(cudaSetDevice(c->device));
   const size_t in_bytes = (size_t)img->width * img->height * 4;
@@ -507,9 +532,14 @@ int hdll_b200_encode_host(hdll_b200_ctx* ctx, const hdll_b200_image* img, uint8_
 
 int hdll_b200_trace(hdll_b200_ctx* ctx, int index, int which, uint8_t* h_dst, uint64_t nbytes) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
-  if (!c || index < 0 || index >= (int)c->descs.size() || !h_dst) return HDLL_B200_E_ARG;
-  const ImgDesc& d = c->descs[index];
-  CK(cudaEventSynchronize(c->done_ev));
+  if (!c || !h_dst) return HDLL_B200_E_ARG;
+  CtxLock lock(c);
+  const bool dec = (which & 16) != 0;  // the last decode batch (synchronous: already complete)
+  which &= 15;
+  const std::vector<ImgDesc>& dv = dec ? c->dec_descs : c->descs;
+  if (index < 0 || index >= (int)dv.size() || (dec && which != 1 && which != 3)) return HDLL_B200_E_ARG;
+  const ImgDesc& d = dv[index];
+  if (!dec) CK(cudaEventSynchronize(c->done_ev));
   const uint64_t n3 = 3 * (uint64_t)d.n;
   if (nbytes != n3) return HDLL_B200_E_ARG;
   if (which == 0 || which == 2) {
@@ -576,6 +606,7 @@ int hdll_b200_lossless_encode_plane(hdll_b200_ctx* ctx, const uint8_t* h_plane, 
                                     uint8_t* h_body, uint64_t cap, uint64_t* body_len, uint32_t* crc) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c || !h_plane || !h_body || !body_len || !crc) return HDLL_B200_E_ARG;
+  CtxLock lock(c);
   return plugin_common(c, h_plane, (size_t)w * h, w, h, 85, 1, h_body, cap, body_len, crc, nullptr);
 }
 
@@ -583,6 +614,7 @@ int hdll_b200_lossy_encode(hdll_b200_ctx* ctx, const uint8_t* h_rgb, uint32_t w,
                            uint8_t* h_body, uint64_t cap, uint64_t* body_len, uint8_t* h_decoded, uint32_t* crc) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c || !h_rgb || !h_body || !body_len || !crc || !h_decoded) return HDLL_B200_E_ARG;
+  CtxLock lock(c);
   if (quality < 1 || quality > 100) return HDLL_B200_E_ARG;
   return plugin_common(c, h_rgb, (size_t)w * h * 3, w, h, quality, 2, h_body, cap, body_len, crc, h_decoded);
 }
@@ -591,6 +623,7 @@ int hdll_b200_decode_batch(hdll_b200_ctx* ctx, const hdll_b200_decode_image* img
                            uint32_t* h_status, void* stream) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c || !imgs || !d_out || !h_status) return HDLL_B200_E_ARG;
+  CtxLock lock(c);
   return run_decode(c, imgs, n, d_out, h_status, (cudaStream_t)stream);
 }
 
@@ -602,6 +635,7 @@ int hdll_b200_last_launch_count(hdll_b200_ctx* ctx) {
 int hdll_b200_stage_times(hdll_b200_ctx* ctx, float* ms, int n) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c || !ms || n < kStages || !c->stage_ev[0]) return HDLL_B200_E_ARG;
+  CtxLock lock(c);
   CK(cudaEventSynchronize(c->stage_ev[kStages]));
   for (int k = 0; k < kStages; k++) {
     ms[k] = 0.f;

@@ -93,6 +93,12 @@ __global__ void __launch_bounds__(256) k_assemble(const ImgDesc* __restrict__ de
     L.total = o;
     if (blockIdx.x == 0) *d.out_len = (unsigned long long)o;
     if (o > d.out_cap) atomicOr(d.status, kErrCapacity);
+    // every earlier stage of this batch has finished (stream order); fold the
+    // image's status into the context's accumulated word
+    if (blockIdx.x == 0 && at.err_acc) {
+      const unsigned s = *(volatile unsigned*)d.status;
+      if (s) atomicOr(at.err_acc, s);
+    }
   }
   __syncthreads();
   const long long total = min(L.total, d.out_cap);

@@ -139,6 +139,7 @@ extern "C" {
 int hdll_b200_band_begin(hdll_b200_ctx* ctx, const hdll_b200_image* img, const hdll_b200_band* band, void* stream,
                          double* h_nodes, double* h_maxlw) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  CtxLock lock(c);
   if (!c || !img || !band || !h_nodes || !h_maxlw) return HDLL_B200_E_ARG;
   if (img->width == 0 || img->height == 0) return HDLL_B200_E_EMPTY;
   const auto& p = img->params;
@@ -272,6 +273,7 @@ int hdll_b200_band_begin(hdll_b200_ctx* ctx, const hdll_b200_image* img, const h
 int hdll_b200_band_layers(hdll_b200_ctx* ctx, const double* h_nodes_all, uint64_t n_nodes, double maxlw,
                           uint32_t* h_hist) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  CtxLock lock(c);
   Band* b = band_of(ctx);
   if (!b || !h_nodes_all || !h_hist || n_nodes != (1ULL << b->level) || !(maxlw >= 0.0)) return HDLL_B200_E_ARG;
   CK(cudaSetDevice(c->device));
@@ -299,6 +301,7 @@ int hdll_b200_band_layers(hdll_b200_ctx* ctx, const double* h_nodes_all, uint64_
 int hdll_b200_band_fit_send(hdll_b200_ctx* ctx, const uint32_t* owner_lo, int nowners, uint8_t* d_send,
                             uint64_t send_cap, uint64_t* h_send_bytes) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  CtxLock lock(c);
   Band* b = band_of(ctx);
   if (!b || !owner_lo || nowners < 1 || !h_send_bytes || b->hist.size() != 256) return HDLL_B200_E_ARG;
   CK(cudaSetDevice(c->device));
@@ -339,6 +342,7 @@ int hdll_b200_band_fit_owner(hdll_b200_ctx* ctx, const uint8_t* d_recv, const ui
                              const uint32_t* h_hist, int nsrc, uint32_t e_lo, uint32_t e_hi, float* h_a32,
                              float* h_b32, uint32_t* h_status) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  CtxLock lock(c);
   Band* b = band_of(ctx);
   if (!b || !h_recv_bytes || !h_hist || nsrc < 1 || e_lo > e_hi || e_hi > 256 || !h_a32 || !h_b32 || !h_status)
     return HDLL_B200_E_ARG;
@@ -450,6 +454,7 @@ int hdll_b200_band_fit_owner(hdll_b200_ctx* ctx, const uint8_t* d_recv, const ui
 
 int hdll_b200_band_code(hdll_b200_ctx* ctx, const float* h_a32, const float* h_b32, uint32_t* h_crc, int64_t* h_cnt) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  CtxLock lock(c);
   Band* b = band_of(ctx);
   if (!b || !h_a32 || !h_b32 || !h_crc || !h_cnt) return HDLL_B200_E_ARG;
   CK(cudaSetDevice(c->device));
@@ -469,6 +474,7 @@ int hdll_b200_band_code(hdll_b200_ctx* ctx, const float* h_a32, const float* h_b
 
 int hdll_b200_band_maps(hdll_b200_ctx* ctx, const int64_t* h_in_cnt, int64_t* h_maps) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  CtxLock lock(c);
   Band* b = band_of(ctx);
   if (!b || !h_in_cnt || !h_maps) return HDLL_B200_E_ARG;
   CK(cudaSetDevice(c->device));
@@ -486,6 +492,7 @@ int hdll_b200_band_maps(hdll_b200_ctx* ctx, const int64_t* h_in_cnt, int64_t* h_
 
 int hdll_b200_band_emit(hdll_b200_ctx* ctx, const int32_t* h_in_a, uint64_t* h_bits, uint64_t* h_piece_ptr) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  CtxLock lock(c);
   Band* b = band_of(ctx);
   if (!b || !h_in_a || !h_bits || !h_piece_ptr) return HDLL_B200_E_ARG;
   CK(cudaSetDevice(c->device));
@@ -507,6 +514,7 @@ int hdll_b200_assemble_pieces(hdll_b200_ctx* ctx, const hdll_b200_image* img, co
                               const uint64_t* piece_ptr, const uint64_t* piece_bits, uint8_t* d_out, uint64_t cap,
                               uint64_t* d_len, void* stream) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  CtxLock lock(c);
   if (!c || !img || !crc || !a32 || !b32 || !hist || !npieces || !piece_ptr || !piece_bits || !d_out || !d_len)
     return HDLL_B200_E_ARG;
   if (img->width == 0 || img->height == 0) return HDLL_B200_E_EMPTY;

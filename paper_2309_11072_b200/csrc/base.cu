@@ -54,8 +54,8 @@ __device__ __forceinline__ double rgbe_scale_b(unsigned e) {
 
 // srgb_quantize(pow(m, g)) = round_half_away(255 * clip(m^g, 0, 1)) for m >= 0.
 // The quantised byte only depends on which side of k + 0.5 the product lies,
-// so it is first evaluated in fp32 (log2f 1 ulp, exp2f 2 ulp: |err(255 m^g)|
-// < 2e-4 for g <= 50) and accepted when 255 m^g + 0.5 is more than kAmb away
+// so it is first evaluated in fp32 (log2f 1 ulp, exp2f 2 ulp, m rounded to fp32:
+// |err(255 m^g)| < 1e-3 for g <= 32, normal fp32 m) and accepted when 255 m^g + 0.5 is more than kAmb away
 // from an integer; otherwise the fp64 pow decides (as numpy's does; numpy's
 // own power is SVML, not correctly rounded).
 constexpr float kAmb = 2e-3f;
@@ -68,6 +68,9 @@ __device__ __noinline__ uint8_t quantize_pow_exact(double m, double g) {
 // For 1 / gamma <= 4 the fp32 pass uses the MUFU approximations (lg2 / ex2
 // .approx: ~2^-22 relative): |err(255 m^g)| stays below 4e-4, well inside kAmb.
 constexpr float kApproxMaxG = 4.0f;
+// The fp32 pass at all: |err(255 m^g)| ~ 255 g 2^-24 (m's rounding) + 2e-4 stays
+// below kAmb / 2 up to g = 32; larger 1 / gamma always takes the fp64 pow.
+constexpr float kFastMaxG = 32.0f;
 
 __device__ __forceinline__ float lg2_approx(float x) {
   float r;
@@ -94,6 +97,12 @@ __device__ __forceinline__ int quantize_pow_fast(double m, float g32, bool appro
   if (m >= 1.0) return 255;  // m^g >= 1 clips to 1
   if (m <= 0.0) return 0;
   const float mf = __double2float_rn(m);
+  // Outside the certified range the fp64 pow decides: an m below FLT_MIN has
+  // no normal fp32 image (lg2.approx.ftz flushes it, a subnormal loses bits,
+  // and a zero would give byte 0 where m^g can be far from 0 for small g);
+  // rounding m to fp32 contributes ~255 g 2^-24 to 255 m^g, inside kAmb only
+  // for g <= kFastMaxG.
+  if (!(mf >= 1.17549435e-38f) || g32 > kFastMaxG) return -1;
   const float y = 255.0f * (approx ? ex2_approx(g32 * lg2_approx(mf)) : exp2f(g32 * log2f(mf)));
   const float yf = y + 0.5f;
   const float fl = floorf(yf), fr = yf - fl;

@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(160) k_decode_coders(const ImgDesc* __restrict
   const ImgDesc& d = descs[blockIdx.x];
   if (threadIdx.x & 31) return;
   const int t = threadIdx.x >> 5;
+  if (d.crc_mask == 0x2 && t != 1) return;  // plane-only job: body 1 alone
   unsigned st = 0;
   if (t == 0) st = decode_dct_image(d);
   else if (with_planes) st = decode_plane_dev(d, t, dec_rows + (long long)(t - 1) * 2 * max_w);
@@ -259,6 +260,10 @@ __global__ void __launch_bounds__(256) k_decode_output(const ImgDesc* __restrict
   __syncthreads();
   const bool real = d.sigma_milli != 0;
   for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < d.n; p += (long long)gridDim.x * blockDim.x) {
+    if (d.crc_mask == 0x2) {  // plane-only job: the decoded plane itself
+      d.out_rgbe[p] = d.e_plane[p];
+      continue;
+    }
     if (sdr_only) {
 #pragma unroll
       for (int c = 0; c < 3; c++) d.out_rgbe[3 * p + c] = d.s_planes[(long long)c * d.n + p];

@@ -206,6 +206,7 @@ struct AsmTab {
   bool dct_split = false;
   uint8_t* const* plane_out;                 // [nimg*4] E, R, G, B plane byte streams
   const unsigned long long* plane_bits;      // [nimg*4]
+  unsigned* err_acc = nullptr;               // the context's accumulated status (Ctx::err_acc)
 };
 
 void upload_base_constants();

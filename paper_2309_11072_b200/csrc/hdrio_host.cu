@@ -93,6 +93,7 @@ extern "C" {
 int hdll_b200_hdr_decode(hdll_b200_ctx* ctx, const uint8_t* h_data, uint64_t len, uint32_t width, uint32_t height,
                          uint8_t* d_rgbe, uint64_t* h_consumed, int64_t* h_detail, void* stream) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  CtxLock lock(c);
   if (!c || (!h_data && len) || !d_rgbe || !h_consumed || !h_detail || width == 0 || height == 0)
     return HDLL_B200_E_ARG;
   CK(cudaSetDevice(c->device));
@@ -166,6 +167,7 @@ int hdll_b200_hdr_decode(hdll_b200_ctx* ctx, const uint8_t* h_data, uint64_t len
 int hdll_b200_hdr_encode(hdll_b200_ctx* ctx, const uint8_t* d_rgbe, uint32_t width, uint32_t height, int32_t rle,
                          uint8_t* h_out, uint64_t cap, uint64_t* h_len, void* stream) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  CtxLock lock(c);
   if (!c || !d_rgbe || !h_out || !h_len || width == 0 || height == 0) return HDLL_B200_E_ARG;
   CK(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;

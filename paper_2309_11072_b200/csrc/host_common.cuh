@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "../../include/hdll_b200.h"
@@ -76,7 +77,17 @@ constexpr size_t kEstatPerTile = 16 + 16 * kMaxCtx + sizeof(AMap) * kMaxCtx + 4 
 constexpr size_t kZeroBytes = 8 /*maxlw*/ + 8 /*status, amb*/ + 1024 /*bin_count*/ + 8 * 768 /*sum_y*/;
 
 struct Ctx {
+  // Every C entry point taking the context holds this lock (CtxLock), so
+  // threads sharing a context serialise instead of racing on the arena, the
+  // staging slots and the entropy status; a batch launched on another stream
+  // than the previous one waits for it on the device (run_batch).
+  std::recursive_mutex mu;
   int device = 0;
+  // device-side OR of every encode batch's image status words since the last
+  // hdll_b200_sync (k_assemble folds each image's word in), so an error in an
+  // earlier batch of a pipeline is not lost when a later batch reuses the
+  // descriptors
+  unsigned* err_acc = nullptr;
   void* arena = nullptr;
   size_t arena_cap = 0;
   // entropy status (epoch-tagged, zeroed once at allocation)
@@ -102,6 +113,7 @@ struct Ctx {
   // last batch (for traces / status)
   std::vector<ImgDesc> descs;
   std::vector<ImgLayout> lays;
+  std::vector<ImgDesc> dec_descs;  // last decode batch (hdll_b200_trace, which | 16)
   ImgDesc* d_descs = nullptr;
   // scratch for the host convenience path
   void* h2d = nullptr;
@@ -123,6 +135,13 @@ inline int cuda_fail(cudaError_t e, const char* what) {
   }
   return HDLL_B200_OK;
 }
+struct CtxLock {
+  std::unique_lock<std::recursive_mutex> g;
+  explicit CtxLock(Ctx* c) {
+    if (c) g = std::unique_lock<std::recursive_mutex>(c->mu);
+  }
+};
+
 #define CK(x)                                      \
   do {                                             \
     int _rc = cuda_fail((x), #x);                  \
@@ -458,7 +477,7 @@ inline int prepare_estat(Ctx* c, long long ntiles, cudaStream_t st) {
     long long cap = ntiles + ntiles / 4 + 1024;
     size_t bytes = (size_t)cap * kEstatPerTile;
     CK(cudaMalloc(&c->estat, bytes));
-    CK(cudaMemset(c->estat, 0, bytes));
+    CK(cudaMemsetAsync(c->estat, 0, bytes, st));
     c->estat_tiles = cap;
     c->epoch = 0;
   }

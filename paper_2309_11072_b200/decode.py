@@ -121,7 +121,20 @@ class _Job:
                 raise ChecksumError(f"{_NAMES[k]} payload failed its CRC-32 check")
 
 
-def _decode(streams, sdr_only: bool, device: int = 0):
+def _decode_trace(ctx, index: int, j: "_Job", px: np.ndarray, trace: dict):
+    """decode_hdr's trace hook (container.py:269-271): the decoded S and M*
+    (M* = (M - r) & 255, r the decoded residual planes)."""
+    n3 = 3 * j.w * j.h
+    buf = np.empty(n3, np.uint8)
+    _native.check(_native.lib().hdll_b200_trace(ctx.handle, index, 16 | 1, buf.ctypes.data, n3), "decode trace")
+    trace["s"] = SdrImage.from_array(buf.reshape(j.h, j.w, 3))
+    res = np.empty(n3, np.uint8)
+    _native.check(_native.lib().hdll_b200_trace(ctx.handle, index, 16 | 3, res.ctypes.data, n3), "decode trace")
+    res = res.reshape(3, j.h, j.w)
+    trace["m_star"] = tuple(((px[..., c].astype(np.int16) - res[c]) & 255).astype(np.uint8) for c in range(3))
+
+
+def _decode(streams, sdr_only: bool, device: int = 0, trace: dict | None = None):
     import torch
 
     jobs = []
@@ -140,13 +153,16 @@ def _decode(streams, sdr_only: bool, device: int = 0):
     status = np.zeros(len(jobs), np.uint32)
     ctx = _native.context(device)
     stream = torch.cuda.current_stream(dev)
-    _native.check(_native.lib().hdll_b200_decode_batch(ctx.handle, arr, len(jobs), ptrs,
-                                                       status.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
-                                                       stream.cuda_stream), "decode")
-    results = []
-    for j, o, s in zip(jobs, outs, status):
-        j.raise_first(int(s))
-        results.append(o.cpu().numpy().reshape(j.h, j.w, ch))
+    with ctx.lock:  # the trace reads this batch's planes
+        _native.check(_native.lib().hdll_b200_decode_batch(ctx.handle, arr, len(jobs), ptrs,
+                                                           status.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
+                                                           stream.cuda_stream), "decode")
+        results = []
+        for j, o, s in zip(jobs, outs, status):
+            j.raise_first(int(s))
+            results.append(o.cpu().numpy().reshape(j.h, j.w, ch))
+        if trace is not None and not sdr_only:
+            _decode_trace(ctx, 0, jobs[0], results[0], trace)
     return results
 
 
@@ -158,9 +174,11 @@ def decode_hdr_batch(streams, device: int = 0) -> list:
     return out
 
 
-def decode_hdr(stream: DualLayerStream, device: int = 0) -> RadianceImage:
-    """Reconstruct the original Radiance image (container.py:238-280)."""
-    return decode_hdr_batch([stream], device)[0]
+def decode_hdr(stream: DualLayerStream, trace: dict | None = None, device: int = 0) -> RadianceImage:
+    """Reconstruct the original Radiance image (container.py:238-280); `trace`
+    receives the decoded S and M* like the reference's hook."""
+    px = _decode([stream], False, device, trace)[0]
+    return RadianceImage(stream.width, stream.height, px, list(stream.header_vars), stream.resolution_orientation)
 
 
 def decode_sdr(stream: DualLayerStream, device: int = 0) -> SdrImage:

@@ -142,6 +142,18 @@ def main() -> int:
     for i, tmo in enumerate([dict(gamma=1.0), dict(gamma=0.2, key=0.36), dict(white_point=2.5, gamma=2.4),
                              dict(gamma=0.05, epsilon=1e-4), dict(key=0.05, white_point=0.5)]):
         run(f"tmo_{i}", synth.make_config(0, 200 + i, scale=0.09), [("FORMAT", "32-bit_rle_rgbe")], tmo=tmo)
+    # extreme 1 / gamma (the GPU's fp32 gamma pass stops at 1 / gamma = 32) and
+    # dark quads with E in {0, 1}: their radiance is subnormal in fp32, so the
+    # fp32 pass must hand them to the fp64 pow (m^g is far from 0 for small g)
+    for i, tmo in enumerate([dict(gamma=0.002), dict(gamma=0.005), dict(gamma=0.03)]):
+        run(f"tmo_x{i}", synth.make_config(0, 210 + i, scale=0.09), [("FORMAT", "32-bit_rle_rgbe")], tmo=tmo)
+    dark = synth.make_config(0, 220, scale=0.09)
+    drng = np.random.default_rng(220)
+    sel = drng.random(dark.shape[:2]) < 0.15
+    dark[sel, :3] = drng.integers(1, 256, (int(sel.sum()), 3), dtype=np.uint8)
+    dark[sel, 3] = drng.integers(0, 2, int(sel.sum()), dtype=np.uint8)
+    for i, tmo in enumerate([dict(gamma=20.0), dict(), dict(gamma=0.005), dict(gamma=100.0, key=0.5)]):
+        run(f"dark_{i}", dark, [("FORMAT", "32-bit_rle_rgbe")], tmo=tmo)
     # error parity
     run("err_sigma", rng.integers(0, 256, (4, 4, 4), dtype=np.uint8), [], sigma=70.0)
     run("err_quality", rng.integers(0, 256, (4, 4, 4), dtype=np.uint8), [], quality=0)
