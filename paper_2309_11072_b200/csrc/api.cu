@@ -154,7 +154,7 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
 
   long long max_n = 0, max_sort_tiles = 0, max_nodes = 0, max_out = 0;
   int max_w = 0, max_h = 0, max_radius = 0, max_level = 0, max_base_tiles = 0, max_chunks = 1;
-  bool any_real = false, any_slrme = false, any_non3 = false, any_hist = false;
+  bool any_real = false, any_slrme = false, any_non3 = false, any_hist = false, any_int = false, any_sortfit = false;
   for (int i = 0; i < n; i++) {
     const auto& im = imgs[i];
     const auto& p = im.params;
@@ -181,6 +181,8 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
     any_non3 |= (d.slrme && d.sigma_milli != 0 && d.radius != 3);
     any_slrme |= d.slrme != 0;
     any_hist |= (d.slrme && !d.fit_owner && !d.hist_fused);
+    any_int |= d.int_fit != 0;
+    any_sortfit |= (d.slrme && !d.int_fit);
   }
   const long long crc_units = crc_assign_units(ds.data(), n);
   memcpy(H + t_descs, ds.data(), sizeof(ImgDesc) * n);
@@ -221,9 +223,16 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
     c->launches += any_non3 ? 2 : 1;
   }
   mark(kStPrefilter);
-  if (mode == 0 && any_slrme) {
+  if (mode == 0 && any_sortfit) {  // sigma > 0: the order-replicating sums
     launch_fit(dd, n, (int)max_sort_tiles, max_nodes, max_chunks, st, any_hist);
     c->launches += any_hist ? 7 : 6;
+  } else if (mode == 0 && any_hist) {  // bin counts of sigma-0 global-regression images
+    launch_fit_hist(dd, n, (int)max_sort_tiles, st);
+    c->launches += 1;
+  }
+  if (mode == 0 && any_int) {  // sigma = 0: exact integer bins
+    launch_fit_int(dd, n, max_n, st);
+    c->launches += 2;
   }
   mark(kStFit);
   if (mode == 0) {

@@ -250,6 +250,7 @@ int hdll_b200_band_begin(hdll_b200_ctx* ctx, const hdll_b200_image* img, const h
   d.fit_m = rows * W;
   d.sort_tiles = (int)((d.fit_m + kSortTile - 1) / kSortTile);
   d.hist_fused = 0;  // the band's fit rows are a sub-range: k_sort_hist counts them
+  d.int_fit = 0;     // bins are fitted by their owner rank from the exchanged samples
   d.crc_p0 = d.fit_p0;
   d.crc_np = d.fit_m;
   b->crc_units = crc_assign_units(&d, 1);

@@ -49,6 +49,7 @@ struct ImgDesc {
   long long node0, node1;     // pairwise nodes (level tm_level) this desc sums
   long long fit_p0, fit_m;    // fit samples: desc pixels [fit_p0, fit_p0 + fit_m); xs/ys plane stride
   int fit_owner;              // 1: xs/ys/bin_* were filled by the exchange (skip the sort)
+  int int_fit;                // 1: sigma = 0 -- S* = S is integer, every sum exact: k_fit_int, no sort
   int hist_fused;             // 1: k_sdr_ycc builds the sort's tile histograms (whole-image fit)
   long long crc_p0, crc_np;   // CRC jobs cover desc pixels [crc_p0, crc_p0 + crc_np)
 
@@ -79,6 +80,7 @@ struct ImgDesc {
   unsigned* bin_count;        // 256
   unsigned* bin_start;        // 257
   long long* sum_y;           // [3][256] exact integer sums of M per bin
+  long long* isum;            // int_fit: [3][256][3] exact integer sums of x, x*x, x*y per bin
   double* seg_nodes;          // pairwise node values of every (channel, bin) segment
   int* seg_level;             // [3*256] L per segment
   long long* seg_node_off;    // [3*256+1] node offsets
@@ -232,6 +234,8 @@ void launch_fit(const ImgDesc*, int nimg, int max_sort_tiles, long long max_node
                 bool any_hist = true);
 void launch_fit_sort(const ImgDesc*, int nimg, int max_sort_tiles, cudaStream_t, bool any_hist = true);
 void launch_fit_bins(const ImgDesc*, int nimg, long long max_nodes, int max_chunks, cudaStream_t);
+void launch_fit_int(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
+void launch_fit_hist(const ImgDesc*, int nimg, int max_sort_tiles, cudaStream_t);
 struct RegroupTab {
   int nsrc;
   const uint8_t* recv;             // concatenated chunks, one per source rank

@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(256) k_sort_hist(const ImgDesc* __restrict__ d
 // [256][sort_tiles]): one CTA per bin, threads scan contiguous runs of tiles
 __global__ void __launch_bounds__(256) k_sort_scan(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
-  if (!d.slrme || d.fit_owner) return;
+  if (!d.slrme || d.fit_owner || d.int_fit) return;
   const int e = blockIdx.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
   __shared__ unsigned s_below, wsum[8];
   if (w == 0) {  // bin start: counts of the lower bins
@@ -109,7 +109,7 @@ struct ScatterSmem {
 
 __global__ void __launch_bounds__(256) k_sort_scatter(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
-  if (!d.slrme || d.fit_owner) return;
+  if (!d.slrme || d.fit_owner || d.int_fit) return;
   const int tile = blockIdx.x;
   if (tile >= d.sort_tiles) return;
   extern __shared__ __align__(16) uint8_t sm_raw[];
@@ -265,7 +265,7 @@ __device__ __forceinline__ XAcc x_acc(const ImgDesc& d, int c, const SegView& v)
 // exclusive scan of the node counts (2^L per non-empty segment)
 __global__ void __launch_bounds__(kSegs) k_seg_setup(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.x];
-  if (!d.slrme) return;
+  if (!d.slrme || d.int_fit) return;
   const int s = threadIdx.x;
   const SegView v = seg_view(d, s);
   const int L = v.n > 0 ? pairwise_level(v.n) : 0;
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(kSegs) k_seg_setup(const ImgDesc* __restrict__
 // one warp per depth-L node of a segment's pairwise tree
 __global__ void __launch_bounds__(128) k_seg_nodes(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
-  if (!d.slrme) return;
+  if (!d.slrme || d.int_fit) return;
   __shared__ PwScratch pw[4];
   const int warp = threadIdx.x >> 5;
   const long long g = (long long)blockIdx.x * 4 + warp;
@@ -453,7 +453,7 @@ struct DotSmem {
 // grid: (kSegs, nimg, max chunks); one warp per (segment, OpenBLAS thread-chunk)
 __global__ void __launch_bounds__(32) k_seg_dot(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
-  if (!d.slrme) return;
+  if (!d.slrme || d.int_fit) return;
   const int s = blockIdx.x;
   SegView v = seg_view(d, s);
   if (v.n == 0) return;
@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(32) k_seg_dot(const ImgDesc* __restrict__ desc
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_seg_reduce_coef(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
-  if (!d.slrme) return;
+  if (!d.slrme || d.int_fit) return;
   const int s = blockIdx.x;
   SegView v = seg_view(d, s);
   if (v.n == 0) return;
@@ -655,6 +655,126 @@ __global__ void __launch_bounds__(256) k_seg_reduce_coef(const ImgDesc* __restri
     d.b32[s] = b32;
   }
   if (!isfinite(a32) || !isfinite(b32)) atomicOr(d.status, kErrNonFinite);
+}
+
+// ---------------------------------------------------------------------------
+// sigma = 0 (north_star item 3): S* = S is an integer
+// plane, so every sum of fit_region (estimator.py:159-162) is an exact integer
+// below 2^53 whatever the order -- numpy's pairwise x.sum() and OpenBLAS's ddot
+// (FMA of integer products) included.  No sort: every CTA privatises
+// per-(channel, exponent) bins of sum x, sum y, sum x^2, sum x*y in shared
+// memory, lanes holding the same bin merge through warp reductions first, and
+// the CTA's bins are added into the image's int64 table with global atomics.
+// The coefficients then follow the reference's fp64 formula from the exact
+// sums (k_fit_int_coef), bit-identical to the order-replicating path.
+// ---------------------------------------------------------------------------
+struct IntFitSmem {
+  unsigned long long sxx[3][256], sxy[3][256];
+  unsigned sx[3][256], sy[3][256];
+};
+
+__global__ void __launch_bounds__(256) k_fit_int(const ImgDesc* __restrict__ descs) {
+  const ImgDesc& d = descs[blockIdx.y];
+  if (!d.int_fit) return;
+  __shared__ IntFitSmem sm;
+  for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) {
+    (&sm.sxx[0][0])[i] = 0ull;
+    (&sm.sxy[0][0])[i] = 0ull;
+    (&sm.sx[0][0])[i] = 0u;
+    (&sm.sy[0][0])[i] = 0u;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const bool global = d.global_regression != 0;
+  const long long n = d.n;
+  const uint32_t* px = reinterpret_cast<const uint32_t*>(d.rgbe);
+  const uint8_t* S = d.s_planes;
+  // one pixel per lane per step; the grid stride keeps warps on whole 32-pixel rows of memory
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long b0 = (long long)blockIdx.x * blockDim.x; b0 < n; b0 += stride) {
+    const long long p = b0 + threadIdx.x;
+    const bool valid = p < n;
+    const unsigned act = __ballot_sync(0xffffffffu, valid);
+    if (!valid) continue;
+    const uint32_t q = __ldg(px + p);
+    const unsigned key = global ? 0u : (q >> 24);  // global_regression: one (c, 0) segment per plane
+    const unsigned peers = __match_any_sync(act, key);
+    const bool leader = (peers & lt) == 0;
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      const unsigned x = __ldg(S + (long long)c * n + p), y = (q >> (8 * c)) & 0xFFu;
+      // a warp's partial sums fit 32 bits (32 * 255^2 < 2^21)
+      const unsigned rx = __reduce_add_sync(peers, x), ry = __reduce_add_sync(peers, y);
+      const unsigned rxx = __reduce_add_sync(peers, x * x), rxy = __reduce_add_sync(peers, x * y);
+      if (leader) {
+        atomicAdd(&sm.sx[c][key], rx);
+        atomicAdd(&sm.sy[c][key], ry);
+        atomicAdd(&sm.sxx[c][key], (unsigned long long)rxx);
+        atomicAdd(&sm.sxy[c][key], (unsigned long long)rxy);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) {
+    const unsigned long long xx = (&sm.sxx[0][0])[i];
+    if (xx == 0ull && (&sm.sy[0][0])[i] == 0u && (&sm.sx[0][0])[i] == 0u) continue;  // empty (or all-zero) bin
+    unsigned long long* g = reinterpret_cast<unsigned long long*>(d.isum) + 3 * i;
+    atomicAdd(g + 0, (unsigned long long)(&sm.sx[0][0])[i]);
+    atomicAdd(g + 1, xx);
+    atomicAdd(g + 2, (&sm.sxy[0][0])[i]);
+    atomicAdd(reinterpret_cast<unsigned long long*>(d.sum_y) + i, (unsigned long long)(&sm.sy[0][0])[i]);
+  }
+}
+
+// fit_region (estimator.py:145-169) from the exact sums, one thread per segment
+__global__ void __launch_bounds__(256) k_fit_int_coef(const ImgDesc* __restrict__ descs) {
+  const ImgDesc& d = descs[blockIdx.y];
+  if (!d.int_fit) return;
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= kSegs) return;
+  const int c = s >> 8, e = s & 255;
+  const long long nn = d.global_regression ? (e == 0 ? d.n : 0) : (long long)d.bin_count[e];
+  if (nn == 0) return;
+  const long long* g = d.isum + 3 * s;
+  const double sx = (double)g[0], sxx = (double)g[1], sxy = (double)g[2];  // exact: < 2^53
+  const double sy = (double)d.sum_y[s];
+  const double dn = (double)nn;
+  double a = 0.0, b = sy / dn;
+  const double den = dn * sxx - sx * sx;
+  if (den > 0.0) {
+    const double aa = (dn * sxy - sx * sy) / den;
+    const double bb = (sy - aa * sx) / dn;
+    if (isfinite(aa) && isfinite(bb)) {
+      a = aa;
+      b = bb;
+    }
+  }
+  const float a32 = __double2float_rn(a), b32 = __double2float_rn(b);
+  if (d.global_regression) {
+    for (int k = 0; k < 256; k++) {
+      d.a32[c * 256 + k] = a32;
+      d.b32[c * 256 + k] = b32;
+    }
+  } else {
+    d.a32[s] = a32;
+    d.b32[s] = b32;
+  }
+  if (!isfinite(a32) || !isfinite(b32)) atomicOr(d.status, kErrNonFinite);
+}
+
+void launch_fit_int(const ImgDesc* d_descs, int nimg, long long max_n, cudaStream_t st) {
+  // about 4 CTAs per SM over the batch, each striding over its image
+  long long gx = (max_n + 255) / 256;
+  const long long cap = (148 * 4 + nimg - 1) / nimg;
+  if (gx > cap) gx = cap;
+  if (gx < 1) gx = 1;
+  k_fit_int<<<dim3((unsigned)gx, nimg), 256, 0, st>>>(d_descs);
+  k_fit_int_coef<<<dim3(kSegs / 256, nimg), 256, 0, st>>>(d_descs);
+}
+
+void launch_fit_hist(const ImgDesc* d_descs, int nimg, int max_sort_tiles, cudaStream_t st) {
+  k_sort_hist<<<dim3(max_sort_tiles, nimg), 256, 0, st>>>(d_descs);
 }
 
 void launch_fit_sort(const ImgDesc* d_descs, int nimg, int max_sort_tiles, cudaStream_t st, bool any_hist) {

@@ -74,7 +74,8 @@ enum { kStTonemap, kStBase, kStPrefilter, kStFit, kStEstimate, kStCrc, kStEntrop
 
 constexpr size_t kEstatPerTile = 16 + 16 * kMaxCtx + sizeof(AMap) * kMaxCtx + 4 * kMaxCtx + 16 + 8;
 
-constexpr size_t kZeroBytes = 8 /*maxlw*/ + 8 /*status, amb*/ + 1024 /*bin_count*/ + 8 * 768 /*sum_y*/;
+constexpr size_t kZeroBytes = 8 /*maxlw*/ + 8 /*status, amb*/ + 1024 /*bin_count*/ + 8 * 768 /*sum_y*/ +
+                              8 * 3 * 768 /*isum*/;
 
 struct Ctx {
   // Every C entry point taking the context holds this lock (CtxLock), so
@@ -426,6 +427,8 @@ inline void fill_desc(ImgDesc& d, const hdll_b200_image& im, const ImgLayout& L,
   d.amb_cap = (unsigned)amb_cap(d.n);
   d.bin_count = (unsigned*)(B + L.off_zero + 16);
   d.sum_y = (long long*)(B + L.off_zero + 16 + 1024);
+  d.isum = (long long*)(B + L.off_zero + 16 + 1024 + 8 * 768);
+  d.int_fit = (mode == 0 && p.slrme && p.sigma_milli == 0) ? 1 : 0;
   d.full_n = d.n;
   d.pix_base = 0;
   d.node0 = 0;
