@@ -200,6 +200,15 @@ int hdll_b200_band_begin(hdll_b200_ctx *ctx, const hdll_b200_image *img, const h
  * the band's fit samples by exponent.  Out: the band's exponent histogram. */
 int hdll_b200_band_layers(hdll_b200_ctx *ctx, const double *h_nodes_all, uint64_t n_nodes, double maxlw,
                           uint32_t *h_hist);
+/* Phases 3-4 for sigma = 0 (S* = S: every regression sum is an exact integer).
+ * fit_sums: the band's table, int64 [3][256][3] sums of x, x^2, x*y then
+ * [3][256] sums of y (3072 values, 24 KB).  Exchange: all-reduce (sum) of the
+ * tables and of the histograms.  fit_coef: the coefficients from the summed
+ * table and histogram -- identical on every rank, no sample crosses ranks.
+ * Out: a32/b32 [3][256], error bits. */
+int hdll_b200_band_fit_sums(hdll_b200_ctx *ctx, int64_t *h_sums);
+int hdll_b200_band_fit_coef(hdll_b200_ctx *ctx, const int64_t *h_sums, const uint32_t *h_hist, float *h_a32,
+                            float *h_b32, uint32_t *h_status);
 /* Phase 3: pack the sorted samples for their owners (owner o fits exponents
  * [owner_lo[o], owner_lo[o+1])) into d_send; h_send_bytes[o] = chunk sizes.
  * Exchange: all-to-all of the chunks. */
@@ -211,16 +220,26 @@ int hdll_b200_band_fit_send(hdll_b200_ctx *ctx, const uint32_t *owner_lo, int no
 int hdll_b200_band_fit_owner(hdll_b200_ctx *ctx, const uint8_t *d_recv, const uint64_t *h_recv_bytes,
                              const uint32_t *h_hist, int nsrc, uint32_t e_lo, uint32_t e_hi, float *h_a32,
                              float *h_b32, uint32_t *h_status);
-/* Phase 5: estimate with the full table, CRCs of the band's rows, context
- * counts of every piece.  Out: crc[5], counts [7][6].  Exchange: allgather counts. */
-int hdll_b200_band_code(hdll_b200_ctx *ctx, const float *h_a32, const float *h_b32, uint32_t *h_crc,
-                        int64_t *h_cnt);
-/* Phase 6: A-maps of every piece given the counts before it.  Out: [7][6][3]
- * (c, s, t of common.cuh AMap).  Exchange: allgather maps. */
-int hdll_b200_band_maps(hdll_b200_ctx *ctx, const int64_t *h_in_cnt, int64_t *h_maps);
-/* Phase 7: code every piece given its entering A.  Out: bit lengths [7] and
- * the device addresses of the piece streams (valid until the next begin). */
-int hdll_b200_band_emit(hdll_b200_ctx *ctx, const int32_t *h_in_a, uint64_t *h_bits, uint64_t *h_piece_ptr);
+/* Phase 5: estimate with the full table, CRCs of the band's rows, and a coder
+ * pass over the pieces.  A piece with h_first[k] set starts its chain (the
+ * first rank's Y, Cb and plane pieces: nothing enters them) and is coded now
+ * from the reset state -- its outgoing A h_out_a[k][6] (the next piece's
+ * entering A, no map of it needed), bit length h_bits[k] and stream are final;
+ * the other pieces are only counted.  Out: crc[5], counts [7][6] of every
+ * piece, piece stream addresses (valid until the next begin).
+ * Exchange: allgather counts (and the first pieces' outgoing A). */
+int hdll_b200_band_code(hdll_b200_ctx *ctx, const float *h_a32, const float *h_b32, const int32_t *h_first,
+                        uint32_t *h_crc, int64_t *h_cnt, int32_t *h_out_a, uint64_t *h_bits, uint64_t *h_piece_ptr);
+/* Phase 6: A-maps of the pieces with h_need[k] set (a later piece of the chain
+ * composes them; not the chain's first or last piece) given the counts before
+ * them.  Out: [7][6][3] (c, s, t of common.cuh AMap).  Exchange: allgather
+ * maps (skipped when no rank needs one). */
+int hdll_b200_band_maps(hdll_b200_ctx *ctx, const int64_t *h_in_cnt, const int32_t *h_need, int64_t *h_maps);
+/* Phase 7: code the pieces with h_emit[k] set (those not coded in phase 5)
+ * given their entering counts and A.  Out: bit lengths [7] (emitted pieces)
+ * and the device addresses of the piece streams. */
+int hdll_b200_band_emit(hdll_b200_ctx *ctx, const int64_t *h_in_cnt, const int32_t *h_in_a, const int32_t *h_emit,
+                        uint64_t *h_bits, uint64_t *h_piece_ptr);
 /* Rank 0: concatenate the pieces of the 5 chains (npieces[k] each, in order;
  * piece_ptr device addresses, piece_bits lengths) and serialize the stream
  * with the combined CRCs, table and full-image exponent histogram. */

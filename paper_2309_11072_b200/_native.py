@@ -22,7 +22,8 @@ EXPORTS = (
     "hdll_b200_encode_batch_device", "hdll_b200_sync", "hdll_b200_encode_host", "hdll_b200_trace",
     "hdll_b200_lossless_encode_plane", "hdll_b200_lossy_encode", "hdll_b200_last_launch_count",
     "hdll_b200_stage_times", "hdll_b200_status_string",
-    "hdll_b200_band_begin", "hdll_b200_band_layers", "hdll_b200_band_fit_send", "hdll_b200_band_fit_owner",
+    "hdll_b200_band_begin", "hdll_b200_band_layers", "hdll_b200_band_fit_sums", "hdll_b200_band_fit_coef",
+    "hdll_b200_band_fit_send", "hdll_b200_band_fit_owner",
     "hdll_b200_band_code", "hdll_b200_band_maps", "hdll_b200_band_emit", "hdll_b200_assemble_pieces",
     "hdll_b200_decode_batch", "hdll_b200_hdr_decode", "hdll_b200_hdr_encode",
 )
@@ -109,15 +110,18 @@ def lib():
             L.hdll_b200_status_string.restype = ctypes.c_char_p
             dp, i64p = ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)
             u32p, f32p = ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_float)
+            i32p = ctypes.POINTER(ctypes.c_int32)
             sig = {
                 "hdll_b200_band_begin": [vp, ctypes.POINTER(Image), ctypes.POINTER(Band), vp, dp, dp],
                 "hdll_b200_band_layers": [vp, dp, ctypes.c_uint64, ctypes.c_double, u32p],
                 "hdll_b200_band_fit_send": [vp, u32p, ctypes.c_int, vp, ctypes.c_uint64, u64p],
                 "hdll_b200_band_fit_owner": [vp, vp, u64p, u32p, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32,
                                              f32p, f32p, u32p],
-                "hdll_b200_band_code": [vp, f32p, f32p, u32p, i64p],
-                "hdll_b200_band_maps": [vp, i64p, i64p],
-                "hdll_b200_band_emit": [vp, ctypes.POINTER(ctypes.c_int32), u64p, u64p],
+                "hdll_b200_band_fit_sums": [vp, i64p],
+                "hdll_b200_band_fit_coef": [vp, i64p, u32p, f32p, f32p, u32p],
+                "hdll_b200_band_code": [vp, f32p, f32p, i32p, u32p, i64p, i32p, u64p, u64p],
+                "hdll_b200_band_maps": [vp, i64p, i32p, i64p],
+                "hdll_b200_band_emit": [vp, i64p, i32p, i32p, u64p, u64p],
                 "hdll_b200_assemble_pieces": [vp, ctypes.POINTER(Image), u32p, f32p, f32p, u32p,
                                               ctypes.POINTER(ctypes.c_int32), u64p, u64p, vp, ctypes.c_uint64, vp, vp],
                 "hdll_b200_decode_batch": [vp, ctypes.POINTER(DecodeImage), ctypes.c_int,

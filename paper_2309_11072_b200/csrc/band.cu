@@ -57,6 +57,7 @@ struct Band {
   HostChains hc_dct, hc_pln;
   HostChains::Staged sc_dct{}, sc_pln{};
   int* d_ticket = nullptr;
+  size_t t_cmode = 0;  // per-chain modes in tabs: DCT chains at +0, plane chains at +16
 };
 
 void band_free(Ctx* c) {
@@ -87,25 +88,39 @@ int sync_status(Band* b) {
   return HDLL_B200_OK;
 }
 
-// run the 7 chains in `mode` (entropy.cu ChainTab::mode)
-int run_chains(Ctx* c, Band* b, int mode) {
+// run the 7 piece chains, piece k in modes[k] (entropy.cu ChainTab: 0 code,
+// 1 counts, 2 A-maps, kModeSkip not run)
+int run_chains(Ctx* c, Band* b, const int* modes) {
+  int pres_dct = 0, pres_pln = 0;
+  for (int k = 0; k < kPieces; k++)
+    if (modes[k] != kModeSkip) (k < 3 ? pres_dct : pres_pln) |= 1 << modes[k];
+  if (!pres_dct && !pres_pln) return HDLL_B200_OK;
   const long long ntiles = b->hc_dct.ntiles() + b->hc_pln.ntiles();
   if (int rc = prepare_estat(c, ntiles, b->st)) return rc;
   CK(cudaMemsetAsync(b->d_ticket, 0, 16, b->st));
   uint8_t* D = (uint8_t*)b->tabs;
+  CK(cudaMemcpyAsync(D + b->t_cmode, modes, 4 * 3, cudaMemcpyHostToDevice, b->st));
+  CK(cudaMemcpyAsync(D + b->t_cmode + 16, modes + 3, 4 * 4, cudaMemcpyHostToDevice, b->st));
   uint8_t* E = (uint8_t*)c->estat;
-  ChainTab ct_dct = b->hc_dct.table(b->sc_dct, D, E, c->estat_tiles, 0, b->d_ticket, c->epoch, mode);
-  ChainTab ct_pln = b->hc_pln.table(b->sc_pln, D, E, c->estat_tiles, b->hc_dct.ntiles(), b->d_ticket + 2, c->epoch, mode);
+  ChainTab ct_dct = b->hc_dct.table(b->sc_dct, D, E, c->estat_tiles, 0, b->d_ticket, c->epoch, 0);
+  ChainTab ct_pln = b->hc_pln.table(b->sc_pln, D, E, c->estat_tiles, b->hc_dct.ntiles(), b->d_ticket + 2, c->epoch, 0);
+  ct_dct.chain_mode = (const int*)(D + b->t_cmode);
+  ct_pln.chain_mode = (const int*)(D + b->t_cmode + 16);
+  ct_dct.modes_present = pres_dct;
+  ct_pln.modes_present = pres_pln;
   if (ensure(&c->plane_scratch, &c->plane_scratch_cap,
              std::max(dct_scratch_bytes(ct_dct), plane_scratch_bytes(ct_pln, b->W)), true))
     return HDLL_B200_E_CUDA;
-  launch_entropy_dct(b->d_desc, ct_dct, c->plane_scratch, b->st);
-  launch_entropy_fixup(ct_dct, b->st);
-  if (ensure(&c->plane_scratch, &c->plane_scratch_cap, plane_scratch_bytes(ct_pln, b->W), true))
-    return HDLL_B200_E_CUDA;
-  launch_entropy_plane(b->d_desc, ct_pln, b->W, c->plane_scratch, b->st);
-  launch_entropy_fixup(ct_pln, b->st);
-  c->launches += 4;
+  if (pres_dct) {
+    launch_entropy_dct(b->d_desc, ct_dct, c->plane_scratch, b->st);
+    launch_entropy_fixup(ct_dct, b->st);
+    c->launches += 2;
+  }
+  if (pres_pln) {
+    launch_entropy_plane(b->d_desc, ct_pln, b->W, c->plane_scratch, b->st);
+    launch_entropy_fixup(ct_pln, b->st);
+    c->launches += 2;
+  }
   return sync_status(b);
 }
 
@@ -238,6 +253,7 @@ int hdll_b200_band_begin(hdll_b200_ctx* ctx, const hdll_b200_image* img, const h
   b->sc_dct = b->hc_dct.stage(stage);
   b->sc_pln = b->hc_pln.stage(stage);
   const size_t t_ticket = stage(nullptr, 16);
+  b->t_cmode = stage(nullptr, 32);
   ImgDesc& d = b->desc;
   fill_desc(d, b->im, b->L, B, 0, false, D, sp);
   d.full_n = full_n;
@@ -250,7 +266,9 @@ int hdll_b200_band_begin(hdll_b200_ctx* ctx, const hdll_b200_image* img, const h
   d.fit_m = rows * W;
   d.sort_tiles = (int)((d.fit_m + kSortTile - 1) / kSortTile);
   d.hist_fused = 0;  // the band's fit rows are a sub-range: k_sort_hist counts them
-  d.int_fit = 0;     // bins are fitted by their owner rank from the exchanged samples
+  // sigma > 0: bins are fitted by their owner rank from the exchanged samples;
+  // sigma = 0 (int_fit from fill_desc): every rank sums its rows' exact
+  // integer bins and the ranks all-reduce the table (hdll_b200_band_fit_sums)
   d.crc_p0 = d.fit_p0;
   d.crc_np = d.fit_m;
   b->crc_units = crc_assign_units(&d, 1);
@@ -289,7 +307,12 @@ int hdll_b200_band_layers(hdll_b200_ctx* ctx, const double* h_nodes_all, uint64_
     c->launches += 2;
   }
   b->hist.assign(256, 0);
-  if (d.slrme) {
+  if (d.slrme && d.int_fit) {  // sigma = 0: the band's exact bin sums, no sort
+    launch_fit_hist(b->d_desc, 1, d.sort_tiles, b->st);
+    launch_fit_int_sums(b->d_desc, 1, d.fit_m, b->st);
+    c->launches += 2;
+    CK(cudaMemcpyAsync(b->hist.data(), d.bin_count, 4 * 256, cudaMemcpyDeviceToHost, b->st));
+  } else if (d.slrme) {
     launch_fit_sort(b->d_desc, 1, d.sort_tiles, b->st);
     c->launches += 3;
     CK(cudaMemcpyAsync(b->hist.data(), d.bin_count, 4 * 256, cudaMemcpyDeviceToHost, b->st));
@@ -297,6 +320,40 @@ int hdll_b200_band_layers(hdll_b200_ctx* ctx, const double* h_nodes_all, uint64_
   if (int rc = sync_status(b)) return rc;
   memcpy(h_hist, b->hist.data(), 4 * 256);
   return HDLL_B200_OK;
+}
+
+int hdll_b200_band_fit_sums(hdll_b200_ctx* ctx, int64_t* h_sums) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  CtxLock lock(c);
+  Band* b = band_of(ctx);
+  if (!b || !h_sums || !b->desc.int_fit) return HDLL_B200_E_ARG;
+  CK(cudaSetDevice(c->device));
+  const ImgDesc& d = b->desc;
+  CK(cudaMemcpyAsync(h_sums, d.isum, 8 * 3 * 768, cudaMemcpyDeviceToHost, b->st));
+  CK(cudaMemcpyAsync(h_sums + 3 * 768, d.sum_y, 8 * 768, cudaMemcpyDeviceToHost, b->st));
+  return sync_status(b);
+}
+
+int hdll_b200_band_fit_coef(hdll_b200_ctx* ctx, const int64_t* h_sums, const uint32_t* h_hist, float* h_a32,
+                            float* h_b32, uint32_t* h_status) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  CtxLock lock(c);
+  Band* b = band_of(ctx);
+  if (!b || !h_sums || !h_hist || !h_a32 || !h_b32 || !h_status || !b->desc.int_fit) return HDLL_B200_E_ARG;
+  CK(cudaSetDevice(c->device));
+  const ImgDesc& d = b->desc;
+  // the whole image's table replaces the band's: counts, sums of x, x^2, x*y and y
+  CK(cudaMemcpyAsync(d.bin_count, h_hist, 4 * 256, cudaMemcpyHostToDevice, b->st));
+  CK(cudaMemcpyAsync(d.isum, h_sums, 8 * 3 * 768, cudaMemcpyHostToDevice, b->st));
+  CK(cudaMemcpyAsync(d.sum_y, h_sums + 3 * 768, 8 * 768, cudaMemcpyHostToDevice, b->st));
+  CK(cudaMemsetAsync(d.a32, 0, 4 * 768, b->st));
+  CK(cudaMemsetAsync(d.b32, 0, 4 * 768, b->st));
+  launch_fit_int_coef(b->d_desc, 1, b->st);
+  c->launches += 1;
+  CK(cudaMemcpyAsync(h_a32, d.a32, 4 * 768, cudaMemcpyDeviceToHost, b->st));
+  CK(cudaMemcpyAsync(h_b32, d.b32, 4 * 768, cudaMemcpyDeviceToHost, b->st));
+  CK(cudaMemcpyAsync(h_status, d.status, 4, cudaMemcpyDeviceToHost, b->st));
+  return sync_status(b);
 }
 
 int hdll_b200_band_fit_send(hdll_b200_ctx* ctx, const uint32_t* owner_lo, int nowners, uint8_t* d_send,
@@ -453,11 +510,25 @@ int hdll_b200_band_fit_owner(hdll_b200_ctx* ctx, const uint8_t* d_recv, const ui
   return sync_status(b);
 }
 
-int hdll_b200_band_code(hdll_b200_ctx* ctx, const float* h_a32, const float* h_b32, uint32_t* h_crc, int64_t* h_cnt) {
+}  // extern "C"
+
+namespace {
+void piece_bits(Band* b, uint64_t* h_bits) {
+  uint8_t* D = (uint8_t*)b->tabs;
+  cudaMemcpy(h_bits, D + b->sc_dct.bits, 8 * 3, cudaMemcpyDeviceToHost);
+  cudaMemcpy(h_bits + 3, D + b->sc_pln.bits, 8 * 4, cudaMemcpyDeviceToHost);
+}
+}  // namespace
+
+extern "C" {
+
+int hdll_b200_band_code(hdll_b200_ctx* ctx, const float* h_a32, const float* h_b32, const int32_t* h_first,
+                        uint32_t* h_crc, int64_t* h_cnt, int32_t* h_out_a, uint64_t* h_bits, uint64_t* h_piece_ptr) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   CtxLock lock(c);
   Band* b = band_of(ctx);
-  if (!b || !h_a32 || !h_b32 || !h_crc || !h_cnt) return HDLL_B200_E_ARG;
+  if (!b || !h_a32 || !h_b32 || !h_first || !h_crc || !h_cnt || !h_out_a || !h_bits || !h_piece_ptr)
+    return HDLL_B200_E_ARG;
   CK(cudaSetDevice(c->device));
   const ImgDesc& d = b->desc;
   CK(cudaMemcpyAsync(d.a32, h_a32, 4 * 768, cudaMemcpyHostToDevice, b->st));
@@ -466,21 +537,34 @@ int hdll_b200_band_code(hdll_b200_ctx* ctx, const float* h_a32, const float* h_b
   launch_crc(b->d_desc, 1, b->crc_units, b->st);
   c->launches += 3;
   CK(cudaMemcpyAsync(h_crc, d.crc, 4 * 5, cudaMemcpyDeviceToHost, b->st));
-  if (int rc = run_chains(c, b, 1)) return rc;
+  // a piece that starts its chain is coded now from the reset state (count 0,
+  // A = 4); the others only count their symbols per context
+  std::vector<long long> zc(kPieces * kMaxCtx, 0);
+  std::vector<int> a4(kPieces * kMaxCtx, 4);
+  if (int rc = pieces_to_dev(b, b->sc_dct.in_cnt, b->sc_pln.in_cnt, zc.data())) return rc;
+  if (int rc = pieces_to_dev(b, b->sc_dct.in_a, b->sc_pln.in_a, a4.data())) return rc;
+  int modes[kPieces];
+  for (int k = 0; k < kPieces; k++) modes[k] = h_first[k] ? 0 : 1;
+  if (int rc = run_chains(c, b, modes)) return rc;
   if (int rc = pieces_from_dev(b, b->sc_dct.out_cnt, b->sc_pln.out_cnt, (long long*)h_cnt)) return rc;
+  if (int rc = pieces_from_dev(b, b->sc_dct.out_a, b->sc_pln.out_a, (int*)h_out_a)) return rc;
+  piece_bits(b, h_bits);
+  for (int k = 0; k < kPieces; k++) h_piece_ptr[k] = (uint64_t)(uintptr_t)b->piece_ptr[k];
   unsigned s = 0;
   CK(cudaMemcpy(&s, d.status, 4, cudaMemcpyDeviceToHost));
   return map_status(s);
 }
 
-int hdll_b200_band_maps(hdll_b200_ctx* ctx, const int64_t* h_in_cnt, int64_t* h_maps) {
+int hdll_b200_band_maps(hdll_b200_ctx* ctx, const int64_t* h_in_cnt, const int32_t* h_need, int64_t* h_maps) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   CtxLock lock(c);
   Band* b = band_of(ctx);
-  if (!b || !h_in_cnt || !h_maps) return HDLL_B200_E_ARG;
+  if (!b || !h_in_cnt || !h_need || !h_maps) return HDLL_B200_E_ARG;
   CK(cudaSetDevice(c->device));
   if (int rc = pieces_to_dev(b, b->sc_dct.in_cnt, b->sc_pln.in_cnt, (const long long*)h_in_cnt)) return rc;
-  if (int rc = run_chains(c, b, 2)) return rc;
+  int modes[kPieces];
+  for (int k = 0; k < kPieces; k++) modes[k] = h_need[k] ? 2 : kModeSkip;
+  if (int rc = run_chains(c, b, modes)) return rc;
   AMap m[kPieces * kMaxCtx];
   if (int rc = pieces_from_dev(b, b->sc_dct.out_map, b->sc_pln.out_map, m)) return rc;
   for (int i = 0; i < kPieces * kMaxCtx; i++) {
@@ -491,19 +575,21 @@ int hdll_b200_band_maps(hdll_b200_ctx* ctx, const int64_t* h_in_cnt, int64_t* h_
   return HDLL_B200_OK;
 }
 
-int hdll_b200_band_emit(hdll_b200_ctx* ctx, const int32_t* h_in_a, uint64_t* h_bits, uint64_t* h_piece_ptr) {
+int hdll_b200_band_emit(hdll_b200_ctx* ctx, const int64_t* h_in_cnt, const int32_t* h_in_a, const int32_t* h_emit,
+                        uint64_t* h_bits, uint64_t* h_piece_ptr) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   CtxLock lock(c);
   Band* b = band_of(ctx);
-  if (!b || !h_in_a || !h_bits || !h_piece_ptr) return HDLL_B200_E_ARG;
+  if (!b || !h_in_cnt || !h_in_a || !h_emit || !h_bits || !h_piece_ptr) return HDLL_B200_E_ARG;
   CK(cudaSetDevice(c->device));
   for (int i = 0; i < kPieces * kMaxCtx; i++)
     if (h_in_a[i] < 0 || h_in_a[i] >= kADomain) return HDLL_B200_E_ARG;
+  if (int rc = pieces_to_dev(b, b->sc_dct.in_cnt, b->sc_pln.in_cnt, (const long long*)h_in_cnt)) return rc;
   if (int rc = pieces_to_dev(b, b->sc_dct.in_a, b->sc_pln.in_a, (const int*)h_in_a)) return rc;
-  if (int rc = run_chains(c, b, 0)) return rc;
-  uint8_t* D = (uint8_t*)b->tabs;
-  CK(cudaMemcpy(h_bits, D + b->sc_dct.bits, 8 * 3, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(h_bits + 3, D + b->sc_pln.bits, 8 * 4, cudaMemcpyDeviceToHost));
+  int modes[kPieces];
+  for (int k = 0; k < kPieces; k++) modes[k] = h_emit[k] ? 0 : kModeSkip;
+  if (int rc = run_chains(c, b, modes)) return rc;
+  piece_bits(b, h_bits);
   for (int k = 0; k < kPieces; k++) h_piece_ptr[k] = (uint64_t)(uintptr_t)b->piece_ptr[k];
   unsigned s = 0;
   CK(cudaMemcpy(&s, b->desc.status, 4, cudaMemcpyDeviceToHost));

@@ -158,6 +158,8 @@ inline int plane_segw_for(long long rows, int max_w) {
 }
 
 // Sequential-coder chains for the entropy kernel (entropy.cu).
+constexpr int kModeSkip = 3;  // ChainTab::chain_mode: the chain is not run
+
 struct ChainTab {
   int nchains;
   const long long* tile_base;  // [nchains+1] global tile index of each chain's tile 0
@@ -175,9 +177,12 @@ struct ChainTab {
   // mode 2 after the A-maps, reporting the chain totals in out_cnt / out_map.
   const long long* in_cnt;     // [nchains][kMaxCtx] context counts before the chain
   const int* in_a;             // [nchains][kMaxCtx] A entering the chain
-  long long* out_cnt;          // [nchains][kMaxCtx] counts after the chain (mode 1)
+  long long* out_cnt;          // [nchains][kMaxCtx] counts after the chain (modes 0 and 1)
   AMap* out_map;               // [nchains][kMaxCtx] the chain's composed A-map (mode 2)
+  int* out_a;                  // [nchains][kMaxCtx] A after the chain (mode 0)
   int mode;                    // 0 full encode, 1 counts, 2 counts + A-maps
+  const int* chain_mode;       // [nchains] or null: per-chain mode overriding `mode` (kModeSkip: not run)
+  int modes_present;           // host: bit m set when some chain runs mode m (launch_entropy_fixup)
   int plane_segw;              // plane rows are cut into segments of <= plane_segw samples
   // per global tile status (epoch-tagged)
   int* flags;                  // [ntiles][4]: cnt, map, bit, done
@@ -235,6 +240,8 @@ void launch_fit(const ImgDesc*, int nimg, int max_sort_tiles, long long max_node
 void launch_fit_sort(const ImgDesc*, int nimg, int max_sort_tiles, cudaStream_t, bool any_hist = true);
 void launch_fit_bins(const ImgDesc*, int nimg, long long max_nodes, int max_chunks, cudaStream_t);
 void launch_fit_int(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
+void launch_fit_int_sums(const ImgDesc*, int nimg, long long max_n, cudaStream_t);
+void launch_fit_int_coef(const ImgDesc*, int nimg, cudaStream_t);
 void launch_fit_hist(const ImgDesc*, int nimg, int max_sort_tiles, cudaStream_t);
 struct RegroupTab {
   int nsrc;

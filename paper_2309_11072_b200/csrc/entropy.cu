@@ -155,20 +155,27 @@ __device__ __forceinline__ AMap warp_compose_down(AMap x) {
 }
 
 // ticket -> (chain, tile-in-chain, global tile) through the round-robin schedule
+__device__ __forceinline__ int chain_mode(const ChainTab& ct, int chain) {
+  return ct.chain_mode ? ct.chain_mode[chain] : ct.mode;
+}
+
+// the next ticket's tile, passing over the tiles of chains that are not run
 __device__ __forceinline__ bool next_tile(const ChainTab& ct, int* chain, long long* tin, long long* g) {
   const int lane = threadIdx.x & 31;
-  long long t = 0;
-  if (lane == 0) t = atomicAdd(ct.ticket, 1);
-  t = __shfl_sync(0xffffffffu, t, 0);
-  if (t >= ct.ntiles) return false;
-  int k = 0;
-  while (k + 1 < ct.nseg && ct.seg_t0[k + 1] <= t) k++;
-  const long long rel = t - ct.seg_t0[k];
-  const int act = ct.seg_active[k];
-  *tin = ct.seg_r0[k] + rel / act;
-  *chain = ct.rr_chain[rel % act];
-  *g = ct.tile_base[*chain] + *tin;
-  return true;
+  for (;;) {
+    long long t = 0;
+    if (lane == 0) t = atomicAdd(ct.ticket, 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= ct.ntiles) return false;
+    int k = 0;
+    while (k + 1 < ct.nseg && ct.seg_t0[k + 1] <= t) k++;
+    const long long rel = t - ct.seg_t0[k];
+    const int act = ct.seg_active[k];
+    *tin = ct.seg_r0[k] + rel / act;
+    *chain = ct.rr_chain[rel % act];
+    *g = ct.tile_base[*chain] + *tin;
+    if (chain_mode(ct, *chain) != kModeSkip) return true;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -313,6 +320,7 @@ template <int NL, int NC, class Gen>
 __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long g, int base, const Gen& gen,
                          const int* cnt_in, const LaneState& ls, unsigned* status, uint32_t* scr, int scr_cap) {
   const int lane = threadIdx.x & 31;
+  const int mode = chain_mode(ct, chain);
 #ifdef HDLL_EXP_NO_LB  // timing experiment only: no look-backs (wrong output)
   const bool chain_start = true;
 #else
@@ -359,10 +367,10 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
 #pragma unroll
     for (int c = 0; c < NC; c++) cv[kMaxCtx + c] = incnt[c] + ((c >= base && c < base + NL) ? tot[c - base] : 0);
     publish(ct, g, 0, 2);
-    if (ct.mode == 1 && chain_last)
+    if (mode != 2 && chain_last)
       for (int c = 0; c < NC; c++) ct.out_cnt[chain * kMaxCtx + c] = cv[kMaxCtx + c];
   }
-  if (ct.mode == 1) return;
+  if (mode == 1) return;
   int n0[NL];  // N before this lane's first symbol of each context
 #pragma unroll
   for (int c = 0; c < NL; c++) n0[c] = n_before(incnt[base + c] + lbase[c]);
@@ -429,7 +437,7 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
     AMap m{ls.mc[c * 32 + lane], ls.ms[c * 32 + lane], ls.mt[c * 32 + lane]};
     pre[c] = warp_excl_amap_small(m, &agg[c]);
   }
-  if (ct.mode == 2) {  // totals only: every tile's aggregate, composed per chain by k_chain_maps
+  if (mode == 2) {  // totals only: every tile's aggregate, composed per chain by k_chain_maps
     if (lane == 0) {
       AMap* mv = ct.maps + g * kMaxCtx;
 #pragma unroll
@@ -480,6 +488,8 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
     for (int c = 0; c < NC; c++)
       sv[c] = (c >= base && c < base + NL) ? (int)amap_apply(agg[c - base], ain[c]) : ain[c];
     publish(ct, g, 1, 2);
+    if (chain_last)
+      for (int c = 0; c < NC; c++) ct.out_a[chain * kMaxCtx + c] = sv[c];
   }
 
   // ---- 3. codes: every symbol's Rice code (and raw bits) into the lane's scratch words ----
@@ -1119,6 +1129,7 @@ __global__ void __launch_bounds__(256) k_entropy_fixup(ChainTab ct) {
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= ct.ntiles) return;
   const int chain = find_chain(ct, g);
+  if (chain_mode(ct, chain) != 0) return;
   const long long gend = ct.tile_base[chain + 1];
   const long long e = (long long)ct.bitv[g * 2 + 1];
   const long long s = e - (long long)ct.bitv[g * 2 + 0];
@@ -1143,6 +1154,7 @@ __global__ void __launch_bounds__(256) k_entropy_fixup(ChainTab ct) {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(32) k_chain_maps(ChainTab ct) {
   const int chain = blockIdx.x, c = blockIdx.y, lane = threadIdx.x;
+  if (chain_mode(ct, chain) != 2) return;
   const long long t0 = ct.tile_base[chain], nt = ct.tile_base[chain + 1] - t0;
   const long long per = (nt + 31) / 32;
   AMap m = amap_identity();
@@ -1225,12 +1237,8 @@ void launch_entropy_plane(const ImgDesc* d_descs, const ChainTab& ct, int max_w,
 
 void launch_entropy_fixup(const ChainTab& ct, cudaStream_t st) {
   if (ct.ntiles <= 0) return;
-  if (ct.mode == 2) {
-    k_chain_maps<<<dim3(ct.nchains, kMaxCtx), 32, 0, st>>>(ct);
-    return;
-  }
-  if (ct.mode == 1) return;
-  k_entropy_fixup<<<(unsigned)((ct.ntiles + 255) / 256), 256, 0, st>>>(ct);
+  if (ct.modes_present & 4) k_chain_maps<<<dim3(ct.nchains, kMaxCtx), 32, 0, st>>>(ct);
+  if (ct.modes_present & 1) k_entropy_fixup<<<(unsigned)((ct.ntiles + 255) / 256), 256, 0, st>>>(ct);
 }
 
 }  // namespace hdll

@@ -687,9 +687,10 @@ __global__ void __launch_bounds__(256) k_fit_int(const ImgDesc* __restrict__ des
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const bool global = d.global_regression != 0;
-  const long long n = d.n;
-  const uint32_t* px = reinterpret_cast<const uint32_t*>(d.rgbe);
-  const uint8_t* S = d.s_planes;
+  // the fit samples: desc pixels [fit_p0, fit_p0 + fit_m) (a row band's own rows)
+  const long long n = d.fit_m, plane = d.n;
+  const uint32_t* px = reinterpret_cast<const uint32_t*>(d.rgbe) + d.fit_p0;
+  const uint8_t* S = d.s_planes + d.fit_p0;
   // one pixel per lane per step; the grid stride keeps warps on whole 32-pixel rows of memory
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long b0 = (long long)blockIdx.x * blockDim.x; b0 < n; b0 += stride) {
@@ -703,7 +704,7 @@ __global__ void __launch_bounds__(256) k_fit_int(const ImgDesc* __restrict__ des
     const bool leader = (peers & lt) == 0;
 #pragma unroll
     for (int c = 0; c < 3; c++) {
-      const unsigned x = __ldg(S + (long long)c * n + p), y = (q >> (8 * c)) & 0xFFu;
+      const unsigned x = __ldg(S + (long long)c * plane + p), y = (q >> (8 * c)) & 0xFFu;
       // a warp's partial sums fit 32 bits (32 * 255^2 < 2^21)
       const unsigned rx = __reduce_add_sync(peers, x), ry = __reduce_add_sync(peers, y);
       const unsigned rxx = __reduce_add_sync(peers, x * x), rxy = __reduce_add_sync(peers, x * y);
@@ -734,7 +735,12 @@ __global__ void __launch_bounds__(256) k_fit_int_coef(const ImgDesc* __restrict_
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= kSegs) return;
   const int c = s >> 8, e = s & 255;
-  const long long nn = d.global_regression ? (e == 0 ? d.n : 0) : (long long)d.bin_count[e];
+  long long nn = 0;
+  if (!d.global_regression) {
+    nn = d.bin_count[e];
+  } else if (e == 0) {  // the whole plane: every bin's samples
+    for (int k = 0; k < 256; k++) nn += d.bin_count[k];
+  }
   if (nn == 0) return;
   const long long* g = d.isum + 3 * s;
   const double sx = (double)g[0], sxx = (double)g[1], sxy = (double)g[2];  // exact: < 2^53
@@ -761,6 +767,18 @@ __global__ void __launch_bounds__(256) k_fit_int_coef(const ImgDesc* __restrict_
     d.b32[s] = b32;
   }
   if (!isfinite(a32) || !isfinite(b32)) atomicOr(d.status, kErrNonFinite);
+}
+
+void launch_fit_int_sums(const ImgDesc* d_descs, int nimg, long long max_n, cudaStream_t st) {
+  long long gx = (max_n + 255) / 256;
+  const long long cap = (148 * 4 + nimg - 1) / nimg;
+  if (gx > cap) gx = cap;
+  if (gx < 1) gx = 1;
+  k_fit_int<<<dim3((unsigned)gx, nimg), 256, 0, st>>>(d_descs);
+}
+
+void launch_fit_int_coef(const ImgDesc* d_descs, int nimg, cudaStream_t st) {
+  k_fit_int_coef<<<dim3(kSegs / 256, nimg), 256, 0, st>>>(d_descs);
 }
 
 void launch_fit_int(const ImgDesc* d_descs, int nimg, long long max_n, cudaStream_t st) {

@@ -288,11 +288,11 @@ struct HostChains {
   }
   size_t staged_bytes() const {
     size_t nc = img.size() + 2;
-    return 16 * kAlign + 8 * (nc + 1) + 4 * nc * 3 + 8 * nc * 5 + (8 + 4 + 8 + sizeof(AMap)) * kMaxCtx * nc +
+    return 17 * kAlign + 8 * (nc + 1) + 4 * nc * 3 + 8 * nc * 5 + (8 + 4 + 8 + 4 + sizeof(AMap)) * kMaxCtx * nc +
            8 * 2 * seg_r0.size() + 4 * seg_active.size() + 4 * rr_chain.size();
   }
   struct Staged {
-    size_t tile_base, img, kind, comp, first, units, out, cap, bits, in_cnt, in_a, out_cnt, out_map, seg_r0, seg_t0,
+    size_t tile_base, img, kind, comp, first, units, out, cap, bits, in_cnt, in_a, out_cnt, out_map, out_a, seg_r0, seg_t0,
         seg_active, rr_chain;
   };
   template <class F>
@@ -312,6 +312,7 @@ struct HostChains {
     s.in_a = st(in_a.data(), 4 * in_a.size());
     s.out_cnt = st(nullptr, 8 * kMaxCtx * nc);
     s.out_map = st(nullptr, sizeof(AMap) * kMaxCtx * nc);
+    s.out_a = st(nullptr, 4 * kMaxCtx * nc);
     s.seg_r0 = st(seg_r0.data(), 8 * seg_r0.size());
     s.seg_t0 = st(seg_t0.data(), 8 * seg_t0.size());
     s.seg_active = st(seg_active.data(), 4 * seg_active.size());
@@ -336,7 +337,10 @@ struct HostChains {
     ct.in_a = (const int*)(D + s.in_a);
     ct.out_cnt = (long long*)(D + s.out_cnt);
     ct.out_map = (AMap*)(D + s.out_map);
+    ct.out_a = (int*)(D + s.out_a);
     ct.mode = mode;
+    ct.chain_mode = nullptr;
+    ct.modes_present = 1 << mode;
     ct.plane_segw = segw;
     size_t o = 0;
     ct.flags = (int*)(E + o) + t0 * 4;

@@ -241,6 +241,16 @@ class _ThreadView:
     def allgather(self, arr: np.ndarray):
         return [np.array(a, copy=True) for a in self._swap(np.asarray(arr))]
 
+    def allgather_var(self, arr: np.ndarray, counts):
+        return self.allgather(arr)
+
+    def allreduce_sum(self, arr: np.ndarray):
+        parts = self._swap(np.asarray(arr))
+        out = np.zeros_like(parts[0])
+        for p in parts:
+            out += p
+        return out
+
     def alltoall(self, send, send_bytes, recv_bytes):
         import torch
 
@@ -264,19 +274,57 @@ class _ThreadView:
 
 
 class TorchExchange:
-    """torch.distributed exchange (NCCL on GPUs, gloo on CPU)."""
+    """torch.distributed exchange (NCCL on GPUs, gloo on CPU).
 
-    def __init__(self, group=None):
+    The small per-phase summaries travel as flat tensors (one
+    all_gather_into_tensor / all_reduce each; on NCCL staged through the
+    device), not pickled objects."""
+
+    def __init__(self, group=None, device=None):
+        import torch
         import torch.distributed as dist
 
         self.dist, self.group = dist, group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        nccl = dist.get_backend(group) == "nccl"
+        self.dev = (torch.device("cuda", torch.cuda.current_device()) if device is None else device) if nccl else None
+
+    def _t(self, arr: np.ndarray):
+        import torch
+
+        t = torch.from_numpy(np.ascontiguousarray(arr).reshape(-1).view(np.uint8).copy())
+        return t.to(self.dev) if self.dev is not None else t
 
     def allgather(self, arr: np.ndarray):
-        out = [None] * self.world
-        self.dist.all_gather_object(out, np.asarray(arr), group=self.group)
-        return out
+        """arr has the same dtype and shape on every rank"""
+        import torch
+
+        arr = np.ascontiguousarray(arr)
+        t = self._t(arr)
+        out = torch.empty(self.world * t.numel(), dtype=torch.uint8, device=t.device)
+        self.dist.all_gather_into_tensor(out, t, group=self.group)
+        raw = out.cpu().numpy()
+        n = t.numel()
+        return [raw[r * n:(r + 1) * n].view(arr.dtype).reshape(arr.shape).copy() for r in range(self.world)]
+
+    def allgather_var(self, arr: np.ndarray, counts):
+        """1-D arr of counts[rank] elements (every rank knows all counts): padded to the largest"""
+        arr = np.asarray(arr)
+        m = max(1, max(int(c) for c in counts))
+        pad = np.zeros(m, arr.dtype)
+        pad[: arr.size] = arr
+        return [g[: int(c)] for g, c in zip(self.allgather(pad), counts)]
+
+    def allreduce_sum(self, arr: np.ndarray):
+        import torch
+
+        arr = np.ascontiguousarray(arr)
+        t = torch.from_numpy(arr.copy())
+        if self.dev is not None:
+            t = t.to(self.dev)
+        self.dist.all_reduce(t, group=self.group)
+        return t.cpu().numpy().reshape(arr.shape)
 
     def alltoall(self, send, send_bytes, recv_bytes):
         import torch
@@ -321,24 +369,54 @@ def _ptr(a, ct):
     return a.ctypes.data_as(ctypes.POINTER(ct))
 
 
-def _prefix_states(cnts, maps_or_none, world):
-    """Per (rank, piece): context counts entering the piece and, given maps, the
-    entering A.  Stream order: DCT pieces (component, rank), then each plane by rank."""
-    order = [[(r, c) for c in range(3) for r in range(world)]] + [[(r, 3 + k) for r in range(world)] for k in range(4)]
+def piece_chains(world: int):
+    """The coder chains over the ranks' pieces, in stream order.  Pieces 0-2 are
+    a band's Y, Cb, Cr slices of the base-layer DCT stream, 3-6 its E, R, G, B
+    plane rows.  Y (contexts 0-2) and Cb, Cr (contexts 3-5) share no state
+    (codec_core.py:439-450), so the DCT stream is two chains: Y of every rank,
+    and Cb of every rank followed by Cr of every rank."""
+    R = range(world)
+    return ([[(r, 0) for r in R], [(r, 1) for r in R] + [(r, 2) for r in R]]
+            + [[(r, 3 + k) for r in R] for k in range(4)])
+
+
+def piece_roles(world: int):
+    """Per (rank, piece): `first` -- it starts its chain, nothing enters it, so
+    it is coded in phase 5 from the reset state; `need_map` -- a later piece
+    composes its A-map (neither the chain's first nor its last); `emit` -- coded
+    in phase 7 once its entering state is known."""
+    first = np.zeros((world, PIECES), bool)
+    need = np.zeros((world, PIECES), bool)
+    for ch in piece_chains(world):
+        for i, (r, p) in enumerate(ch):
+            first[r, p] = i == 0
+            need[r, p] = 0 < i < len(ch) - 1
+    return first, need, ~first
+
+
+def prefix_counts(cnts, world: int) -> np.ndarray:
+    """Context counts entering every piece: the counts of the earlier pieces of its chain."""
     in_cnt = np.zeros((world, PIECES, NCTX), np.int64)
-    in_a = np.full((world, PIECES, NCTX), 4, np.int32)  # AdaptiveRiceState A = 4 (_kernels.py:114-128)
-    for chain in order:
+    for ch in piece_chains(world):
         run = np.zeros(NCTX, np.int64)
-        comp = [IDENTITY] * NCTX
-        for r, p in chain:
+        for r, p in ch:
             in_cnt[r, p] = run
-            run = run + cnts[r][p]
-            if maps_or_none is not None:
-                for c in range(NCTX):
-                    in_a[r, p, c] = amap_apply(comp[c], 4)
-                    m = tuple(int(x) for x in maps_or_none[r][p, c])
-                    comp[c] = amap_then(comp[c], m)
-    return in_cnt, in_a
+            run = run + np.asarray(cnts[r][p], np.int64)
+    return in_cnt
+
+
+def entering_a(out_a, maps, world: int) -> np.ndarray:
+    """A entering every piece: the chain's first piece's outgoing A (phase 5),
+    then the A-maps of the pieces between (phase 6) applied in order."""
+    in_a = np.full((world, PIECES, NCTX), 4, np.int32)  # AdaptiveRiceState A = 4 (_kernels.py:114-128)
+    for ch in piece_chains(world):
+        r0, p0 = ch[0]
+        state = [int(v) for v in out_a[r0][p0]]
+        for i, (r, p) in enumerate(ch[1:], start=1):
+            in_a[r, p] = state
+            if i < len(ch) - 1:
+                state = [amap_apply(tuple(int(x) for x in maps[r][p, c]), state[c]) for c in range(NCTX)]
+    return in_a
 
 
 def encode_band(ex, prep, rows_ptr: int, spec: BandSpec, ctx, stream_handle: int, device, out=None):
@@ -352,105 +430,139 @@ def encode_band(ex, prep, rows_ptr: int, spec: BandSpec, ctx, stream_handle: int
     h = ctx.handle
     W, H = prep.w, prep.h
     world, rank = ex.world, ex.rank
+    specs = ex.specs
     im = container._image_struct(prep, rows_ptr)
     bd = _native.Band(spec.row0, spec.row1, spec.crow0, spec.crow1, spec.node0, spec.node1)
-    # 1. tone-map node sums
-    nodes = np.zeros(max(1, spec.node1 - spec.node0), np.float64)
+    # 1. tone-map node sums and max Lw
+    nodes = np.zeros(1 + max(1, spec.node1 - spec.node0), np.float64)
     mx = ctypes.c_double(0.0)
-    _native.check(L.hdll_b200_band_begin(h, ctypes.byref(im), ctypes.byref(bd), stream_handle, _ptr(nodes, ctypes.c_double),
-                                         ctypes.byref(mx)), "band_begin")
-    got = ex.allgather(np.concatenate([[mx.value], nodes[: spec.node1 - spec.node0]]))
+    _native.check(L.hdll_b200_band_begin(h, ctypes.byref(im), ctypes.byref(bd), stream_handle,
+                                         _ptr(nodes[1:], ctypes.c_double), ctypes.byref(mx)), "band_begin")
+    nodes[0] = mx.value
+    got = ex.allgather_var(nodes[: 1 + spec.node1 - spec.node0], [1 + s.node1 - s.node0 for s in specs])
     nodes_all = np.ascontiguousarray(np.concatenate([g[1:] for g in got]))
     maxlw = float(max(g[0] for g in got))
     # 2. layers -> histogram
     hist = np.zeros(256, np.uint32)
     _native.check(L.hdll_b200_band_layers(h, _ptr(nodes_all, ctypes.c_double), nodes_all.size, maxlw,
                                           _ptr(hist, ctypes.c_uint32)), "band_layers")
-    hists = np.stack(ex.allgather(hist)).astype(np.uint32)
-    hist_total = hists.astype(np.int64).sum(0)
-    # 3. fit samples to their owners
-    glob = bool(prep.params.global_regression)
-    bounds = [0] + [256] * world if glob else owner_bounds(hist_total, world)
-
-    def chunk(hs, o):
-        if not prep.slrme:
-            return 0
-        if glob:
-            return int(hs.astype(np.int64).sum()) if o == 0 else 0
-        return int(hs[bounds[o]: bounds[o + 1]].astype(np.int64).sum())
-
-    send_b = [fit_chunk_bytes(chunk(hist, o)) for o in range(world)]
-    send = torch.empty(max(16, sum(send_b)), dtype=torch.uint8, device=device)
-    send_bytes = np.zeros(world, np.uint64)
-    lo_arr = np.asarray(bounds, np.uint32)
-    _native.check(L.hdll_b200_band_fit_send(h, _ptr(lo_arr, ctypes.c_uint32), world, send.data_ptr(), send.numel(),
-                                            _ptr(send_bytes, ctypes.c_uint64)), "band_fit_send")
-    assert [int(x) for x in send_bytes] == send_b
-    recv_b = [fit_chunk_bytes(chunk(hists[s], rank)) for s in range(world)]
-    recv = ex.alltoall(send, send_b, recv_b)
-    # 4. owner fit -> table
-    a32 = np.zeros(768, np.float32)
-    b32 = np.zeros(768, np.float32)
-    st = ctypes.c_uint32(0)
-    rb = np.asarray(recv_b, np.uint64)
-    hflat = np.ascontiguousarray(hists.reshape(-1))
-    recv_ptr = recv.data_ptr() if recv.numel() else send.data_ptr()
-    _native.check(L.hdll_b200_band_fit_owner(h, recv_ptr, _ptr(rb, ctypes.c_uint64), _ptr(hflat, ctypes.c_uint32),
-                                             world, bounds[rank], bounds[rank + 1], _ptr(a32, ctypes.c_float),
-                                             _ptr(b32, ctypes.c_float), ctypes.byref(st)), "band_fit_owner")
-    tabs = ex.allgather(np.concatenate([a32.view(np.uint32), b32.view(np.uint32), [st.value]]).astype(np.uint32))
     A32 = np.zeros(768, np.float32)
     B32 = np.zeros(768, np.float32)
     status = 0
-    for o, t in enumerate(tabs):
-        status |= int(t[-1])
-        for c in range(3):
-            sl = slice(c * 256 + bounds[o], c * 256 + bounds[o + 1])
-            A32[sl] = t[:768].view(np.float32)[sl]
-            B32[sl] = t[768:1536].view(np.float32)[sl]
+    if prep.slrme and prep.sigma_milli == 0:
+        # 3-4, sigma = 0: every sum is an exact integer -- all-reduce the bin table
+        # (counts, sums of x, x^2, x*y, y: 3328 int64) and fit on every rank
+        sums = np.zeros(4 * 768, np.int64)
+        _native.check(L.hdll_b200_band_fit_sums(h, _ptr(sums, ctypes.c_int64)), "band_fit_sums")
+        tot = ex.allreduce_sum(np.concatenate([hist.astype(np.int64), sums]))
+        hist_total = tot[:256]
+        sums_t = np.ascontiguousarray(tot[256:])
+        hist_u = np.ascontiguousarray(hist_total.astype(np.uint32))
+        st = ctypes.c_uint32(0)
+        _native.check(L.hdll_b200_band_fit_coef(h, _ptr(sums_t, ctypes.c_int64), _ptr(hist_u, ctypes.c_uint32),
+                                                _ptr(A32, ctypes.c_float), _ptr(B32, ctypes.c_float),
+                                                ctypes.byref(st)), "band_fit_coef")
+        status = st.value
+    else:
+        hists = np.stack(ex.allgather(hist)).astype(np.uint32)
+        hist_total = hists.astype(np.int64).sum(0)
+        # 3. fit samples to their owners
+        glob = bool(prep.params.global_regression)
+        bounds = [0] + [256] * world if glob else owner_bounds(hist_total, world)
+
+        def chunk(hs, o):
+            if not prep.slrme:
+                return 0
+            if glob:
+                return int(hs.astype(np.int64).sum()) if o == 0 else 0
+            return int(hs[bounds[o]: bounds[o + 1]].astype(np.int64).sum())
+
+        send_b = [fit_chunk_bytes(chunk(hist, o)) for o in range(world)]
+        send = torch.empty(max(16, sum(send_b)), dtype=torch.uint8, device=device)
+        send_bytes = np.zeros(world, np.uint64)
+        lo_arr = np.asarray(bounds, np.uint32)
+        _native.check(L.hdll_b200_band_fit_send(h, _ptr(lo_arr, ctypes.c_uint32), world, send.data_ptr(),
+                                                send.numel(), _ptr(send_bytes, ctypes.c_uint64)), "band_fit_send")
+        assert [int(x) for x in send_bytes] == send_b
+        recv_b = [fit_chunk_bytes(chunk(hists[s], rank)) for s in range(world)]
+        recv = ex.alltoall(send, send_b, recv_b)
+        # 4. owner fit -> table
+        a32 = np.zeros(768, np.float32)
+        b32 = np.zeros(768, np.float32)
+        st = ctypes.c_uint32(0)
+        rb = np.asarray(recv_b, np.uint64)
+        hflat = np.ascontiguousarray(hists.reshape(-1))
+        recv_ptr = recv.data_ptr() if recv.numel() else send.data_ptr()
+        _native.check(L.hdll_b200_band_fit_owner(h, recv_ptr, _ptr(rb, ctypes.c_uint64), _ptr(hflat, ctypes.c_uint32),
+                                                 world, bounds[rank], bounds[rank + 1], _ptr(a32, ctypes.c_float),
+                                                 _ptr(b32, ctypes.c_float), ctypes.byref(st)), "band_fit_owner")
+        tabs = ex.allgather(np.concatenate([a32.view(np.uint32), b32.view(np.uint32), [st.value]]).astype(np.uint32))
+        for o, t in enumerate(tabs):
+            status |= int(t[-1])
+            for c in range(3):
+                sl = slice(c * 256 + bounds[o], c * 256 + bounds[o + 1])
+                A32[sl] = t[:768].view(np.float32)[sl]
+                B32[sl] = t[768:1536].view(np.float32)[sl]
     if status & 1:  # kErrNonFinite: RegressionTable's ValueError (estimator.py:66-67)
         raise ValueError("regression parameters must be finite")
-    # 5. estimate, CRCs, piece counts
+    # 5. estimate, CRCs, piece counts; the pieces that start their chains are coded now
+    first, need, emit = piece_roles(world)
     crc = np.zeros(5, np.uint32)
     cnt = np.zeros((PIECES, NCTX), np.int64)
-    _native.check(L.hdll_b200_band_code(h, _ptr(A32, ctypes.c_float), _ptr(B32, ctypes.c_float),
-                                        _ptr(crc, ctypes.c_uint32), _ptr(cnt, ctypes.c_int64)), "band_code")
-    cnts = ex.allgather(cnt)
-    in_cnt, _ = _prefix_states(cnts, None, world)
-    # 6. A-maps given the counts entering each piece
-    maps = np.zeros((PIECES, NCTX, 3), np.int64)
-    mine = np.ascontiguousarray(in_cnt[rank])
-    _native.check(L.hdll_b200_band_maps(h, _ptr(mine, ctypes.c_int64), _ptr(maps, ctypes.c_int64)), "band_maps")
-    maps_all = ex.allgather(maps)
-    _, in_a = _prefix_states(cnts, maps_all, world)
-    # 7. emit, gather on rank 0
+    out_a = np.zeros((PIECES, NCTX), np.int32)
     bits = np.zeros(PIECES, np.uint64)
     ptrs = np.zeros(PIECES, np.uint64)
-    ina = np.ascontiguousarray(in_a[rank])
-    _native.check(L.hdll_b200_band_emit(h, _ptr(ina, ctypes.c_int32), _ptr(bits, ctypes.c_uint64),
-                                        _ptr(ptrs, ctypes.c_uint64)), "band_emit")
-    meta = ex.allgather(np.concatenate([bits.astype(np.int64), crc.astype(np.int64)]))
+    fr = np.ascontiguousarray(first[rank].astype(np.int32))
+    _native.check(L.hdll_b200_band_code(h, _ptr(A32, ctypes.c_float), _ptr(B32, ctypes.c_float),
+                                        _ptr(fr, ctypes.c_int32), _ptr(crc, ctypes.c_uint32),
+                                        _ptr(cnt, ctypes.c_int64), _ptr(out_a, ctypes.c_int32),
+                                        _ptr(bits, ctypes.c_uint64), _ptr(ptrs, ctypes.c_uint64)), "band_code")
+    meta = ex.allgather(np.concatenate([cnt.reshape(-1), out_a.reshape(-1).astype(np.int64), crc.astype(np.int64)]))
+    nc = PIECES * NCTX
+    cnts = [m[:nc].reshape(PIECES, NCTX) for m in meta]
+    outs_a = [m[nc:2 * nc].reshape(PIECES, NCTX) for m in meta]
+    crc_all = [m[2 * nc:] for m in meta]
+    in_cnt = prefix_counts(cnts, world)
+    # 6. A-maps of the pieces between a chain's first and last (none for one rank)
+    maps_all = None
+    if need.any():
+        maps = np.zeros((PIECES, NCTX, 3), np.int64)
+        mine = np.ascontiguousarray(in_cnt[rank])
+        nd = np.ascontiguousarray(need[rank].astype(np.int32))
+        if nd.any():
+            _native.check(L.hdll_b200_band_maps(h, _ptr(mine, ctypes.c_int64), _ptr(nd, ctypes.c_int32),
+                                                _ptr(maps, ctypes.c_int64)), "band_maps")
+        maps_all = ex.allgather(maps)
+    # 7. code the remaining pieces from their entering state, gather on rank 0
+    if emit[rank].any():
+        in_a = entering_a(outs_a, maps_all, world)
+        ina = np.ascontiguousarray(in_a[rank])
+        inc = np.ascontiguousarray(in_cnt[rank])
+        em = np.ascontiguousarray(emit[rank].astype(np.int32))
+        bits7 = np.zeros(PIECES, np.uint64)
+        _native.check(L.hdll_b200_band_emit(h, _ptr(inc, ctypes.c_int64), _ptr(ina, ctypes.c_int32),
+                                            _ptr(em, ctypes.c_int32), _ptr(bits7, ctypes.c_uint64),
+                                            _ptr(ptrs, ctypes.c_uint64)), "band_emit")
+        bits = np.where(emit[rank], bits7, bits)
+    bits_all = ex.allgather(bits.astype(np.int64)) if world > 1 else [bits.astype(np.int64)]
     nbytes = [int((int(b) + 31) // 32 * 4) for b in bits]
     all_ptrs, keep = ex.gather_pieces([int(p) for p in ptrs], nbytes, device)
     if rank != 0:
         ex.barrier()  # rank 0 reads the pieces in place (ThreadExchange) until it has assembled
         return None
-    bits_all = [m[:PIECES] for m in meta]
-    crc_all = [m[PIECES:] for m in meta]
     order = [[(r, c) for c in range(3) for r in range(world)]] + [[(r, 3 + k) for r in range(world)] for k in range(4)]
     npieces = np.asarray([len(ch) for ch in order], np.int32)
     pp = np.asarray([all_ptrs[r][p] for ch in order for r, p in ch], np.uint64)
     pb = np.asarray([bits_all[r][p] for ch in order for r, p in ch], np.uint64)
     # CRCs of the whole image, band by band (codec_core.py:252-253)
     crc_full = np.zeros(5, np.uint32)
-    specs = ex.specs
     for j in range(5):
         acc = None
         for r in range(world):
             ln = (specs[r].row1 - specs[r].row0) * W * (3 if j == 0 else 1)
             acc = int(crc_all[r][j]) if acc is None else crc32_combine(acc, int(crc_all[r][j]), ln)
         crc_full[j] = acc
-    hist_u32 = np.ascontiguousarray(hist_total.astype(np.uint32))
+    hist_u32 = np.ascontiguousarray(np.asarray(hist_total).astype(np.uint32))
     cap = container.stream_capacity(prep)
     if out is not None:
         d_out, d_len = out

@@ -136,30 +136,57 @@ def test_amap_then_is_associative_on_domain():
             assert tiled.amap_apply(left, a) == want == tiled.amap_apply(right, a)
 
 
-def test_prefix_states_order():
-    """Pieces chain DCT (component, rank), then each plane by rank."""
+@pytest.mark.parametrize("world", [1, 2, 3, 5])
+def test_piece_roles(world):
+    """Chains in stream order: Y by rank; Cb by rank then Cr by rank (they share
+    contexts 3-5); each plane by rank.  First pieces are coded in phase 5, the
+    rest in phase 7; A-maps only for pieces strictly inside a chain."""
+    chains = tiled.piece_chains(world)
+    assert chains[0] == [(r, 0) for r in range(world)]
+    assert chains[1] == [(r, 1) for r in range(world)] + [(r, 2) for r in range(world)]
+    assert sorted(x for ch in chains for x in ch) == [(r, p) for r in range(world) for p in range(tiled.PIECES)]
+    first, need, emit = tiled.piece_roles(world)
+    assert first[0].tolist() == [True, True, False, True, True, True, True]
+    assert not first[1:].any()
+    assert (emit == ~first).all()
+    if world == 1:
+        assert not need.any()  # one rank: phase 5 codes all but Cr, phase 7 codes Cr alone
+        assert emit[0].tolist() == [False, False, True, False, False, False, False]
+    else:
+        assert need[0, 2] and need[world - 1, 1] and not need[world - 1, 2] and not need[0, 0]
+
+
+def test_prefix_counts_and_entering_a_equal_sequential_state():
+    """entering_a(out_a of the first pieces, maps) == the A a sequential coder
+    has when it reaches each piece (maps composed in chain order)."""
     world = 3
     rng = np.random.default_rng(5)
     cnts = [rng.integers(0, 100, (tiled.PIECES, tiled.NCTX)) for _ in range(world)]
+    in_cnt = tiled.prefix_counts(cnts, world)
+    for ch in tiled.piece_chains(world):
+        run = np.zeros(tiled.NCTX, np.int64)
+        for r, p in ch:
+            assert np.array_equal(in_cnt[r, p], run)
+            run += cnts[r][p]
+    # every piece's map: a random exact map (A + c) >> s of small shift
     maps = [np.zeros((tiled.PIECES, tiled.NCTX, 3), np.int64) for _ in range(world)]
     for r in range(world):
         for p in range(tiled.PIECES):
             for c in range(tiled.NCTX):
-                maps[r][p, c] = (int(rng.integers(0, 50)), 0, 0)
-    in_cnt, in_a = tiled._prefix_states(cnts, maps, world)
-    order = [(r, c) for c in range(3) for r in range(world)]
-    run = np.zeros(tiled.NCTX, np.int64)
-    acc = np.zeros(tiled.NCTX, np.int64)
-    for r, p in order:
-        assert np.array_equal(in_cnt[r, p], run)
-        assert np.array_equal(in_a[r, p], 4 + acc)
-        run += cnts[r][p]
-        acc += maps[r][p, :, 0]
-    for k in range(4):
-        run = np.zeros(tiled.NCTX, np.int64)
-        for r in range(world):
-            assert np.array_equal(in_cnt[r, 3 + k], run)
-            run += cnts[r][3 + k]
+                maps[r][p, c] = (int(rng.integers(0, 300)), int(rng.integers(0, 3)), 0)
+    # the sequential state: start at A = 4, apply each piece's map in chain order
+    want = np.zeros((world, tiled.PIECES, tiled.NCTX), np.int64)
+    out_a = [np.zeros((tiled.PIECES, tiled.NCTX), np.int64) for _ in range(world)]
+    for ch in tiled.piece_chains(world):
+        state = [4] * tiled.NCTX
+        for i, (r, p) in enumerate(ch):
+            want[r, p] = state
+            state = [tiled.amap_apply(tuple(maps[r][p, c]), state[c]) for c in range(tiled.NCTX)]
+            if i == 0:
+                out_a[r][p] = state  # phase 5 reports the first piece's outgoing A
+    got = tiled.entering_a(out_a, maps, world)
+    first, _, _ = tiled.piece_roles(world)
+    assert np.array_equal(got[~first], want[~first])
 
 
 def _free_port():
@@ -175,10 +202,14 @@ def _exchange_worker(rank, world, port, q):
     try:
         ex = tiled.TorchExchange()
         got = ex.allgather(np.arange(3) + 10 * rank)
+        var = ex.allgather_var(np.arange(rank + 2, dtype=np.float64), [2, 3])
+        red = ex.allreduce_sum(np.array([1, 2, 3], np.int64) * (rank + 1))
         # all-to-all with uneven chunks, as phase 3 sends fit samples to owners
         sizes = [[3, 5], [0, 7]]  # sizes[src][dst]
         send = torch.cat([torch.full((sizes[rank][d],), 16 * rank + d, dtype=torch.uint8) for d in range(world)])
         recv = ex.alltoall(send, sizes[rank], [sizes[s][rank] for s in range(world)])
+        assert [v.tolist() for v in var] == [[0.0, 1.0], [0.0, 1.0, 2.0]]
+        assert red.tolist() == [3, 6, 9]
         q.put((rank, [g.tolist() for g in got], recv.tolist()))
         ex.barrier()
     finally:
