@@ -413,6 +413,7 @@ def run_b200(args):
             dist.destroy_process_group()
         return
 
+    dec = None if args.no_decode else decode_timing(args, P, preps, npx_l)
     value = total_px / (ms / 1000.0) / 1e6
     e2e_value = total_px / (e2e_ms / 1000.0) / 1e6
     peak, peak_src = peaks()
@@ -479,12 +480,55 @@ def run_b200(args):
         "cpu_baseline": cpu,
         "parity_vs_reference": par_ref,
         "parity_vs_oracle": par_oracle,
+        "decode": dec,
     }
     if args.digests:
         line["stream_sha256"] = [all_digests[i][0] for i in sorted(all_digests)]
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def decode_timing(args, P, preps, npx_l):
+    """GPU decode_hdr / decode_sdr through the public
+    API (host stream in, host pixels out), one image and a batch of the kept
+    streams, checked lossless; beside it the oracle's decoder on one image on
+    a host core.  The adaptive-Rice streams decode one GPU thread per stream
+    (DESIGN.md section 6), so batches are where the GPU decoder is fast."""
+    kept = [i for i in range(len(preps)) if getattr(preps[i], "blob", None) is not None][:64]
+    if not kept:
+        return None
+    streams = [P.deserialize(preps[i].blob) for i in kept]
+    px = sum(npx_l[i] for i in kept)
+
+    def timed(fn, reps=2):
+        fn()
+        best = 1e30
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            r = fn()
+            best = min(best, time.perf_counter() - t0)
+        return best, r
+
+    t1, img = timed(lambda: P.decode_hdr(streams[0]))
+    tb, imgs = timed(lambda: P.decode_hdr_batch(streams), reps=1)
+    ts1, _ = timed(lambda: P.decode_sdr(streams[0]))
+    ok = np.array_equal(img.pixels, preps[kept[0]].pixels) and all(
+        np.array_equal(o.pixels, preps[i].pixels) for o, i in zip(imgs, kept))
+    out = {"unit": UNIT, "lossless_roundtrip": ok,
+           "decode_hdr_one_image": {"ms": round(t1 * 1e3, 2), "value": round(npx_l[kept[0]] / t1 / 1e6, 3)},
+           "decode_hdr_batch": {"images": len(kept), "ms": round(tb * 1e3, 2), "value": round(px / tb / 1e6, 3)},
+           "decode_sdr_one_image": {"ms": round(ts1 * 1e3, 2), "value": round(npx_l[kept[0]] / ts1 / 1e6, 3)},
+           "path": "paper_2309_11072_b200.decode_hdr / decode_hdr_batch / decode_sdr (host stream -> host pixels)"}
+    if not args.no_cpu:
+        from oracle import hdll_oracle as O
+        t0 = time.perf_counter()
+        O.decode_hdr(preps[kept[0]].blob)
+        tc = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": round(npx_l[kept[0]] / tc / 1e6, 3), "unit": UNIT, "cores": 1, "kind": "port",
+                               "sample": "one image, oracle decode_hdr (oracle/ port of container.py:238-280)",
+                               "ms": round(tc * 1e3, 1)}
+    return out
 
 
 def run_dry(args, indices, pix):
@@ -686,6 +730,7 @@ def main():
     ap.add_argument("--chunk", type=int, default=64, help="images per HostPipeline chunk (e2e leg)")
     ap.add_argument("--chunk-mpx", type=float, default=160.0, help="Mpx per batched device encode")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-decode", action="store_true", help="skip the decode_hdr / decode_sdr timing")
     ap.add_argument("--tiled", action="store_true", help="config 3: tile-sharded path even on one rank")
     ap.add_argument("--digests", action="store_true", help="add every stream's SHA-256 to the JSON line")
     ap.add_argument("--dry-run", action="store_true", help=argparse.SUPPRESS)

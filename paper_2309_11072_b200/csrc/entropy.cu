@@ -156,7 +156,11 @@ __device__ __forceinline__ AMap warp_compose_down(AMap x) {
 
 // ticket -> (chain, tile-in-chain, global tile) through the round-robin schedule
 __device__ __forceinline__ int chain_mode(const ChainTab& ct, int chain) {
+#ifdef HDLL_EXP_NOCMODE  // A/B experiment only: per-chain modes off (band pieces wrong)
+  return ct.mode;
+#else
   return ct.chain_mode ? ct.chain_mode[chain] : ct.mode;
+#endif
 }
 
 // the next ticket's tile, passing over the tiles of chains that are not run
