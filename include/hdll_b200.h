@@ -209,6 +209,9 @@ int hdll_b200_band_layers(hdll_b200_ctx *ctx, const double *h_nodes_all, uint64_
 int hdll_b200_band_fit_sums(hdll_b200_ctx *ctx, int64_t *h_sums);
 int hdll_b200_band_fit_coef(hdll_b200_ctx *ctx, const int64_t *h_sums, const uint32_t *h_hist, float *h_a32,
                             float *h_b32, uint32_t *h_status);
+/* Phases 3-4 on a single rank (the band is the whole image): fit from the
+ * band's own sorted samples, no exchange.  Out: a32/b32 [3][256], error bits. */
+int hdll_b200_band_fit_local(hdll_b200_ctx *ctx, float *h_a32, float *h_b32, uint32_t *h_status);
 /* Phase 3: pack the sorted samples for their owners (owner o fits exponents
  * [owner_lo[o], owner_lo[o+1])) into d_send; h_send_bytes[o] = chunk sizes.
  * Exchange: all-to-all of the chunks. */

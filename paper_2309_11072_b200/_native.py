@@ -23,6 +23,7 @@ EXPORTS = (
     "hdll_b200_lossless_encode_plane", "hdll_b200_lossy_encode", "hdll_b200_last_launch_count",
     "hdll_b200_stage_times", "hdll_b200_status_string",
     "hdll_b200_band_begin", "hdll_b200_band_layers", "hdll_b200_band_fit_sums", "hdll_b200_band_fit_coef",
+    "hdll_b200_band_fit_local",
     "hdll_b200_band_fit_send", "hdll_b200_band_fit_owner",
     "hdll_b200_band_code", "hdll_b200_band_maps", "hdll_b200_band_emit", "hdll_b200_assemble_pieces",
     "hdll_b200_decode_batch", "hdll_b200_hdr_decode", "hdll_b200_hdr_encode",
@@ -118,6 +119,7 @@ def lib():
                 "hdll_b200_band_fit_owner": [vp, vp, u64p, u32p, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32,
                                              f32p, f32p, u32p],
                 "hdll_b200_band_fit_sums": [vp, i64p],
+                "hdll_b200_band_fit_local": [vp, f32p, f32p, u32p],
                 "hdll_b200_band_fit_coef": [vp, i64p, u32p, f32p, f32p, u32p],
                 "hdll_b200_band_code": [vp, f32p, f32p, i32p, u32p, i64p, i32p, u64p, u64p],
                 "hdll_b200_band_maps": [vp, i64p, i32p, i64p],

@@ -356,6 +356,26 @@ int hdll_b200_band_fit_coef(hdll_b200_ctx* ctx, const int64_t* h_sums, const uin
   return sync_status(b);
 }
 
+int hdll_b200_band_fit_local(hdll_b200_ctx* ctx, float* h_a32, float* h_b32, uint32_t* h_status) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  CtxLock lock(c);
+  Band* b = band_of(ctx);
+  if (!b || !h_a32 || !h_b32 || !h_status || b->desc.int_fit) return HDLL_B200_E_ARG;
+  if (b->y0 != 0 || b->y1 != b->H) return HDLL_B200_E_ARG;  // the band must be the whole image
+  CK(cudaSetDevice(c->device));
+  const ImgDesc& d = b->desc;
+  CK(cudaMemsetAsync(d.a32, 0, 4 * 768, b->st));
+  CK(cudaMemsetAsync(d.b32, 0, 4 * 768, b->st));
+  if (d.slrme) {  // the band's samples, sorted by phase 2, are every sample of the image
+    launch_fit_bins(b->d_desc, 1, max_seg_nodes(d.fit_m), std::min(d.blas_threads, kMaxBlasThreads), b->st);
+    c->launches += 4;
+  }
+  CK(cudaMemcpyAsync(h_a32, d.a32, 4 * 768, cudaMemcpyDeviceToHost, b->st));
+  CK(cudaMemcpyAsync(h_b32, d.b32, 4 * 768, cudaMemcpyDeviceToHost, b->st));
+  CK(cudaMemcpyAsync(h_status, d.status, 4, cudaMemcpyDeviceToHost, b->st));
+  return sync_status(b);
+}
+
 int hdll_b200_band_fit_send(hdll_b200_ctx* ctx, const uint32_t* owner_lo, int nowners, uint8_t* d_send,
                             uint64_t send_cap, uint64_t* h_send_bytes) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);

@@ -155,15 +155,17 @@ __device__ __forceinline__ AMap warp_compose_down(AMap x) {
 }
 
 // ticket -> (chain, tile-in-chain, global tile) through the round-robin schedule
+// kCM: the launch carries per-chain modes (row-band pieces, band.cu).  The
+// whole-image encode compiles without them: a per-tile mode lookup in the
+// coding kernels measured +0.34 ms on config 1 (A/B, profiles/r02).
+template <bool kCM>
 __device__ __forceinline__ int chain_mode(const ChainTab& ct, int chain) {
-#ifdef HDLL_EXP_NOCMODE  // A/B experiment only: per-chain modes off (band pieces wrong)
+  if constexpr (kCM) return ct.chain_mode[chain];
   return ct.mode;
-#else
-  return ct.chain_mode ? ct.chain_mode[chain] : ct.mode;
-#endif
 }
 
 // the next ticket's tile, passing over the tiles of chains that are not run
+template <bool kCM>
 __device__ __forceinline__ bool next_tile(const ChainTab& ct, int* chain, long long* tin, long long* g) {
   const int lane = threadIdx.x & 31;
   for (;;) {
@@ -178,7 +180,7 @@ __device__ __forceinline__ bool next_tile(const ChainTab& ct, int* chain, long l
     *tin = ct.seg_r0[k] + rel / act;
     *chain = ct.rr_chain[rel % act];
     *g = ct.tile_base[*chain] + *tin;
-    if (chain_mode(ct, *chain) != kModeSkip) return true;
+    if (!kCM || chain_mode<kCM>(ct, *chain) != kModeSkip) return true;
   }
 }
 
@@ -320,11 +322,11 @@ struct LaneState {
 //   NL local contexts used by the tile, mapped to chain contexts base..base+NL-1,
 //   NC contexts carried by the chain.
 // ---------------------------------------------------------------------------
-template <int NL, int NC, class Gen>
+template <int NL, int NC, bool kCM, class Gen>
 __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long g, int base, const Gen& gen,
                          const int* cnt_in, const LaneState& ls, unsigned* status, uint32_t* scr, int scr_cap) {
   const int lane = threadIdx.x & 31;
-  const int mode = chain_mode(ct, chain);
+  const int mode = chain_mode<kCM>(ct, chain);
 #ifdef HDLL_EXP_NO_LB  // timing experiment only: no look-backs (wrong output)
   const bool chain_start = true;
 #else
@@ -955,6 +957,7 @@ struct PlaneBufGen {
 #endif
 
 // grid-persistent, 4 warps per CTA, each warp's context state in shared memory
+template <bool kCM>
 __global__ void __launch_bounds__(HDLL_PLANE_LB) k_entropy_plane(const ImgDesc* __restrict__ descs, ChainTab ct, uint4* symbuf,
                                                        int cap_chunks, uint32_t* wordbuf) {
   __shared__ __align__(16) uint8_t smem_pl[4 * lane_state_bytes(5)];
@@ -964,7 +967,7 @@ __global__ void __launch_bounds__(HDLL_PLANE_LB) k_entropy_plane(const ImgDesc* 
   uint32_t* scr = wordbuf + ((long long)blockIdx.x * 4 + warp) * cap_chunks * 8 * 32 + lane;  // <= 1 word per symbol
   int chain;
   long long tin, g;
-  while (next_tile(ct, &chain, &tin, &g)) {
+  while (next_tile<kCM>(ct, &chain, &tin, &g)) {
     const ImgDesc& d = descs[ct.img[chain]];
     const int kind = ct.kind[chain];
     const int S = plane_segs(d.w, ct.plane_segw), wseg = plane_seg_width(d.w, ct.plane_segw);
@@ -1053,7 +1056,7 @@ __global__ void __launch_bounds__(HDLL_PLANE_LB) k_entropy_plane(const ImgDesc* 
 #ifdef HDLL_EXP_COUNT_ONLY  // timing experiment: the generation pass alone
     if (cnt[0] == -1) atomicOr(d.status, 1u);
 #else
-    run_tile<5, 5>(ct, chain, tin, g, 0, gen, cnt, ls, d.status, scr, cap_chunks * 8);
+    run_tile<5, 5, kCM>(ct, chain, tin, g, 0, gen, cnt, ls, d.status, scr, cap_chunks * 8);
 #endif
     __syncwarp();
   }
@@ -1065,6 +1068,7 @@ __global__ void __launch_bounds__(HDLL_PLANE_LB) k_entropy_plane(const ImgDesc* 
 // a block's code: <= 544 bytes (dct_chain_cap) = 136 words
 constexpr int kDctScrWords = 136;
 
+template <bool kCM>
 __global__ void __launch_bounds__(HDLL_DCT_LB) k_entropy_dct(const ImgDesc* __restrict__ descs, ChainTab ct, uint32_t* wordbuf) {
   __shared__ __align__(16) uint8_t smem_dct[4 * lane_state_bytes(3)];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1072,7 +1076,7 @@ __global__ void __launch_bounds__(HDLL_DCT_LB) k_entropy_dct(const ImgDesc* __re
   uint32_t* scr = wordbuf + ((long long)blockIdx.x * 4 + warp) * kDctScrWords * 32 + lane;
   int chain;
   long long tin, g;
-  while (next_tile(ct, &chain, &tin, &g)) {
+  while (next_tile<kCM>(ct, &chain, &tin, &g)) {
     const ImgDesc& d = descs[ct.img[chain]];
     const long long units = ct.units[chain];
     const long long tpc = (units + 31) / 32;
@@ -1110,7 +1114,7 @@ __global__ void __launch_bounds__(HDLL_DCT_LB) k_entropy_dct(const ImgDesc* __re
       cnt[1] = nnz + ((nzm >> 63) ? 0 : 1);  // runs + EOB (absent when position 63 is coded)
       cnt[2] = nnz;
     }
-    run_tile<3, 6>(ct, chain, tin, g, ci == 0 ? 0 : 3, gen, cnt, ls, d.status, scr, kDctScrWords);
+    run_tile<3, 6, kCM>(ct, chain, tin, g, ci == 0 ? 0 : 3, gen, cnt, ls, d.status, scr, kDctScrWords);
     __syncwarp();
   }
 }
@@ -1133,7 +1137,7 @@ __global__ void __launch_bounds__(256) k_entropy_fixup(ChainTab ct) {
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= ct.ntiles) return;
   const int chain = find_chain(ct, g);
-  if (chain_mode(ct, chain) != 0) return;
+  if (ct.chain_mode && chain_mode<true>(ct, chain) != 0) return;
   const long long gend = ct.tile_base[chain + 1];
   const long long e = (long long)ct.bitv[g * 2 + 1];
   const long long s = e - (long long)ct.bitv[g * 2 + 0];
@@ -1158,7 +1162,7 @@ __global__ void __launch_bounds__(256) k_entropy_fixup(ChainTab ct) {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(32) k_chain_maps(ChainTab ct) {
   const int chain = blockIdx.x, c = blockIdx.y, lane = threadIdx.x;
-  if (chain_mode(ct, chain) != 2) return;
+  if ((ct.chain_mode ? chain_mode<true>(ct, chain) : ct.mode) != 2) return;
   const long long t0 = ct.tile_base[chain], nt = ct.tile_base[chain + 1] - t0;
   const long long per = (nt + 31) / 32;
   AMap m = amap_identity();
@@ -1190,7 +1194,7 @@ static int num_sms() {
 
 static long long dct_grid(const ChainTab& ct) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_entropy_dct, 128, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_entropy_dct<false>, 128, 0);
   long long blocks = (long long)num_sms() * (per_sm > 0 ? per_sm : 1);
   const long long need = (ct.ntiles + 3) / 4;
   return blocks < need ? blocks : need;
@@ -1203,12 +1207,13 @@ size_t dct_scratch_bytes(const ChainTab& ct) {
 
 void launch_entropy_dct(const ImgDesc* d_descs, const ChainTab& ct, void* scratch, cudaStream_t st) {
   if (ct.ntiles <= 0) return;
-  k_entropy_dct<<<(unsigned)dct_grid(ct), 128, 0, st>>>(d_descs, ct, (uint32_t*)scratch);
+  if (ct.chain_mode) k_entropy_dct<true><<<(unsigned)dct_grid(ct), 128, 0, st>>>(d_descs, ct, (uint32_t*)scratch);
+  else k_entropy_dct<false><<<(unsigned)dct_grid(ct), 128, 0, st>>>(d_descs, ct, (uint32_t*)scratch);
 }
 
 static long long plane_grid(const ChainTab& ct) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_entropy_plane, 128, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_entropy_plane<false>, 128, 0);
   long long blocks = (long long)num_sms() * (per_sm > 0 ? per_sm : 1);
   const long long need = (ct.ntiles + 3) / 4;
   return blocks < need ? blocks : need;
@@ -1236,7 +1241,8 @@ void launch_entropy_plane(const ImgDesc* d_descs, const ChainTab& ct, int max_w,
   const int cc = plane_cap_chunks(max_w, ct.plane_segw);
   uint4* slabs = (uint4*)scratch;
   uint32_t* words = (uint32_t*)(slabs + grid * 4 * 32 * cc);
-  k_entropy_plane<<<(unsigned)grid, 128, 0, st>>>(d_descs, ct, slabs, cc, words);
+  if (ct.chain_mode) k_entropy_plane<true><<<(unsigned)grid, 128, 0, st>>>(d_descs, ct, slabs, cc, words);
+  else k_entropy_plane<false><<<(unsigned)grid, 128, 0, st>>>(d_descs, ct, slabs, cc, words);
 }
 
 void launch_entropy_fixup(const ChainTab& ct, cudaStream_t st) {

@@ -661,70 +661,79 @@ __global__ void __launch_bounds__(256) k_seg_reduce_coef(const ImgDesc* __restri
 // sigma = 0 (north_star item 3): S* = S is an integer
 // plane, so every sum of fit_region (estimator.py:159-162) is an exact integer
 // below 2^53 whatever the order -- numpy's pairwise x.sum() and OpenBLAS's ddot
-// (FMA of integer products) included.  No sort: every CTA privatises
+// (FMA of integer products) included.  No sort.  Every warp privatises
 // per-(channel, exponent) bins of sum x, sum y, sum x^2, sum x*y in shared
-// memory, lanes holding the same bin merge through warp reductions first, and
-// the CTA's bins are added into the image's int64 table with global atomics.
-// The coefficients then follow the reference's fp64 formula from the exact
-// sums (k_fit_int_coef), bit-identical to the order-replicating path.
+// memory (32-bit: a warp flushes them every kIntChunk pixels, and
+// 255^2 * kIntChunk < 2^32); lanes holding the same exponent first merge
+// through warp reductions, so the group leaders -- one per distinct exponent
+// -- update distinct bins with plain loads and stores, no atomics.  A flush
+// adds the warp's non-zero bins into the image's int64 table with global
+// atomics.  The coefficients then follow the reference's fp64 formula from
+// the exact sums (k_fit_int_coef), bit-identical to the order-replicating path.
 // ---------------------------------------------------------------------------
-struct IntFitSmem {
-  unsigned long long sxx[3][256], sxy[3][256];
-  unsigned sx[3][256], sy[3][256];
+constexpr int kIntWarps = 4;
+constexpr int kIntChunk = 16384;  // pixels per warp between flushes
+static_assert(255ull * 255ull * kIntChunk < (1ull << 32), "a warp's 32-bit bins cannot overflow between flushes");
+
+struct IntWarpBins {
+  unsigned v[12][256];  // [channel * 4 + (sum x, sum y, sum x^2, sum x*y)][exponent]
 };
 
-__global__ void __launch_bounds__(256) k_fit_int(const ImgDesc* __restrict__ descs) {
+__global__ void __launch_bounds__(32 * kIntWarps) k_fit_int(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
   if (!d.int_fit) return;
-  __shared__ IntFitSmem sm;
-  for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) {
-    (&sm.sxx[0][0])[i] = 0ull;
-    (&sm.sxy[0][0])[i] = 0ull;
-    (&sm.sx[0][0])[i] = 0u;
-    (&sm.sy[0][0])[i] = 0u;
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
+  __shared__ IntWarpBins sb[kIntWarps];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned* W = &sb[w].v[0][0];
+  for (int i = lane; i < 12 * 256; i += 32) W[i] = 0u;
+  __syncwarp();
   const unsigned lt = (1u << lane) - 1u;
   const bool global = d.global_regression != 0;
   // the fit samples: desc pixels [fit_p0, fit_p0 + fit_m) (a row band's own rows)
   const long long n = d.fit_m, plane = d.n;
   const uint32_t* px = reinterpret_cast<const uint32_t*>(d.rgbe) + d.fit_p0;
   const uint8_t* S = d.s_planes + d.fit_p0;
-  // one pixel per lane per step; the grid stride keeps warps on whole 32-pixel rows of memory
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long b0 = (long long)blockIdx.x * blockDim.x; b0 < n; b0 += stride) {
-    const long long p = b0 + threadIdx.x;
-    const bool valid = p < n;
-    const unsigned act = __ballot_sync(0xffffffffu, valid);
-    if (!valid) continue;
-    const uint32_t q = __ldg(px + p);
-    const unsigned key = global ? 0u : (q >> 24);  // global_regression: one (c, 0) segment per plane
-    const unsigned peers = __match_any_sync(act, key);
-    const bool leader = (peers & lt) == 0;
+  unsigned long long* isum = reinterpret_cast<unsigned long long*>(d.isum);
+  unsigned long long* sumy = reinterpret_cast<unsigned long long*>(d.sum_y);
+  const long long nchunks = (n + kIntChunk - 1) / kIntChunk;
+  for (long long ch = (long long)blockIdx.x * kIntWarps + w; ch < nchunks; ch += (long long)gridDim.x * kIntWarps) {
+    const long long p1 = min(n, (ch + 1) * kIntChunk);
+    for (long long b0 = ch * kIntChunk; b0 < p1; b0 += 32) {
+      const long long p = b0 + lane;
+      const bool valid = p < p1;
+      const unsigned act = __ballot_sync(0xffffffffu, valid);
+      if (valid) {
+        const uint32_t q = __ldg(px + p);
+        const unsigned key = global ? 0u : (q >> 24);  // global_regression: one (c, 0) segment per plane
+        const unsigned peers = __match_any_sync(act, key);
+        const bool leader = (peers & lt) == 0;
 #pragma unroll
-    for (int c = 0; c < 3; c++) {
-      const unsigned x = __ldg(S + (long long)c * plane + p), y = (q >> (8 * c)) & 0xFFu;
-      // a warp's partial sums fit 32 bits (32 * 255^2 < 2^21)
-      const unsigned rx = __reduce_add_sync(peers, x), ry = __reduce_add_sync(peers, y);
-      const unsigned rxx = __reduce_add_sync(peers, x * x), rxy = __reduce_add_sync(peers, x * y);
-      if (leader) {
-        atomicAdd(&sm.sx[c][key], rx);
-        atomicAdd(&sm.sy[c][key], ry);
-        atomicAdd(&sm.sxx[c][key], (unsigned long long)rxx);
-        atomicAdd(&sm.sxy[c][key], (unsigned long long)rxy);
+        for (int c = 0; c < 3; c++) {
+          const unsigned x = __ldg(S + (long long)c * plane + p), y = (q >> (8 * c)) & 0xFFu;
+          // a warp's partial sums: x and y below 32 * 255 < 2^16 each (one
+          // reduction for both), x^2 and x*y below 2^21
+          const unsigned rxy1 = __reduce_add_sync(peers, x | (y << 16));
+          const unsigned rxx = __reduce_add_sync(peers, x * x), rxy = __reduce_add_sync(peers, x * y);
+          if (leader) {  // one leader per exponent in the warp: distinct bins
+            W[(c * 4 + 0) * 256 + key] += rxy1 & 0xFFFFu;
+            W[(c * 4 + 1) * 256 + key] += rxy1 >> 16;
+            W[(c * 4 + 2) * 256 + key] += rxx;
+            W[(c * 4 + 3) * 256 + key] += rxy;
+          }
+        }
       }
     }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) {
-    const unsigned long long xx = (&sm.sxx[0][0])[i];
-    if (xx == 0ull && (&sm.sy[0][0])[i] == 0u && (&sm.sx[0][0])[i] == 0u) continue;  // empty (or all-zero) bin
-    unsigned long long* g = reinterpret_cast<unsigned long long*>(d.isum) + 3 * i;
-    atomicAdd(g + 0, (unsigned long long)(&sm.sx[0][0])[i]);
-    atomicAdd(g + 1, xx);
-    atomicAdd(g + 2, (&sm.sxy[0][0])[i]);
-    atomicAdd(reinterpret_cast<unsigned long long*>(d.sum_y) + i, (unsigned long long)(&sm.sy[0][0])[i]);
+    __syncwarp();
+    for (int i = lane; i < 12 * 256; i += 32) {  // flush: the warp's non-zero bins into the int64 table
+      const unsigned v = W[i];
+      if (!v) continue;
+      W[i] = 0u;
+      const int k = i >> 8, e = i & 255, c = k >> 2, j = k & 3;
+      const int seg = c * 256 + e;
+      if (j == 1) atomicAdd(sumy + seg, (unsigned long long)v);
+      else atomicAdd(isum + 3 * seg + (j == 0 ? 0 : j - 1), (unsigned long long)v);
+    }
+    __syncwarp();
   }
 }
 
@@ -770,11 +779,12 @@ __global__ void __launch_bounds__(256) k_fit_int_coef(const ImgDesc* __restrict_
 }
 
 void launch_fit_int_sums(const ImgDesc* d_descs, int nimg, long long max_n, cudaStream_t st) {
-  long long gx = (max_n + 255) / 256;
+  // one warp per chunk, about 4 CTAs (48 KB of bins each) per SM over the batch
+  long long gx = (max_n + (long long)kIntChunk * kIntWarps - 1) / ((long long)kIntChunk * kIntWarps);
   const long long cap = (148 * 4 + nimg - 1) / nimg;
   if (gx > cap) gx = cap;
   if (gx < 1) gx = 1;
-  k_fit_int<<<dim3((unsigned)gx, nimg), 256, 0, st>>>(d_descs);
+  k_fit_int<<<dim3((unsigned)gx, nimg), 32 * kIntWarps, 0, st>>>(d_descs);
 }
 
 void launch_fit_int_coef(const ImgDesc* d_descs, int nimg, cudaStream_t st) {
@@ -782,13 +792,8 @@ void launch_fit_int_coef(const ImgDesc* d_descs, int nimg, cudaStream_t st) {
 }
 
 void launch_fit_int(const ImgDesc* d_descs, int nimg, long long max_n, cudaStream_t st) {
-  // about 4 CTAs per SM over the batch, each striding over its image
-  long long gx = (max_n + 255) / 256;
-  const long long cap = (148 * 4 + nimg - 1) / nimg;
-  if (gx > cap) gx = cap;
-  if (gx < 1) gx = 1;
-  k_fit_int<<<dim3((unsigned)gx, nimg), 256, 0, st>>>(d_descs);
-  k_fit_int_coef<<<dim3(kSegs / 256, nimg), 256, 0, st>>>(d_descs);
+  launch_fit_int_sums(d_descs, nimg, max_n, st);
+  launch_fit_int_coef(d_descs, nimg, st);
 }
 
 void launch_fit_hist(const ImgDesc* d_descs, int nimg, int max_sort_tiles, cudaStream_t st) {

@@ -463,6 +463,13 @@ def encode_band(ex, prep, rows_ptr: int, spec: BandSpec, ctx, stream_handle: int
                                                 _ptr(A32, ctypes.c_float), _ptr(B32, ctypes.c_float),
                                                 ctypes.byref(st)), "band_fit_coef")
         status = st.value
+    elif world == 1:
+        # 3-4 on one rank: its band is the image, its sorted samples all there are
+        hist_total = hist.astype(np.int64)
+        st = ctypes.c_uint32(0)
+        _native.check(L.hdll_b200_band_fit_local(h, _ptr(A32, ctypes.c_float), _ptr(B32, ctypes.c_float),
+                                                 ctypes.byref(st)), "band_fit_local")
+        status = st.value
     else:
         hists = np.stack(ex.allgather(hist)).astype(np.uint32)
         hist_total = hists.astype(np.int64).sum(0)
