@@ -661,6 +661,7 @@ def run_tiled(args):
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
         "parity_vs_reference": par_ref,
+        "phase_ms_rank0": dict(tiled.last_phase_ms),
     }
     print(json.dumps(line), flush=True)
     dist.destroy_process_group()

@@ -661,32 +661,27 @@ __global__ void __launch_bounds__(256) k_seg_reduce_coef(const ImgDesc* __restri
 // sigma = 0 (north_star item 3): S* = S is an integer
 // plane, so every sum of fit_region (estimator.py:159-162) is an exact integer
 // below 2^53 whatever the order -- numpy's pairwise x.sum() and OpenBLAS's ddot
-// (FMA of integer products) included.  No sort.  Every warp privatises
+// (FMA of integer products) included.  No sort.  Every CTA privatises
 // per-(channel, exponent) bins of sum x, sum y, sum x^2, sum x*y in shared
-// memory (32-bit: a warp flushes them every kIntChunk pixels, and
-// 255^2 * kIntChunk < 2^32); lanes holding the same exponent first merge
-// through warp reductions, so the group leaders -- one per distinct exponent
-// -- update distinct bins with plain loads and stores, no atomics.  A flush
-// adds the warp's non-zero bins into the image's int64 table with global
-// atomics.  The coefficients then follow the reference's fp64 formula from
-// the exact sums (k_fit_int_coef), bit-identical to the order-replicating path.
+// memory, 32-bit (12 KB, so eight CTAs fit an SM): the CTA flushes them every
+// kIntChunk pixels, and 255^2 * kIntChunk < 2^32.  Lanes holding the same
+// exponent first merge through warp reductions, so one native 32-bit shared
+// atomic per (distinct exponent in the warp, value) remains.  A flush adds
+// the CTA's non-zero bins into the image's int64 table with global atomics.
+// The coefficients then follow the reference's fp64 formula from the exact
+// sums (k_fit_int_coef), bit-identical to the order-replicating path.
 // ---------------------------------------------------------------------------
-constexpr int kIntWarps = 4;
-constexpr int kIntChunk = 16384;  // pixels per warp between flushes
-static_assert(255ull * 255ull * kIntChunk < (1ull << 32), "a warp's 32-bit bins cannot overflow between flushes");
+constexpr int kIntThreads = 256;
+constexpr int kIntChunk = kIntThreads * 64;  // pixels per CTA between flushes
+static_assert(255ull * 255ull * kIntChunk < (1ull << 32), "32-bit bins cannot overflow between flushes");
 
-struct IntWarpBins {
-  unsigned v[12][256];  // [channel * 4 + (sum x, sum y, sum x^2, sum x*y)][exponent]
-};
-
-__global__ void __launch_bounds__(32 * kIntWarps) k_fit_int(const ImgDesc* __restrict__ descs) {
+__global__ void __launch_bounds__(kIntThreads) k_fit_int(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
   if (!d.int_fit) return;
-  __shared__ IntWarpBins sb[kIntWarps];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  unsigned* W = &sb[w].v[0][0];
-  for (int i = lane; i < 12 * 256; i += 32) W[i] = 0u;
-  __syncwarp();
+  __shared__ unsigned W[12 * 256];  // [channel * 4 + (sum x, sum y, sum x^2, sum x*y)][exponent]
+  for (int i = threadIdx.x; i < 12 * 256; i += kIntThreads) W[i] = 0u;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const bool global = d.global_regression != 0;
   // the fit samples: desc pixels [fit_p0, fit_p0 + fit_m) (a row band's own rows)
@@ -696,35 +691,36 @@ __global__ void __launch_bounds__(32 * kIntWarps) k_fit_int(const ImgDesc* __res
   unsigned long long* isum = reinterpret_cast<unsigned long long*>(d.isum);
   unsigned long long* sumy = reinterpret_cast<unsigned long long*>(d.sum_y);
   const long long nchunks = (n + kIntChunk - 1) / kIntChunk;
-  for (long long ch = (long long)blockIdx.x * kIntWarps + w; ch < nchunks; ch += (long long)gridDim.x * kIntWarps) {
+  for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const long long p1 = min(n, (ch + 1) * kIntChunk);
-    for (long long b0 = ch * kIntChunk; b0 < p1; b0 += 32) {
-      const long long p = b0 + lane;
+    for (long long p = ch * kIntChunk + threadIdx.x; p - threadIdx.x < p1; p += kIntThreads) {
       const bool valid = p < p1;
       const unsigned act = __ballot_sync(0xffffffffu, valid);
-      if (valid) {
-        const uint32_t q = __ldg(px + p);
-        const unsigned key = global ? 0u : (q >> 24);  // global_regression: one (c, 0) segment per plane
-        const unsigned peers = __match_any_sync(act, key);
-        const bool leader = (peers & lt) == 0;
+      if (!valid) continue;
+      const uint32_t q = __ldg(px + p);
+      unsigned x[3];
 #pragma unroll
-        for (int c = 0; c < 3; c++) {
-          const unsigned x = __ldg(S + (long long)c * plane + p), y = (q >> (8 * c)) & 0xFFu;
-          // a warp's partial sums: x and y below 32 * 255 < 2^16 each (one
-          // reduction for both), x^2 and x*y below 2^21
-          const unsigned rxy1 = __reduce_add_sync(peers, x | (y << 16));
-          const unsigned rxx = __reduce_add_sync(peers, x * x), rxy = __reduce_add_sync(peers, x * y);
-          if (leader) {  // one leader per exponent in the warp: distinct bins
-            W[(c * 4 + 0) * 256 + key] += rxy1 & 0xFFFFu;
-            W[(c * 4 + 1) * 256 + key] += rxy1 >> 16;
-            W[(c * 4 + 2) * 256 + key] += rxx;
-            W[(c * 4 + 3) * 256 + key] += rxy;
-          }
+      for (int c = 0; c < 3; c++) x[c] = __ldg(S + (long long)c * plane + p);
+      const unsigned key = global ? 0u : (q >> 24);  // global_regression: one (c, 0) segment per plane
+      const unsigned peers = __match_any_sync(act, key);
+      const bool leader = (peers & lt) == 0;
+#pragma unroll
+      for (int c = 0; c < 3; c++) {
+        const unsigned y = (q >> (8 * c)) & 0xFFu;
+        // a warp's partial sums: x and y below 32 * 255 < 2^16 each (one
+        // reduction for both), x^2 and x*y below 2^21
+        const unsigned rxy1 = __reduce_add_sync(peers, x[c] | (y << 16));
+        const unsigned rxx = __reduce_add_sync(peers, x[c] * x[c]), rxy = __reduce_add_sync(peers, x[c] * y);
+        if (leader) {
+          atomicAdd(&W[(c * 4 + 0) * 256 + key], rxy1 & 0xFFFFu);
+          atomicAdd(&W[(c * 4 + 1) * 256 + key], rxy1 >> 16);
+          atomicAdd(&W[(c * 4 + 2) * 256 + key], rxx);
+          atomicAdd(&W[(c * 4 + 3) * 256 + key], rxy);
         }
       }
     }
-    __syncwarp();
-    for (int i = lane; i < 12 * 256; i += 32) {  // flush: the warp's non-zero bins into the int64 table
+    __syncthreads();
+    for (int i = threadIdx.x; i < 12 * 256; i += kIntThreads) {  // flush the non-zero bins into the int64 table
       const unsigned v = W[i];
       if (!v) continue;
       W[i] = 0u;
@@ -733,7 +729,7 @@ __global__ void __launch_bounds__(32 * kIntWarps) k_fit_int(const ImgDesc* __res
       if (j == 1) atomicAdd(sumy + seg, (unsigned long long)v);
       else atomicAdd(isum + 3 * seg + (j == 0 ? 0 : j - 1), (unsigned long long)v);
     }
-    __syncwarp();
+    __syncthreads();
   }
 }
 
@@ -779,12 +775,12 @@ __global__ void __launch_bounds__(256) k_fit_int_coef(const ImgDesc* __restrict_
 }
 
 void launch_fit_int_sums(const ImgDesc* d_descs, int nimg, long long max_n, cudaStream_t st) {
-  // one warp per chunk, about 4 CTAs (48 KB of bins each) per SM over the batch
-  long long gx = (max_n + (long long)kIntChunk * kIntWarps - 1) / ((long long)kIntChunk * kIntWarps);
-  const long long cap = (148 * 4 + nimg - 1) / nimg;
+  // one CTA per chunk, about 8 CTAs (12 KB of bins each) per SM over the batch
+  long long gx = (max_n + kIntChunk - 1) / kIntChunk;
+  const long long cap = (148 * 8 + nimg - 1) / nimg;
   if (gx > cap) gx = cap;
   if (gx < 1) gx = 1;
-  k_fit_int<<<dim3((unsigned)gx, nimg), 32 * kIntWarps, 0, st>>>(d_descs);
+  k_fit_int<<<dim3((unsigned)gx, nimg), kIntThreads, 0, st>>>(d_descs);
 }
 
 void launch_fit_int_coef(const ImgDesc* d_descs, int nimg, cudaStream_t st) {

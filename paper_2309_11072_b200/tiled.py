@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import ctypes
 import threading
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -419,6 +420,9 @@ def entering_a(out_a, maps, world: int) -> np.ndarray:
     return in_a
 
 
+last_phase_ms: dict = {}  # host wall time of the last encode_band's phases (each ends in a device sync)
+
+
 def encode_band(ex, prep, rows_ptr: int, spec: BandSpec, ctx, stream_handle: int, device, out=None):
     """Run one rank's band of a tile-sharded encode.  rows_ptr: device RGBE rows
     [spec.crow0, spec.crow1).  Rank 0 returns the serialized stream (bytes), or,
@@ -433,6 +437,13 @@ def encode_band(ex, prep, rows_ptr: int, spec: BandSpec, ctx, stream_handle: int
     specs = ex.specs
     im = container._image_struct(prep, rows_ptr)
     bd = _native.Band(spec.row0, spec.row1, spec.crow0, spec.crow1, spec.node0, spec.node1)
+    t_ph = [time.perf_counter()]
+    names_ph = []
+
+    def mark(name):
+        t_ph.append(time.perf_counter())
+        names_ph.append(name)
+
     # 1. tone-map node sums and max Lw
     nodes = np.zeros(1 + max(1, spec.node1 - spec.node0), np.float64)
     mx = ctypes.c_double(0.0)
@@ -442,10 +453,12 @@ def encode_band(ex, prep, rows_ptr: int, spec: BandSpec, ctx, stream_handle: int
     got = ex.allgather_var(nodes[: 1 + spec.node1 - spec.node0], [1 + s.node1 - s.node0 for s in specs])
     nodes_all = np.ascontiguousarray(np.concatenate([g[1:] for g in got]))
     maxlw = float(max(g[0] for g in got))
+    mark("begin")
     # 2. layers -> histogram
     hist = np.zeros(256, np.uint32)
     _native.check(L.hdll_b200_band_layers(h, _ptr(nodes_all, ctypes.c_double), nodes_all.size, maxlw,
                                           _ptr(hist, ctypes.c_uint32)), "band_layers")
+    mark("layers")
     A32 = np.zeros(768, np.float32)
     B32 = np.zeros(768, np.float32)
     status = 0
@@ -512,6 +525,7 @@ def encode_band(ex, prep, rows_ptr: int, spec: BandSpec, ctx, stream_handle: int
                 B32[sl] = t[768:1536].view(np.float32)[sl]
     if status & 1:  # kErrNonFinite: RegressionTable's ValueError (estimator.py:66-67)
         raise ValueError("regression parameters must be finite")
+    mark("fit")
     # 5. estimate, CRCs, piece counts; the pieces that start their chains are coded now
     first, need, emit = piece_roles(world)
     crc = np.zeros(5, np.uint32)
@@ -530,6 +544,7 @@ def encode_band(ex, prep, rows_ptr: int, spec: BandSpec, ctx, stream_handle: int
     outs_a = [m[nc:2 * nc].reshape(PIECES, NCTX) for m in meta]
     crc_all = [m[2 * nc:] for m in meta]
     in_cnt = prefix_counts(cnts, world)
+    mark("code")
     # 6. A-maps of the pieces between a chain's first and last (none for one rank)
     maps_all = None
     if need.any():
@@ -540,6 +555,7 @@ def encode_band(ex, prep, rows_ptr: int, spec: BandSpec, ctx, stream_handle: int
             _native.check(L.hdll_b200_band_maps(h, _ptr(mine, ctypes.c_int64), _ptr(nd, ctypes.c_int32),
                                                 _ptr(maps, ctypes.c_int64)), "band_maps")
         maps_all = ex.allgather(maps)
+    mark("maps")
     # 7. code the remaining pieces from their entering state, gather on rank 0
     if emit[rank].any():
         in_a = entering_a(outs_a, maps_all, world)
@@ -551,6 +567,7 @@ def encode_band(ex, prep, rows_ptr: int, spec: BandSpec, ctx, stream_handle: int
                                             _ptr(em, ctypes.c_int32), _ptr(bits7, ctypes.c_uint64),
                                             _ptr(ptrs, ctypes.c_uint64)), "band_emit")
         bits = np.where(emit[rank], bits7, bits)
+    mark("emit")
     bits_all = ex.allgather(bits.astype(np.int64)) if world > 1 else [bits.astype(np.int64)]
     nbytes = [int((int(b) + 31) // 32 * 4) for b in bits]
     all_ptrs, keep = ex.gather_pieces([int(p) for p in ptrs], nbytes, device)
@@ -583,6 +600,9 @@ def encode_band(ex, prep, rows_ptr: int, spec: BandSpec, ctx, stream_handle: int
                                               _ptr(pp, ctypes.c_uint64), _ptr(pb, ctypes.c_uint64), d_out.data_ptr(),
                                               cap, d_len.data_ptr(), stream_handle), "assemble_pieces")
     n = int(d_len.item())
+    mark("gather_assemble")
+    last_phase_ms.clear()
+    last_phase_ms.update({k: round((t1 - t0) * 1e3, 3) for k, t0, t1 in zip(names_ph, t_ph, t_ph[1:])})
     res = n if out is not None else bytes(d_out[:n].cpu().numpy())
     del keep
     ex.barrier()
