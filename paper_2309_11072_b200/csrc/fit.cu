@@ -664,9 +664,10 @@ __global__ void __launch_bounds__(256) k_seg_reduce_coef(const ImgDesc* __restri
 // (FMA of integer products) included.  No sort.  Every CTA privatises
 // per-(channel, exponent) bins of sum x, sum y, sum x^2, sum x*y in shared
 // memory, 32-bit (12 KB, so eight CTAs fit an SM): the CTA flushes them every
-// kIntChunk pixels, and 255^2 * kIntChunk < 2^32.  Lanes holding the same
-// exponent first merge through warp reductions, so one native 32-bit shared
-// atomic per (distinct exponent in the warp, value) remains.  A flush adds
+// kIntChunk pixels, and 255^2 * kIntChunk < 2^32.  Every pixel adds to its
+// bins with native 32-bit shared atomics (lanes of a warp sharing an exponent
+// collide on an address a few ways; warp-aggregating with match + reduce over
+// partial masks measured slower: config 1 fit 11.2 ms, c3 1.8 ms).  A flush adds
 // the CTA's non-zero bins into the image's int64 table with global atomics.
 // The coefficients then follow the reference's fp64 formula from the exact
 // sums (k_fit_int_coef), bit-identical to the order-replicating path.
@@ -675,47 +676,53 @@ constexpr int kIntThreads = 256;
 constexpr int kIntChunk = kIntThreads * 64;  // pixels per CTA between flushes
 static_assert(255ull * 255ull * kIntChunk < (1ull << 32), "32-bit bins cannot overflow between flushes");
 
+__device__ __forceinline__ void int_bins_add(unsigned* W, unsigned key, const unsigned (&x)[3], uint32_t q) {
+#pragma unroll
+  for (int c = 0; c < 3; c++) {
+    const unsigned y = (q >> (8 * c)) & 0xFFu;
+    atomicAdd(&W[(c * 4 + 0) * 256 + key], x[c]);
+    atomicAdd(&W[(c * 4 + 1) * 256 + key], y);
+    atomicAdd(&W[(c * 4 + 2) * 256 + key], x[c] * x[c]);
+    atomicAdd(&W[(c * 4 + 3) * 256 + key], x[c] * y);
+  }
+}
+
 __global__ void __launch_bounds__(kIntThreads) k_fit_int(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
   if (!d.int_fit) return;
   __shared__ unsigned W[12 * 256];  // [channel * 4 + (sum x, sum y, sum x^2, sum x*y)][exponent]
   for (int i = threadIdx.x; i < 12 * 256; i += kIntThreads) W[i] = 0u;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const unsigned lt = (1u << lane) - 1u;
   const bool global = d.global_regression != 0;
   // the fit samples: desc pixels [fit_p0, fit_p0 + fit_m) (a row band's own rows)
   const long long n = d.fit_m, plane = d.n;
   const uint32_t* px = reinterpret_cast<const uint32_t*>(d.rgbe) + d.fit_p0;
   const uint8_t* S = d.s_planes + d.fit_p0;
+  // four pixels per thread and step, as one 16-byte RGBE load and one 4-byte
+  // load per S plane when the planes' quads are aligned
+  const bool vec = ((d.fit_p0 | plane) & 3) == 0;
   unsigned long long* isum = reinterpret_cast<unsigned long long*>(d.isum);
   unsigned long long* sumy = reinterpret_cast<unsigned long long*>(d.sum_y);
   const long long nchunks = (n + kIntChunk - 1) / kIntChunk;
   for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const long long p1 = min(n, (ch + 1) * kIntChunk);
-    for (long long p = ch * kIntChunk + threadIdx.x; p - threadIdx.x < p1; p += kIntThreads) {
-      const bool valid = p < p1;
-      const unsigned act = __ballot_sync(0xffffffffu, valid);
-      if (!valid) continue;
-      const uint32_t q = __ldg(px + p);
-      unsigned x[3];
+    for (long long p = ch * kIntChunk + 4LL * threadIdx.x; p < p1; p += 4LL * kIntThreads) {
+      if (vec && p + 4 <= p1) {
+        const uint4 q4 = __ldg(reinterpret_cast<const uint4*>(px + p));
+        uint32_t sw[3];
 #pragma unroll
-      for (int c = 0; c < 3; c++) x[c] = __ldg(S + (long long)c * plane + p);
-      const unsigned key = global ? 0u : (q >> 24);  // global_regression: one (c, 0) segment per plane
-      const unsigned peers = __match_any_sync(act, key);
-      const bool leader = (peers & lt) == 0;
+        for (int c = 0; c < 3; c++) sw[c] = __ldg(reinterpret_cast<const uint32_t*>(S + (long long)c * plane + p));
+        const uint32_t qs[4] = {q4.x, q4.y, q4.z, q4.w};
 #pragma unroll
-      for (int c = 0; c < 3; c++) {
-        const unsigned y = (q >> (8 * c)) & 0xFFu;
-        // a warp's partial sums: x and y below 32 * 255 < 2^16 each (one
-        // reduction for both), x^2 and x*y below 2^21
-        const unsigned rxy1 = __reduce_add_sync(peers, x[c] | (y << 16));
-        const unsigned rxx = __reduce_add_sync(peers, x[c] * x[c]), rxy = __reduce_add_sync(peers, x[c] * y);
-        if (leader) {
-          atomicAdd(&W[(c * 4 + 0) * 256 + key], rxy1 & 0xFFFFu);
-          atomicAdd(&W[(c * 4 + 1) * 256 + key], rxy1 >> 16);
-          atomicAdd(&W[(c * 4 + 2) * 256 + key], rxx);
-          atomicAdd(&W[(c * 4 + 3) * 256 + key], rxy);
+        for (int k = 0; k < 4; k++) {
+          const unsigned x[3] = {(sw[0] >> (8 * k)) & 0xFFu, (sw[1] >> (8 * k)) & 0xFFu, (sw[2] >> (8 * k)) & 0xFFu};
+          int_bins_add(W, global ? 0u : (qs[k] >> 24), x, qs[k]);  // global_regression: one (c, 0) segment
+        }
+      } else {
+        for (long long pp = p; pp < min(p + 4, p1); pp++) {
+          const uint32_t q = __ldg(px + pp);
+          const unsigned x[3] = {__ldg(S + pp), __ldg(S + plane + pp), __ldg(S + 2 * plane + pp)};
+          int_bins_add(W, global ? 0u : (q >> 24), x, q);
         }
       }
     }

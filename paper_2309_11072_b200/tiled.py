@@ -450,10 +450,11 @@ def encode_band(ex, prep, rows_ptr: int, spec: BandSpec, ctx, stream_handle: int
     _native.check(L.hdll_b200_band_begin(h, ctypes.byref(im), ctypes.byref(bd), stream_handle,
                                          _ptr(nodes[1:], ctypes.c_double), ctypes.byref(mx)), "band_begin")
     nodes[0] = mx.value
+    mark("begin_device")
     got = ex.allgather_var(nodes[: 1 + spec.node1 - spec.node0], [1 + s.node1 - s.node0 for s in specs])
     nodes_all = np.ascontiguousarray(np.concatenate([g[1:] for g in got]))
     maxlw = float(max(g[0] for g in got))
-    mark("begin")
+    mark("begin_exchange")
     # 2. layers -> histogram
     hist = np.zeros(256, np.uint32)
     _native.check(L.hdll_b200_band_layers(h, _ptr(nodes_all, ctypes.c_double), nodes_all.size, maxlw,
