@@ -18,6 +18,9 @@
 // A band recomputes the halo rows it needs (one DCT block row above for the DC
 // predictor and the prefilter / plane-coder neighbourhoods) from the RGBE
 // rows it holds, so no pixel data crosses ranks except the fit samples.
+#include <chrono>
+#include <cstdlib>
+
 #include "host_common.cuh"
 #include "pairwise.cuh"
 
@@ -73,6 +76,18 @@ void band_free(Ctx* c) {
 }  // namespace hdll_host
 
 namespace {
+
+// HDLL_B200_BAND_TIMING=1: host time of band_begin's steps on stderr (diagnostic)
+struct StepClock {
+  bool on = std::getenv("HDLL_B200_BAND_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "band_begin %s %.3f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 
 // pixel range of depth-L node idx of the pairwise tree over n (pairwise.cuh)
 void node_range(long long n, int L, long long idx, long long* p0, long long* p1) {
@@ -182,8 +197,10 @@ int hdll_b200_band_begin(hdll_b200_ctx* ctx, const hdll_b200_image* img, const h
     node_range(full_n, level, (long long)bd.node1 - 1, &a, &px1);
   }
   if (px0 < (long long)bd.crow0 * W || px1 > (long long)bd.crow1 * W) return HDLL_B200_E_ARG;
+  StepClock clk;
   CK(cudaSetDevice(c->device));
   if (c->done_ev) CK(cudaEventSynchronize(c->done_ev));  // the shared coder scratch of an encode batch
+  clk.mark("sync");
   c->launches = 0;
   if (!c->band) c->band = new Band();
   Band* b = c->band;
@@ -207,6 +224,7 @@ int hdll_b200_band_begin(hdll_b200_ctx* ctx, const hdll_b200_image* img, const h
   b->L = plan(b->im, false);
   if (ensure(&b->arena, &b->arena_cap, b->L.total, true)) return HDLL_B200_E_CUDA;
   uint8_t* B = (uint8_t*)b->arena;
+  clk.mark("arena");
 
   // chain pieces: Y, Cb, Cr of the band's block rows, then the E, R, G, B rows
   const int nbx = (W + 7) / 8;
@@ -231,6 +249,7 @@ int hdll_b200_band_begin(hdll_b200_ctx* ctx, const hdll_b200_image* img, const h
     b->hc_pln.add(0, k, -1, b->y0 - b->c0, rows, b->piece_ptr[2 + k], (long long)pln_cap, W);
   b->hc_dct.schedule();
   b->hc_pln.schedule();
+  clk.mark("chains");
 
   // host staging -> tabs: desc, parameters, nodes (reserved), chain tables, tickets
   const size_t nodes_bytes = sizeof(double) * ((size_t)1 << level);
@@ -276,15 +295,21 @@ int hdll_b200_band_begin(hdll_b200_ctx* ctx, const hdll_b200_image* img, const h
   b->d_nodes = d.tm_nodes;
   b->d_ticket = (int*)(D + t_ticket);
   memcpy(Hs + t_desc, &d, sizeof(ImgDesc));
+  clk.mark("staging");
   CK(cudaMemcpyAsync(D, Hs, so, cudaMemcpyHostToDevice, b->st));
   CK(cudaMemsetAsync(B + b->L.off_zero, 0, kZeroBytes, b->st));
   launch_tonemap_partial(b->d_desc, 1, d.n, level, b->st);
+  if (clk.on) {
+    CK(cudaStreamSynchronize(b->st));
+    clk.mark("upload+tonemap");
+  }
   c->launches += 2;
   const size_t nn = (size_t)(b->node1 - b->node0);
   if (nn) CK(cudaMemcpyAsync(h_nodes, b->d_nodes + b->node0, sizeof(double) * nn, cudaMemcpyDeviceToHost, b->st));
   unsigned long long mx = 0;
   CK(cudaMemcpyAsync(&mx, d.maxlw, 8, cudaMemcpyDeviceToHost, b->st));
   if (int rc = sync_status(b)) return rc;
+  clk.mark("readback");
   memcpy(h_maxlw, &mx, 8);
   return HDLL_B200_OK;
 }

@@ -134,18 +134,32 @@ __global__ void __launch_bounds__(256) k_sort_scatter(const ImgDesc* __restrict_
     }
     return;
   }
-  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&sm.wcnt[0][0])[i] = 0;
-  __syncthreads();
   constexpr int kPerWarp = kSortTile / 8;
+  constexpr int kSteps = kPerWarp / 32;
   const int wb = w * kPerWarp;
   const unsigned lt = (1u << lane) - 1u;
-  for (int step = 0; step < kPerWarp / 32; step++) {
+  // the warp's RGBE words, all loads in flight before the counters are cleared
+  // (each used to be a dependent DRAM round trip per step); kept for the
+  // placement pass, with the exponent groups
+  uint32_t qv[kSteps];
+  unsigned pv[kSteps];
+#pragma unroll
+  for (int step = 0; step < kSteps; step++) {
+    const int k = wb + step * 32 + lane;
+    qv[step] = k < tn ? __ldg(px + t0 + k) : 0u;
+  }
+  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&sm.wcnt[0][0])[i] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int step = 0; step < kSteps; step++) {
     const int k = wb + step * 32 + lane;
     const bool valid = k < tn;
     const unsigned act = __ballot_sync(0xffffffffu, valid);
+    pv[step] = 0;
     if (valid) {
-      const unsigned e = px[t0 + k] >> 24;
+      const unsigned e = qv[step] >> 24;
       const unsigned peers = __match_any_sync(act, e);
+      pv[step] = peers;
       if ((peers & lt) == 0) sm.wcnt[w][e] += __popc(peers);
     }
   }
@@ -173,16 +187,15 @@ __global__ void __launch_bounds__(256) k_sort_scatter(const ImgDesc* __restrict_
     }
   }
   __syncthreads();
-  for (int step = 0; step < kPerWarp / 32; step++) {
+#pragma unroll
+  for (int step = 0; step < kSteps; step++) {
     const int k = wb + step * 32 + lane;
     const bool valid = k < tn;
-    const unsigned act = __ballot_sync(0xffffffffu, valid);
     unsigned e = 0, peers = 0;
     if (valid) {
-      const long long p = t0 + k;
-      const uint32_t q = px[p];
+      const uint32_t q = qv[step];
       e = q >> 24;
-      peers = __match_any_sync(act, e);
+      peers = pv[step];
       const unsigned slot = sm.wcnt[w][e] + __popc(peers & lt);
 #pragma unroll
       for (int c = 0; c < 3; c++) sm.ys[c][slot] = (uint8_t)((q >> (8 * c)) & 0xFF);
