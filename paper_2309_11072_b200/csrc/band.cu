@@ -199,6 +199,10 @@ int hdll_b200_band_begin(hdll_b200_ctx* ctx, const hdll_b200_image* img, const h
   if (px0 < (long long)bd.crow0 * W || px1 > (long long)bd.crow1 * W) return HDLL_B200_E_ARG;
   StepClock clk;
   CK(cudaSetDevice(c->device));
+  if (clk.on) {
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    clk.mark("pending work on the stream");
+  }
   if (c->done_ev) CK(cudaEventSynchronize(c->done_ev));  // the shared coder scratch of an encode batch
   clk.mark("sync");
   c->launches = 0;
@@ -297,11 +301,20 @@ int hdll_b200_band_begin(hdll_b200_ctx* ctx, const hdll_b200_image* img, const h
   memcpy(Hs + t_desc, &d, sizeof(ImgDesc));
   clk.mark("staging");
   CK(cudaMemcpyAsync(D, Hs, so, cudaMemcpyHostToDevice, b->st));
+  if (clk.on) {
+    CK(cudaStreamSynchronize(b->st));
+    clk.mark("upload");
+  }
   CK(cudaMemsetAsync(B + b->L.off_zero, 0, kZeroBytes, b->st));
+  if (clk.on) {
+    CK(cudaStreamSynchronize(b->st));
+    clk.mark("memset");
+  }
   launch_tonemap_partial(b->d_desc, 1, d.n, level, b->st);
   if (clk.on) {
     CK(cudaStreamSynchronize(b->st));
-    clk.mark("upload+tonemap");
+    clk.mark("tonemap");
+    fprintf(stderr, "band_begin staged %zu bytes, nodes [%lld, %lld) of 2^%d, n %lld\n", so, b->node0, b->node1, level, d.n);
   }
   c->launches += 2;
   const size_t nn = (size_t)(b->node1 - b->node0);

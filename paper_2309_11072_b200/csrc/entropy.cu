@@ -289,25 +289,23 @@ struct DctBlockGen {
     if (!z) return;
     int s = dcu ? 32 - __clz(dcu) : 0;
     f(0, 0, s, s, dcu);
-    // the next nonzero's coefficient is loaded one step ahead, so its latency
-    // overlaps the current symbol's coding (nzm has bit 0 clear: AC only)
+    // (loading the next nonzero's coefficient one symbol ahead measured
+    // slower: entropy_dct 2.85 -> 2.95 ms on config 1)
     int pos = 1, i = 1;
-    unsigned long long rest = nzm;
-    int nz = rest ? __ffsll((long long)rest) - 1 : 64;
-    int zv = rest ? __ldg(z + nz) : 0;
-    while (nz < 64) {
-      rest &= rest - 1;  // the nonzeros after nz
-      const int nz2 = rest ? __ffsll((long long)rest) - 1 : 64;
-      const int zv2 = rest ? __ldg(z + nz2) : 0;
+    while (pos < 64) {
+      const unsigned long long rest = nzm >> pos;
+      if (rest == 0) {
+        f(i, 1, kEOB, 0, 0u);
+        break;
+      }
+      const int nz = pos + __ffsll((long long)rest) - 1;
       f(i++, 1, nz - pos, 0, 0u);
+      const int zv = __ldg(z + nz);
       const unsigned u = zv >= 0 ? 2u * zv : (unsigned)(-2 * zv - 1);
       s = 32 - __clz(u);
       f(i++, 2, s, s, u);
       pos = nz + 1;
-      nz = nz2;
-      zv = zv2;
     }
-    if (pos < 64) f(i, 1, kEOB, 0, 0u);  // EOB unless position 63 was coded
   }
 };
 

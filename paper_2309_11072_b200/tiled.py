@@ -29,6 +29,8 @@ rank's kernel).
 from __future__ import annotations
 
 import ctypes
+import os
+import sys
 import threading
 import time
 from dataclasses import dataclass
@@ -229,6 +231,8 @@ class ThreadExchange:
 
 
 class _ThreadView:
+    pieces_in_place = True  # gather_pieces hands rank 0 the other ranks' device pointers
+
     def __init__(self, ex: ThreadExchange, rank: int):
         self.ex, self.rank, self.world = ex, rank, ex.world
 
@@ -302,6 +306,8 @@ class TorchExchange:
         import torch
 
         arr = np.ascontiguousarray(arr)
+        if self.world == 1:
+            return [arr.copy()]
         t = self._t(arr)
         out = torch.empty(self.world * t.numel(), dtype=torch.uint8, device=t.device)
         self.dist.all_gather_into_tensor(out, t, group=self.group)
@@ -321,6 +327,8 @@ class TorchExchange:
         import torch
 
         arr = np.ascontiguousarray(arr)
+        if self.world == 1:
+            return arr.copy()
         t = torch.from_numpy(arr.copy())
         if self.dev is not None:
             t = t.to(self.dev)
@@ -341,6 +349,8 @@ class TorchExchange:
         """Rank 0 receives every rank's piece streams; returns (device pointers per rank, keep-alive)."""
         import torch
 
+        if self.world == 1:
+            return [list(ptrs)], []
         sizes = self.allgather(np.asarray(nbytes, np.int64))
         if self.rank != 0:
             for p, n in zip(ptrs, nbytes):
@@ -420,6 +430,7 @@ def entering_a(out_a, maps, world: int) -> np.ndarray:
     return in_a
 
 
+_DIAG: dict = {}
 last_phase_ms: dict = {}  # host wall time of the last encode_band's phases (each ends in a device sync)
 
 
@@ -437,6 +448,16 @@ def encode_band(ex, prep, rows_ptr: int, spec: BandSpec, ctx, stream_handle: int
     specs = ex.specs
     im = container._image_struct(prep, rows_ptr)
     bd = _native.Band(spec.row0, spec.row1, spec.crow0, spec.crow1, spec.node0, spec.node1)
+    diag = bool(os.environ.get("HDLL_B200_BAND_TIMING"))
+    if diag:  # diagnostic: is device work pending when the encode starts?
+        t_s = time.perf_counter()
+        gap = 1e3 * (t_s - _DIAG.get("exit", t_s))
+        torch.cuda.synchronize()
+        t_1 = time.perf_counter()
+        torch.cuda.synchronize()
+        t_2 = time.perf_counter()
+        print(f"encode_band entry: host gap {gap:.3f} ms, device sync {1e3 * (t_1 - t_s):.3f} ms, "
+              f"again {1e3 * (t_2 - t_1):.3f} ms", file=sys.stderr)
     t_ph = [time.perf_counter()]
     names_ph = []
 
@@ -572,8 +593,13 @@ def encode_band(ex, prep, rows_ptr: int, spec: BandSpec, ctx, stream_handle: int
     bits_all = ex.allgather(bits.astype(np.int64)) if world > 1 else [bits.astype(np.int64)]
     nbytes = [int((int(b) + 31) // 32 * 4) for b in bits]
     all_ptrs, keep = ex.gather_pieces([int(p) for p in ptrs], nbytes, device)
+    # ThreadExchange: rank 0 reads the other ranks' pieces in place, so they
+    # wait until it has assembled.  TorchExchange sends them (stream-ordered on
+    # NCCL's stream before the next encode's first collective), no barrier.
+    in_place = getattr(ex, "pieces_in_place", False)
     if rank != 0:
-        ex.barrier()  # rank 0 reads the pieces in place (ThreadExchange) until it has assembled
+        if in_place:
+            ex.barrier()
         return None
     order = [[(r, c) for c in range(3) for r in range(world)]] + [[(r, 3 + k) for r in range(world)] for k in range(4)]
     npieces = np.asarray([len(ch) for ch in order], np.int32)
@@ -601,12 +627,18 @@ def encode_band(ex, prep, rows_ptr: int, spec: BandSpec, ctx, stream_handle: int
                                               _ptr(pp, ctypes.c_uint64), _ptr(pb, ctypes.c_uint64), d_out.data_ptr(),
                                               cap, d_len.data_ptr(), stream_handle), "assemble_pieces")
     n = int(d_len.item())
+    if diag:
+        t_s = time.perf_counter()
+        torch.cuda.synchronize()
+        print(f"encode_band exit device sync {1e3 * (time.perf_counter() - t_s):.3f} ms", file=sys.stderr)
+        _DIAG["exit"] = time.perf_counter()
     mark("gather_assemble")
     last_phase_ms.clear()
     last_phase_ms.update({k: round((t1 - t0) * 1e3, 3) for k, t0, t1 in zip(names_ph, t_ph, t_ph[1:])})
     res = n if out is not None else bytes(d_out[:n].cpu().numpy())
     del keep
-    ex.barrier()
+    if in_place:
+        ex.barrier()
     return res
 
 
