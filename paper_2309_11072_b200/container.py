@@ -640,6 +640,7 @@ class HostPipeline:
         self.h_len = [torch.zeros(c, dtype=torch.int64).pin_memory() for _ in range(ns)]
         self._ins, self._outs = ins, outs
         self.slot_free = [torch.cuda.Event() for _ in range(ns)]
+        self.timeline = None
         for e in self.slot_free:
             e.record(torch.cuda.current_stream(self.dev))
 
@@ -694,14 +695,24 @@ class HostPipeline:
         chunks = self._chunks(repeats)
         layouts = [self._layout(c) for c in chunks]
 
+        tl = self.timeline  # optional [(what, chunk, cuda event)] for tools/pipe_timeline.py
+
+        def mark(what, ci, stream):
+            if tl is not None:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(stream)
+                tl.append((what, ci, ev))
+
         def upload(ci):
             s = ci % ns
             self.s_h2d.wait_event(self.slot_free[s])
             oi = layouts[ci][0]
+            mark("h2d_start", ci, self.s_h2d)
             with torch.cuda.stream(self.s_h2d):
                 for k, i in enumerate(chunks[ci]):
                     nb = self.preps[i].pixels.nbytes
                     self.d_in[s][oi[k]:oi[k] + nb].copy_(h_in[i][:nb], non_blocking=True)
+            mark("h2d_end", ci, self.s_h2d)
             ev = torch.cuda.Event()
             ev.record(self.s_h2d)
             return ev
@@ -712,6 +723,7 @@ class HostPipeline:
             if ci + 1 < len(chunks):
                 up[ci + 1] = upload(ci + 1)  # next chunk's upload overlaps this chunk's encode
             self.s_comp.wait_event(up.pop(ci))
+            mark("enc_start", ci, self.s_comp)
             oi, oo = layouts[ci]
             bi, bo = self.d_in[s].data_ptr(), self.d_out[s].data_ptr()
             encode_device([self.preps[i] for i in idx], [bi + o for o in oi], [bo + o for o in oo],
@@ -719,9 +731,10 @@ class HostPipeline:
                           self.device, self.ctx)
             with torch.cuda.stream(self.s_comp):
                 self.h_len[s][: len(idx)].copy_(self.d_len[s][: len(idx)], non_blocking=True)
+            mark("enc_end", ci, self.s_comp)
             done = torch.cuda.Event()
             done.record(self.s_comp)
-            pending.append((idx, s, oo, done))
+            pending.append((idx, s, oo, done, ci))
             if len(pending) == 2:  # read back the previous chunk while this one computes
                 self._drain(pending.pop(0), h_out, lens)
         while pending:
@@ -732,9 +745,13 @@ class HostPipeline:
 
     def _drain(self, item, h_out, lens):
         torch = self.torch
-        idx, s, oo, done = item
+        idx, s, oo, done, ci = item
         done.synchronize()  # the chunk's lengths are on the host now
         self.s_d2h.wait_event(done)
+        if self.timeline is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(self.s_d2h)
+            self.timeline.append(("d2h_start", ci, ev))
         with torch.cuda.stream(self.s_d2h):
             for k, i in enumerate(idx):
                 n = int(self.h_len[s][k])
@@ -743,4 +760,8 @@ class HostPipeline:
                     raise RuntimeError(f"host output buffer of image {i} holds {h_out[i].numel()} bytes, "
                                        f"its stream has {n}")
                 h_out[i][:n].copy_(self.d_out[s][oo[k]:oo[k] + n], non_blocking=True)
+        if self.timeline is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(self.s_d2h)
+            self.timeline.append(("d2h_end", ci, ev))
         self.slot_free[s].record(self.s_d2h)

@@ -56,6 +56,27 @@ int stage_upload(uint8_t* D, const uint8_t* H, size_t bytes, uint8_t* const* zp,
   return cuda_fail(cudaGetLastError(), "stage");
 }
 
+// DCT coder lanes code this many consecutive blocks: more blocks per lane
+// spread each tile's fixed cost (three look-backs, the warp scans of counts
+// and A-maps, the release stores) over more symbols, as long as the launch
+// keeps enough tiles to fill the GPU (~kDctWaves waves of resident warps).
+#ifndef HDLL_DCT_WAVES
+#define HDLL_DCT_WAVES 6
+#endif
+int dct_blocks_per_lane(const hdll_b200_image* imgs, int n, int mode) {
+#ifdef HDLL_DCT_BPL  // experiment builds: a fixed value
+  return HDLL_DCT_BPL;
+#endif
+  if (mode == 1) return 1;
+  long long blocks = 0;
+  for (int i = 0; i < n; i++)
+    blocks += 3LL * ((imgs[i].width + 7) / 8) * ((imgs[i].height + 7) / 8);
+  const long long resident_warps = 148LL * 36;  // 9 CTAs of 4 warps per SM (56 registers)
+  int bpl = kDctMaxBlocksPerLane;
+  while (bpl > 1 && blocks / (32LL * bpl) < (long long)HDLL_DCT_WAVES * resident_warps) bpl >>= 1;
+  return bpl;
+}
+
 // mode: 0 full encode, 1 lossless plane (rgbe -> plane bytes), 2 lossy image (rgbe -> sdr rgb)
 int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out, const uint64_t* out_cap,
               uint64_t* d_out_len, cudaStream_t st, int mode) {
@@ -107,6 +128,7 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   // so twice as many chains share the GPU, and the assembly appends the
   // chroma bits to the Y bits.
   const bool dct_split = mode == 0;
+  hc_dct.dct_bpl = dct_blocks_per_lane(imgs, n, mode);
   for (int i = 0; i < n; i++) {
     const long long w = imgs[i].width, h = imgs[i].height;
     const long long nb = ((w + 7) / 8) * ((h + 7) / 8);

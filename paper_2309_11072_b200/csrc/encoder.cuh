@@ -130,8 +130,7 @@ inline __host__ __device__ int pairwise_level(long long n) {
 }
 
 constexpr int kMaxCtx = 6;
-constexpr int kDctBlocksPerLane = 1;                      // entropy tile: 32 lanes x 1 block
-constexpr int kDctTileBlocks = 32 * kDctBlocksPerLane;
+constexpr int kDctMaxBlocksPerLane = 4;  // entropy tile: 32 lanes x ChainTab::dct_bpl consecutive blocks
 constexpr int kPlaneTileRows = 32;                        // entropy tile: one row (segment) per lane
 
 // Plane entropy tiles: a row of width w is cut into the power-of-two number of
@@ -184,6 +183,7 @@ struct ChainTab {
   const int* chain_mode;       // [nchains] or null: per-chain mode overriding `mode` (kModeSkip: not run)
   int modes_present;           // host: bit m set when some chain runs mode m (launch_entropy_fixup)
   int plane_segw;              // plane rows are cut into segments of <= plane_segw samples
+  int dct_bpl;                 // DCT chains: consecutive blocks per lane (1..kDctMaxBlocksPerLane)
   // per global tile status (epoch-tagged)
   int* flags;                  // [ntiles][4]: cnt, map, bit, done
   long long* cnt;              // [ntiles][2][kMaxCtx]: aggregate, inclusive

@@ -309,6 +309,25 @@ struct DctBlockGen {
   }
 };
 
+// A lane's run of consecutive blocks (their nonzero masks and DC differences
+// staged in shared memory by the count pass): the blocks' symbols in order.
+struct DctRunGen {
+  static constexpr bool kStaticCtx = true;
+  const int16_t* z0;                    // the first block's coefficients (nullptr: idle lane)
+  const unsigned long long* nzm;        // [k * 32] this lane's masks, stride 32
+  const unsigned* dcu;                  // [k * 32]
+  int nb;                               // blocks of the lane
+  template <class F>
+  __device__ __forceinline__ void for_each(F&& f) const {
+    if (!z0) return;
+    int i = 0;
+    for (int k = 0; k < nb; k++) {
+      DctBlockGen b{z0 + 64LL * k, nzm[32 * k], dcu[32 * k]};
+      b.for_each([&](int, int c, int v, int xl, uint32_t xb) { f(i++, c, v, xl, xb); });
+    }
+  }
+};
+
 // Per-lane context state lives in shared memory, [context][lane], so a symbol
 // touches only its own context (no per-context predication).
 struct LaneState {
@@ -1065,7 +1084,7 @@ __global__ void __launch_bounds__(HDLL_PLANE_LB) k_entropy_plane(const ImgDesc* 
 }
 
 // ---------------------------------------------------------------------------
-// DCT coder: tile = 32 blocks of one component, lane = block
+// DCT coder: tile = 32 lanes x dct_bpl consecutive blocks of one component
 // ---------------------------------------------------------------------------
 // a block's code: <= 544 bytes (dct_chain_cap) = 136 words
 constexpr int kDctScrWords = 136;
@@ -1073,22 +1092,28 @@ constexpr int kDctScrWords = 136;
 template <bool kCM>
 __global__ void __launch_bounds__(HDLL_DCT_LB) k_entropy_dct(const ImgDesc* __restrict__ descs, ChainTab ct, uint32_t* wordbuf) {
   __shared__ __align__(16) uint8_t smem_dct[4 * lane_state_bytes(3)];
+  __shared__ unsigned long long s_nzm[4][kDctMaxBlocksPerLane * 32];
+  __shared__ unsigned s_dcu[4][kDctMaxBlocksPerLane * 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const LaneState ls = carve_state(smem_dct + warp * lane_state_bytes(3), 3);
-  uint32_t* scr = wordbuf + ((long long)blockIdx.x * 4 + warp) * kDctScrWords * 32 + lane;
+  const int bpl = ct.dct_bpl;
+  uint32_t* scr = wordbuf + ((long long)blockIdx.x * 4 + warp) * kDctScrWords * bpl * 32 + lane;
   int chain;
   long long tin, g;
   while (next_tile<kCM>(ct, &chain, &tin, &g)) {
     const ImgDesc& d = descs[ct.img[chain]];
     const long long units = ct.units[chain];
-    const long long tpc = (units + 31) / 32;
+    const long long per = 32LL * bpl;
+    const long long tpc = (units + per - 1) / per;
     const int comp = ct.comp[chain];  // >= 0: that component; -1: Y, Cb, Cr; -2: Cb, Cr
     const int ci = comp >= 0 ? comp : (comp == -2 ? 1 : 0) + (int)(tin / tpc);
     const long long tl = comp >= 0 ? tin : tin % tpc;
-    const long long bi = ct.first[chain] + tl * 32 + lane;  // block index in the image arrays
-    DctBlockGen gen{nullptr, 0ULL, 0u};
+    const long long u0 = tl * per + (long long)lane * bpl;  // the lane's first block in the chain
+    const int nb = (int)max(0LL, min((long long)bpl, units - u0));
+    const long long bi0 = ct.first[chain] + u0;             // ... in the image arrays
     int cnt[3] = {0, 0, 0};
-    if (tl * 32 + lane < units) {
+    for (int k = 0; k < nb; k++) {
+      const long long bi = bi0 + k;
       const int16_t* z = d.zz + ((long long)ci * d.nblocks + bi) * 64;
       // nonzero mask of the 64 zigzag coefficients, 128-bit loads
       const uint4* z4 = reinterpret_cast<const uint4*>(z);
@@ -1108,15 +1133,16 @@ __global__ void __launch_bounds__(HDLL_DCT_LB) k_entropy_dct(const ImgDesc* __re
       nzm &= ~1ULL;
       const int prev_dc = bi > 0 ? d.zz[((long long)ci * d.nblocks + bi - 1) * 64] : 0;
       const int dv = dc - prev_dc;
-      gen.z = z;
-      gen.nzm = nzm;
-      gen.dcu = dv >= 0 ? 2u * dv : (unsigned)(-2 * dv - 1);
+      s_nzm[warp][k * 32 + lane] = nzm;
+      s_dcu[warp][k * 32 + lane] = dv >= 0 ? 2u * dv : (unsigned)(-2 * dv - 1);
       const int nnz = __popcll(nzm);
-      cnt[0] = 1;
-      cnt[1] = nnz + ((nzm >> 63) ? 0 : 1);  // runs + EOB (absent when position 63 is coded)
-      cnt[2] = nnz;
+      cnt[0] += 1;
+      cnt[1] += nnz + ((nzm >> 63) ? 0 : 1);  // runs + EOB (absent when position 63 is coded)
+      cnt[2] += nnz;
     }
-    run_tile<3, 6, kCM>(ct, chain, tin, g, ci == 0 ? 0 : 3, gen, cnt, ls, d.status, scr, kDctScrWords);
+    const DctRunGen gen{nb > 0 ? d.zz + ((long long)ci * d.nblocks + bi0) * 64 : nullptr, &s_nzm[warp][lane],
+                        &s_dcu[warp][lane], nb};
+    run_tile<3, 6, kCM>(ct, chain, tin, g, ci == 0 ? 0 : 3, gen, cnt, ls, d.status, scr, kDctScrWords * bpl);
     __syncwarp();
   }
 }
@@ -1204,7 +1230,7 @@ static long long dct_grid(const ChainTab& ct) {
 
 size_t dct_scratch_bytes(const ChainTab& ct) {
   if (ct.ntiles <= 0) return 0;
-  return (size_t)dct_grid(ct) * 4 * 32 * kDctScrWords * sizeof(uint32_t);
+  return (size_t)dct_grid(ct) * 4 * 32 * kDctScrWords * ct.dct_bpl * sizeof(uint32_t);
 }
 
 void launch_entropy_dct(const ImgDesc* d_descs, const ChainTab& ct, void* scratch, cudaStream_t st) {

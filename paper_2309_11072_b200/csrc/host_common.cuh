@@ -241,6 +241,7 @@ struct HostChains {
   // chain of image i, kind k over `units` blocks / rows from `first`, DCT component cp (-1: all three);
   // plane tiles hold plane_tile_rows(width) rows
   int segw = 1 << 30;  // plane segment width (set before adding plane chains)
+  int dct_bpl = 1;     // DCT blocks per lane (set before adding DCT chains)
   void add(int i, int k, int cp, long long fst, long long nunits, uint8_t* o, long long c, int width) {
     img.push_back(i);
     kind.push_back(k);
@@ -253,7 +254,7 @@ struct HostChains {
       in_cnt.push_back(0);
       in_a.push_back(4);  // AdaptiveRiceState: A = 4 (_kernels.py:114-128)
     }
-    const long long per = k == 0 ? kDctTileBlocks : plane_tile_rows(width, segw);
+    const long long per = k == 0 ? 32LL * dct_bpl : plane_tile_rows(width, segw);
     const long long tiles = (k == 0 && cp < 0 ? (cp == -2 ? 2 : 3) : 1) * ((nunits + per - 1) / per);
     tile_base.push_back(tile_base.back() + tiles);
   }
@@ -342,6 +343,7 @@ struct HostChains {
     ct.chain_mode = nullptr;
     ct.modes_present = 1 << mode;
     ct.plane_segw = segw;
+    ct.dct_bpl = dct_bpl;
     size_t o = 0;
     ct.flags = (int*)(E + o) + t0 * 4;
     o += cap_t * 16;
