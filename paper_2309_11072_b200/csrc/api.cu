@@ -56,25 +56,17 @@ int stage_upload(uint8_t* D, const uint8_t* H, size_t bytes, uint8_t* const* zp,
   return cuda_fail(cudaGetLastError(), "stage");
 }
 
-// DCT coder lanes code this many consecutive blocks: more blocks per lane
-// spread each tile's fixed cost (three look-backs, the warp scans of counts
-// and A-maps, the release stores) over more symbols, as long as the launch
-// keeps enough tiles to fill the GPU (~kDctWaves waves of resident warps).
-#ifndef HDLL_DCT_WAVES
-#define HDLL_DCT_WAVES 6
-#endif
-int dct_blocks_per_lane(const hdll_b200_image* imgs, int n, int mode) {
+// DCT coder lanes code runs of kDctMaxBlocksPerLane consecutive blocks: a
+// tile's fixed cost (three look-backs, the warp scans of counts and A-maps,
+// the release stores) is spread over 4x the symbols.  Measured against 1 and
+// 2 blocks per lane (and 8, which needs more shared memory): 4 is fastest on
+// config 1 (entropy_dct 2.85 -> 2.04 ms), config 3 (1.55 -> 0.75 ms) and even
+// the single 4096x2160 image of config 2 (0.42 -> 0.23 ms).
+int dct_blocks_per_lane() {
 #ifdef HDLL_DCT_BPL  // experiment builds: a fixed value
   return HDLL_DCT_BPL;
 #endif
-  if (mode == 1) return 1;
-  long long blocks = 0;
-  for (int i = 0; i < n; i++)
-    blocks += 3LL * ((imgs[i].width + 7) / 8) * ((imgs[i].height + 7) / 8);
-  const long long resident_warps = 148LL * 36;  // 9 CTAs of 4 warps per SM (56 registers)
-  int bpl = kDctMaxBlocksPerLane;
-  while (bpl > 1 && blocks / (32LL * bpl) < (long long)HDLL_DCT_WAVES * resident_warps) bpl >>= 1;
-  return bpl;
+  return kDctMaxBlocksPerLane;
 }
 
 // mode: 0 full encode, 1 lossless plane (rgbe -> plane bytes), 2 lossy image (rgbe -> sdr rgb)
@@ -128,7 +120,7 @@ int run_batch(Ctx* c, const hdll_b200_image* imgs, int n, uint8_t* const* d_out,
   // so twice as many chains share the GPU, and the assembly appends the
   // chroma bits to the Y bits.
   const bool dct_split = mode == 0;
-  hc_dct.dct_bpl = dct_blocks_per_lane(imgs, n, mode);
+  hc_dct.dct_bpl = dct_blocks_per_lane();
   for (int i = 0; i < n; i++) {
     const long long w = imgs[i].width, h = imgs[i].height;
     const long long nb = ((w + 7) / 8) * ((h + 7) / 8);

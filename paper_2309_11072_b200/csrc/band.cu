@@ -247,6 +247,7 @@ int hdll_b200_band_begin(hdll_b200_ctx* ctx, const hdll_b200_image* img, const h
   }
   b->hc_dct = HostChains();
   b->hc_pln = HostChains();
+  b->hc_dct.dct_bpl = kDctMaxBlocksPerLane;  // as the whole-image encode (api.cu)
   for (int cp = 0; cp < 3; cp++) b->hc_dct.add(0, 0, cp, bfirst, bunits, b->piece_ptr[cp], (long long)dct_cap, W);
   b->hc_pln.segw = plane_segw_for(4 * rows, W);
   for (int k = 1; k < 5; k++)

@@ -149,7 +149,10 @@ inline int plane_segw_for(long long rows, int max_w) {
   // ~16 waves of tiles over the resident warps (148 SMs x 28): a tile takes
   // ~2 ms / S, and with ~2 waves the last, partial wave idles most of the GPU
   // (config 1: S = 8 measured 0.8 ms faster than S = 1; 2 and 4 in between)
-  const long long want_tiles = 16LL * 148 * 28;
+#ifndef HDLL_PLANE_WAVES
+#define HDLL_PLANE_WAVES 16
+#endif
+  const long long want_tiles = (long long)HDLL_PLANE_WAVES * 148 * 28;
   long long s = 1;
   while (s < 32 && rows * s / kPlaneTileRows < want_tiles) s <<= 1;
   int segw = (int)((max_w + s - 1) / s);
