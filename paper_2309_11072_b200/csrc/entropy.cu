@@ -749,6 +749,17 @@ struct SymChunk {  // 8 u16 symbols, shifted in at the top
 constexpr uint32_t kCtxTab = (1u << 2) | (1u << 4) | (2u << 6) | (2u << 8) | (2u << 10) | (2u << 12) | (2u << 14) |
                              (2u << 16) | (3u << 18);
 
+__device__ __forceinline__ uint32_t vmin_u16x2(uint32_t x, uint32_t y) {
+  uint32_t r;
+  asm("min.u16x2 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(y));
+  return r;
+}
+__device__ __forceinline__ uint32_t vmax_u16x2(uint32_t x, uint32_t y) {
+  uint32_t r;
+  asm("max.u16x2 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(y));
+  return r;
+}
+
 struct SegGen {
   int a, c;           // left and above-left neighbours of the next sample
   bool inrun;
@@ -757,6 +768,8 @@ struct SegGen {
   SymChunk ch;
   uint4* sp;          // the slab chunk being filled
   uint32_t cpk;       // regular contexts' counts, 8 bits each (< 256 between folds)
+  uint32_t fge2, fge3;  // word4's flags g > 2, g > 8 (16 per flag in a 16-bit lane)
+  int nfast;          // word4's regular samples since the last fold
   int cnt[5];
   // RowTrack
   bool brk;
@@ -776,6 +789,12 @@ struct SegGen {
     cnt[2] += (cpk >> 16) & 0xFF;
     cnt[3] += cpk >> 24;
     cpk = 0;
+    const int ge2 = (int)(((fge2 & 0xFFFFu) + (fge2 >> 16)) >> 4), ge3 = (int)(((fge3 & 0xFFFFu) + (fge3 >> 16)) >> 4);
+    cnt[1] += nfast - ge2;
+    cnt[2] += ge2 - ge3;
+    cnt[3] += ge3;
+    fge2 = fge3 = 0;
+    nfast = 0;
   }
   __device__ __forceinline__ void run_chunks() {  // chunks of <= 255; a chunk of 255 continues
     for (;;) {
@@ -820,6 +839,82 @@ struct SegGen {
     c = b;
     a = xv;
   }
+  // four symbols at once (s01: symbols 0, 1; s23: symbols 2, 3, 16 bits each)
+  __device__ __forceinline__ void put4(uint32_t s01, uint32_t s23) {
+    const unsigned long long S = (unsigned long long)s01 | ((unsigned long long)s23 << 32);
+    const int j = i & 7;  // symbols already in the chunk (at its top)
+    if (j >= 4) {         // it fills within these four: its 8 symbols start 16 j bits below S
+      const int sh = 128 - 16 * j;  // 16..64
+      unsigned long long w0, w1;
+      if (sh == 64) {
+        w0 = ch.hi;
+        w1 = S;
+      } else {
+        w0 = (ch.lo >> sh) | (ch.hi << (64 - sh));
+        w1 = (ch.hi >> sh) | (S << (64 - sh));
+      }
+      *sp = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
+      sp += 32;
+    }
+    ch.lo = ch.hi;
+    ch.hi = S;
+    i += 4;
+  }
+  // Four samples (bytes of cw; pw: the row above) of a row with a row above.
+  // Outside a run and with no sample whose a == b == c, all four are regular
+  // symbols: MED, activity context and folded residual come out of byte-SIMD
+  // and 16x2 arithmetic (VABSDIFF4, VIMNMX.U16x2, plain adds on 16-bit lanes
+  // that cannot carry); otherwise sample by sample.
+  __device__ __forceinline__ void word4(uint32_t cw, uint32_t pw, bool hp, bool track) {
+    const uint32_t a4 = __byte_perm(cw, (uint32_t)a, 0x2104);  // left neighbours [a, x0, x1, x2]
+    const uint32_t c4 = __byte_perm(pw, (uint32_t)c, 0x2104);  // above-left [c, p0, p1, p2]
+    const uint32_t z = (a4 ^ pw) | (pw ^ c4);                   // a zero byte: a == b == c there
+    if (!hp || inrun || ((z - 0x01010101u) & ~z & 0x80808080u)) {
+#pragma unroll 1
+      for (int k = 0; k < 4; k++) {
+        sample((int)(cw & 0xFF), (int)(pw & 0xFF), hp, track);
+        cw >>= 8;
+        pw >>= 8;
+      }
+      return;
+    }
+    const uint32_t d1 = __vabsdiffu4(a4, c4), d2 = __vabsdiffu4(c4, pw);
+    uint32_t sy[2];
+#pragma unroll
+    for (int hh = 0; hh < 2; hh++) {
+      const uint32_t sel = hh ? 0x4342u : 0x4140u;  // bytes 2hh, 2hh + 1 -> 16-bit lanes
+      const uint32_t x = __byte_perm(cw, 0u, sel), la = __byte_perm(a4, 0u, sel);
+      const uint32_t lb = __byte_perm(pw, 0u, sel), lc = __byte_perm(c4, 0u, sel);
+      // g = |a - c| + |c - b| (>= 1 here); ctx = 1 + [g > 2] + [g > 8] from min(g, 9)
+      const uint32_t gm = vmin_u16x2(__byte_perm(d1, 0u, sel) + __byte_perm(d2, 0u, sel), 0x00090009u);
+      const uint32_t f1 = (gm + 0x000D000Du) & 0x00100010u;  // bit 4 of a lane: g > 2
+      const uint32_t f2 = (gm + 0x00070007u) & 0x00100010u;  // g > 8
+      fge2 += f1;
+      fge3 += f2;
+      // MED = mn + mx - clamp(c, mn, mx); r = x - MED, low byte of each lane
+      const uint32_t mx = vmax_u16x2(la, lb), mn = vmin_u16x2(la, lb);
+      const uint32_t cl = vmax_u16x2(mn, vmin_u16x2(lc, mx));
+      const uint32_t r = x + cl + 0x04000400u - mn - mx;
+      // u = 2r or -2r - 1 (r a signed byte), ctx << 8 beside it
+      const uint32_t sgn = (r >> 7) & 0x00010001u;
+      const uint32_t hi = sgn * 0xFFu + (f1 + f2) * 16u + 0x01000100u;
+      sy[hh] = ((r << 1) & 0x00FE00FEu) ^ hi;
+    }
+    put4(sy[0], sy[1]);
+    if (track && !brk) {
+      const uint32_t e = cw ^ a4;  // nonzero byte: x != a (E false)
+      if (e) {
+        const int k = (__ffs((int)e) - 1) >> 3;
+        brk = true;
+        cov = nsamp + k;
+        brk_i = i - 3 + k;  // symbols up to and including sample k
+      }
+    }
+    nfast += 4;
+    nsamp += 4;
+    c = (int)(pw >> 24);
+    a = (int)(cw >> 24);
+  }
   // [x0, x1) of row `cur` (prev: the row above, or nullptr); with `track` the
   // RowTrack facts are recorded
   __device__ __forceinline__ void run(const uint8_t* cur, const uint8_t* prev, int x0, int x1, bool track) {
@@ -830,18 +925,13 @@ struct SegGen {
     if (((reinterpret_cast<uintptr_t>(cur + x0) | reinterpret_cast<uintptr_t>(pv + x0)) & 15) == 0) {
 #pragma unroll 1
       for (; x + 16 <= x1; x += 16) {
-        const uint4 c4 = __ldg(reinterpret_cast<const uint4*>(cur + x));
-        const uint4 p4 = __ldg(reinterpret_cast<const uint4*>(pv + x));
+        uint4 c4 = __ldg(reinterpret_cast<const uint4*>(cur + x));
+        uint4 p4 = __ldg(reinterpret_cast<const uint4*>(pv + x));
 #pragma unroll 1
         for (int q = 0; q < 4; q++) {
-          uint32_t cw = q == 0 ? c4.x : (q == 1 ? c4.y : (q == 2 ? c4.z : c4.w));
-          uint32_t pw = q == 0 ? p4.x : (q == 1 ? p4.y : (q == 2 ? p4.z : p4.w));
-#pragma unroll 1
-          for (int k = 0; k < 4; k++) {
-            sample((int)(cw & 0xFF), (int)(pw & 0xFF), hp, track);
-            cw >>= 8;
-            pw >>= 8;
-          }
+          word4(c4.x, p4.x, hp, track);
+          c4.x = c4.y, c4.y = c4.z, c4.z = c4.w;
+          p4.x = p4.y, p4.y = p4.z, p4.z = p4.w;
         }
         fold();
       }
@@ -957,6 +1047,7 @@ struct PlaneBufGen {
       SymChunk ch;
       ch.load(slab[(q0 >> 3) * 32]);
       const int m = min(8, n - q0);
+#pragma unroll 1  // compact: the kernel's hot code is at the edge of the instruction cache
       for (int j = 0; j < m; j++) {
         const uint32_t sy = ch.pop();
         if (q0 + j >= start) f(i++, (int)((sy >> 8) & 7), (int)(sy & 0xFF), 0, 0u);
@@ -1021,6 +1112,8 @@ __global__ void __launch_bounds__(HDLL_PLANE_LB) k_entropy_plane(const ImgDesc* 
       sg_.i = 0;
       sg_.sp = slab;
       sg_.cpk = 0;
+      sg_.fge2 = sg_.fge3 = 0;
+      sg_.nfast = 0;
 #pragma unroll
       for (int c = 0; c < 5; c++) sg_.cnt[c] = 0;
       sg_.brk = false;
