@@ -51,6 +51,14 @@ __device__ __forceinline__ int kfast(int a, int n) {
   return k < kRiceMaxK ? k : kRiceMaxK;
 }
 
+// kfast without the a <= n branch: bitlen(a - 1) - bitlen(n), clamped at 0,
+// plus one when n << k0 still falls short of a
+__device__ __forceinline__ int kfast_bf(int a, int n) {
+  int k0 = max(__clz(n) - __clz(max(a - 1, 0)), 0);
+  k0 += (n << k0) < a ? 1 : 0;
+  return min(k0, kRiceMaxK);
+}
+
 __device__ __noinline__ AMap amap_push_slow(AMap m, int u, int h) { return amap_push(m, u, h); }
 __device__ __noinline__ AMap amap_then_call(AMap f, AMap g) { return amap_then(f, g); }
 // exact o exact with a small total shift is the common case: inline it
@@ -63,6 +71,17 @@ __device__ __forceinline__ AMap amap_then_slow(const AMap& f, const AMap& g) {
     return r;
   }
   return amap_then_call(f, g);
+}
+
+// the plane coder's packed map state (run_tile) past the exact range: through AMap
+__device__ __noinline__ void plane_map_push_slow(int* x, int* c, int* t, int u, int h) {
+  const int n = *x & 63, sft = *x >> 8;
+  AMap m = sft == 15 ? AMap{*c, -1, *t} : AMap{*c, sft, 0};
+  m = amap_push(m, u, h);
+  const int nn = h ? kStateReset / 2 : n + 1;
+  *x = nn | ((m.s < 0 ? 15 : m.s) << 8);
+  *c = (int)m.c;
+  *t = m.t;
 }
 
 __device__ __forceinline__ void amap_push_fast(AMap& m, int u, int h) {
@@ -439,23 +458,31 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
       ls.mt[c * 32 + lane] = rmt[c];
     }
   } else {
+    // Per context one shared word X = N | shift << 8 (shift 15: a step map)
+    // and the map constant in 32 bits: while exact (shift < 14) it stays below
+    // 255 * (63 + 32 * (2^14 - 2)) < 2^28.
+    int* X = ls.nn;
+    int* C = ls.a;
+#pragma unroll
+    for (int c = 0; c < NL; c++) C[c * 32 + lane] = 0;
     gen.for_each([&](int, int c, int v, int, uint32_t) {
       const int o = c * 32 + lane;
-      const int nb = ls.nn[o];
-      const int h = nb == kStateReset - 1;  // N reaches 64: A and N halve
-      ls.nn[o] = h ? kStateReset / 2 : nb + 1;
-      const int sft = ls.ms[o];
-      if (sft >= 0 && sft + h < kADomainBits) {
-        ls.mc[o] += (long long)v << sft;
-        ls.ms[o] = sft + h;
+      const int x = X[o];
+      const int h = (x & 63) == kStateReset - 1;  // N reaches 64: A and N halve
+      const int xn = x + (h ? 0x100 - (kStateReset / 2 - 1) : 1);
+      if (xn < (kADomainBits << 8)) {
+        C[o] += v << (x >> 8);
+        X[o] = xn;
       } else {
-        AMap m{ls.mc[o], sft, ls.mt[o]};
-        m = amap_push_slow(m, v, h);
-        ls.mc[o] = m.c;
-        ls.ms[o] = m.s;
-        ls.mt[o] = m.t;
+        plane_map_push_slow(X + o, C + o, ls.mt + o, v, h);
       }
     });
+#pragma unroll
+    for (int c = 0; c < NL; c++) {
+      const int o = c * 32 + lane, sft = X[o] >> 8;
+      ls.mc[o] = C[o];
+      ls.ms[o] = sft == 15 ? -1 : sft;
+    }
   }
 #endif
   AMap pre[NL], agg[NL];
@@ -552,14 +579,17 @@ __device__ void run_tile(const ChainTab& ct, int chain, long long tin, long long
 #pragma unroll
     for (int c = 0; c < NL; c++) ls.a[c * 32 + lane] = a_start[c] | (n0[c] << 16);
     int nb32 = 0;
-    gen.for_each([&](int, int c, int v, int xl, uint32_t xb) {
+    gen.for_each([&](int, int c, int v, int xl, uint32_t xb) {  // (plane symbols: v <= 255, no raw bits)
       const int o = c * 32 + lane;
       int st = ls.a[o];
-      const int k = kfast(st & 0xFFFF, st >> 16);
-      const int rl = rice_len(v, k);
-      nb32 += rl + xl;
-      sb.put(rice_bits(v, k), rl);
-      if (xl) sb.put(xb, xl);
+      const int k = kfast_bf(st & 0xFFFF, st >> 16);
+      // _rice_put: q ones, a zero, k low bits; q >= 24: 24 ones and 8 raw bits
+      const int q = v >> k;
+      const bool esc = q >= kRiceEscapeQ;
+      const int rl = esc ? kRiceEscapeQ + 8 : q + 1 + k;  // <= 31 unless escaped (v <= 255)
+      const uint32_t bits = esc ? (0xFFFFFF00u | (uint32_t)v) : (1u << rl) - ((2u + q) << k) + (uint32_t)v;
+      nb32 += rl;
+      sb.put(bits, rl);
       st += v + (1 << 16);  // _update_state: A += u, N += 1; at N = 64 both halve
       if (st >= (kStateReset << 16)) st = (st >> 1) & ~0x8000;
       ls.a[o] = st;
