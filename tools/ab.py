@@ -12,8 +12,9 @@ nimg, cfg, rounds, steps = sys.argv[1:5]
 libs = sys.argv[5:]
 res = defaultdict(lambda: defaultdict(list))
 for r in range(int(rounds)):
-    for lib in libs:
-        env = dict(os.environ, HDLL_B200_LIB=os.path.abspath(lib))
+    for lib in libs:  # "path.so[,VAR=VALUE...]"
+        path, *kv = lib.split(",")
+        env = dict(os.environ, HDLL_B200_LIB=os.path.abspath(path), **dict(a.split("=", 1) for a in kv))
         out = subprocess.run([sys.executable, "tools/steptimes.py", nimg, cfg, steps], env=env,
                              capture_output=True, text=True)
         lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
