@@ -3,6 +3,8 @@ decoder (a restatement of container.py:233-280 pinned to the reference) on
 the golden streams produced by the real reference, on GPU-encoded config
 images, and on corrupted streams (the reference's exceptions, in its order)."""
 
+import hashlib
+
 import numpy as np
 import pytest
 
@@ -37,6 +39,8 @@ def test_decode_golden_streams(P, case):
     st = P.deserialize(blob)
     sdr = P.decode_sdr(st)
     assert sdr.as_array().shape == (st.height, st.width, 3)
+    # the base layer decodes to the encoder's decoded SDRI S, as the reference's does
+    assert hashlib.sha256(np.ascontiguousarray(sdr.as_array()).tobytes()).hexdigest() == case["s_sha256"]
     if st.sdr_only:
         with pytest.raises(P.StreamError):
             P.decode_hdr(st)

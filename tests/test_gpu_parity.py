@@ -3,7 +3,7 @@
 Bar: bit-exact bytes.  Per-stage traces (container.py:224-229) are compared
 first so a failure names the stage.  Sizes here are ones the CPU oracle
 finishes in seconds; full BASELINE sizes are covered by size-independent
-properties (round trip, batch == single) in test_gpu_configs.py.
+properties (round trip, batch == single) in test_gpu_configs.py and test_gpu_decode.py.
 """
 
 from __future__ import annotations
