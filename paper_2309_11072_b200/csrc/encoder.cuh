@@ -156,7 +156,10 @@ inline int plane_segw_for(long long rows, int max_w) {
   long long s = 1;
   while (s < 32 && rows * s / kPlaneTileRows < want_tiles) s <<= 1;
   int segw = (int)((max_w + s - 1) / s);
-  return segw < 256 ? 256 : segw;
+#ifndef HDLL_PLANE_MIN_SEGW
+#define HDLL_PLANE_MIN_SEGW 256
+#endif
+  return segw < HDLL_PLANE_MIN_SEGW ? HDLL_PLANE_MIN_SEGW : segw;
 }
 
 // Sequential-coder chains for the entropy kernel (entropy.cu).
