@@ -130,3 +130,45 @@ def test_sdr_only_stream(P):
     with pytest.raises(P.StreamError):
         P.decode_hdr(st)
     assert P.decode_sdr(st).as_array().shape == (48, 64, 3)
+
+
+def _outcome(fn):
+    try:
+        return ("ok", fn())
+    except Exception as e:  # the failure itself is what is compared
+        return ("fail", type(e).__name__)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_coder_bodies_truncated_or_flipped(P, seed):
+    """The coders' decode of damaged bodies fails exactly when the reference's
+    does (oracle decode_plane / lossy_decode_bits restate _kernels.py:219-262,
+    :327-378), and decodes to the same plane / SDRI when it does not: every
+    truncation of the last 24 bytes, 24 random cuts and 48 single-byte flips of
+    the base body and of the E and R bodies."""
+    from paper_2309_11072_b200 import codec, synth
+
+    rng = np.random.default_rng(seed)
+    px = synth.make_config(0, 5 + seed, scale=1.0)[:40, :56].copy()
+    st = P.encode(P.RadianceImage(56, 40, px, []))
+    h, w = 40, 56
+    pc, dc = codec.MedRicePlaneCoderB200(), codec.BlockDctCoderB200()
+    bodies = [("base", st.base_payload[9:]), ("e", st.e_payload[9:]), ("r", st.residual_payloads[0][9:])]
+    for kind, body in bodies:
+        bits = body[8:]
+        variants = [bits[:n] for n in range(max(0, len(bits) - 24), len(bits))]
+        variants += [bits[: int(n)] for n in rng.integers(0, len(bits), 24)]
+        for _ in range(48):
+            b = bytearray(bits)
+            b[int(rng.integers(0, len(b)))] ^= int(rng.integers(1, 256))
+            variants.append(bytes(b))
+        for v in variants:
+            if kind == "base":
+                got = _outcome(lambda: dc.decode(body[:8] + v, 85).as_array())
+                want = _outcome(lambda: O.lossy_decode_bits(v, h, w, 85))
+            else:
+                got = _outcome(lambda: pc.decode(body[:8] + v))
+                want = _outcome(lambda: O.decode_plane(v, h, w))
+            assert got[0] == want[0], (kind, len(v), got[1] if got[0] == "fail" else "", want)
+            if got[0] == "ok":
+                assert np.array_equal(np.asarray(got[1]), want[1]), (kind, len(v))
