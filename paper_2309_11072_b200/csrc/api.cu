@@ -399,7 +399,7 @@ int run_decode(Ctx* c, const hdll_b200_decode_image* imgs, int n, uint8_t* const
     CK(cudaMemsetAsync(ds[i].zz, 0, sizeof(int16_t) * 3 * ds[i].nblocks * 64, st));
   }
   const ImgDesc* dd = (const ImgDesc*)(D + t_descs);
-  if (!all_sdr && 8LL * max_w > 227 * 1024) return HDLL_B200_E_ARG;  // planes wider than 29k samples
+  if (!all_sdr && 8LL * ((max_w + 4) & ~3) + 2048 > 227 * 1024) return HDLL_B200_E_ARG;  // planes wider than ~28.8k samples
   launch_decode_coders(dd, n, !all_sdr, max_w, st);
   launch_reconstruct(dd, n, max_base_tiles, st);
   c->launches += 2;

@@ -117,12 +117,18 @@ struct FastBits {
   }
 };
 
+// row buffer stride of the plane decoder: whole words and a spare byte for
+// the one-sample-ahead load of the row above
+__host__ __device__ __forceinline__ int dec_row_stride(int w) { return (w + 4) & ~3; }
+
 // _select_k (_kernels.py:114-119): smallest k <= 15 with (N << k) >= A, closed
 // form without branches (A < 2^31: u < 24 << 15 per symbol, and A halves every
 // 32 symbols)
 __device__ __forceinline__ int select_k_dec(int a, int n) {
-  int k0 = max(__clz(n) - __clz(max(a - 1, 0)), 0);  // bitlen(a-1) - bitlen(n), clamped
-  k0 += ((long long)n << k0) < a ? 1 : 0;
+  // bitlen(a-1) - bitlen(n), clamped to [0, 16] (16 and above all give 15, and
+  // n << 16 < 2^22 for n <= 63, so the test stays in 32 bits)
+  int k0 = min(max(__clz(n) - __clz(max(a - 1, 0)), 0), 16);
+  k0 += (n << k0) < a ? 1 : 0;
   return min(k0, kRiceMaxK);
 }
 
@@ -241,7 +247,7 @@ __device__ __forceinline__ unsigned decode_plane_dev(const ImgDesc& d, int kind,
   for (int i = 0; i < 4; i++) sst[i] = 4u | (1u << 26);
   uint32_t kp = 0x2222u;  // select_k(4, 1) = 2 for every context
   const int w = d.w;
-  const int wpad = (w + 3) & ~3;
+  const int wpad = dec_row_stride(w);
   uint8_t* up = nullptr;
   uint8_t* cur = rows;
   for (int y = 0; y < d.h; y++) {
@@ -249,64 +255,68 @@ __device__ __forceinline__ unsigned decode_plane_dev(const ImgDesc& d, int kind,
     int x = 0;
     bool forced = false;
     int a = up ? up[0] : 128;  // a at x = 0 (_kernels.py:131-143)
-    int cprev = a;             // c at x = 0 is b
-    const uint8_t* ub = up ? up : cur;  // (no row above: b = a, read from nothing)
+    int bn = up ? up[0] : 0;   // b of the next sample, loaded a sample ahead
+    int cp = bn;               // c: b of the previous sample (at x = 0, b itself)
 #pragma unroll 1
     while (x < w) {
-      const int bu = ub[x];
-      const int b = up ? bu : a;
-      const int c = (up && x > 0) ? cprev : b;
-      if (!forced && a == b && b == c) {
-        int run = 0;
-        for (;;) {
-          const int chunk = br.rice(krun);
-          rice_update(Ar, Nr, chunk);
-          krun = select_k_dec(Ar, Nr);
-          run += chunk;
-          if (chunk < 255) break;
-          if (run > w) break;  // corrupt either way; bounded
-        }
-        if (x + run > w) return br.past_end() ? kDecTruncated : kDecCorrupt;
-        for (int i = 0; i < run; i++) {
-          cur[x + i] = (uint8_t)a;
-          grow[x + i] = (uint8_t)a;
-        }
-        x += run;
-        if (x < w) forced = true;
-        if (up && x > 0) cprev = up[x - 1];
-        continue;
-      }
+      const int b = up ? bn : a;
+      const int c = up ? cp : a;
+      if (up) bn = up[x + 1];  // (the row buffers have a spare byte)
+      const bool runm = !forced && a == b && b == c;
       const int mx = max(a, b), mn = min(a, b);
       const int pred = c >= mx ? mn : (c <= mn ? mx : a + b - c);
       const int gg = abs(a - c) + abs(c - b);
-      const int ctx = gg == 0 ? 0 : (gg <= 2 ? 1 : (gg <= 8 ? 2 : 3));
-      unsigned st = sst[ctx];
+      const int ctx = (gg > 0 ? 1 : 0) + (gg > 2 ? 1 : 0) + (gg > 8 ? 1 : 0);  // _activity_ctx
       const int k = (int)((kp >> (4 * ctx)) & 15u);
       const uint32_t t = br.top();
       const int q = __clz(~t);
       const int len = q + 1 + k;
-      int u;
-      if (q < kRiceEscapeQ && len <= 32) {
-        u = (q << k) | (int)((t >> (32 - len)) & ((1u << k) - 1u));
-        br.consume(len);
-      } else {
-        u = br.rice_slow(q, k);
+      if (!runm) {
+        unsigned st = sst[ctx];
+        int u;
+        if (q < kRiceEscapeQ && len <= 32) {
+          u = (q << k) | (int)((t >> (32 - len)) & ((1u << k) - 1u));
+          br.consume(len);
+        } else {
+          u = br.rice_slow(q, k);
+        }
+        const int v = (pred + unzig32(u)) & 255;
+        cur[x] = (uint8_t)v;
+        grow[x] = (uint8_t)v;
+        {  // _update_state: A += u, N += 1; at N = 64 both halve
+          const unsigned n = st >> 26;
+          const unsigned A = (st & 0x3FFFFFFu) + (unsigned)u;
+          st = n == kStateReset - 1 ? (A >> 1) | ((unsigned)(kStateReset / 2) << 26) : A | ((n + 1) << 26);
+          sst[ctx] = st;
+          const int sh = 4 * ctx;
+          kp = (kp & ~(15u << sh)) | ((uint32_t)select_k_dec((int)(st & 0x3FFFFFFu), (int)(st >> 26)) << sh);
+        }
+        cp = b;
+        a = v;
+        x++;
+        forced = false;
+        continue;
       }
-      const int v = (pred + unzig32(u)) & 255;
-      cur[x] = (uint8_t)v;
-      grow[x] = (uint8_t)v;
-      {  // _update_state: A += u, N += 1; at N = 64 both halve
-        const unsigned n = st >> 26;
-        const unsigned A = (st & 0x3FFFFFFu) + (unsigned)u;
-        st = n == kStateReset - 1 ? (A >> 1) | ((unsigned)(kStateReset / 2) << 26) : A | ((n + 1) << 26);
-        sst[ctx] = st;
-        const int sh = 4 * ctx;
-        kp = (kp & ~(15u << sh)) | ((uint32_t)select_k_dec((int)(st & 0x3FFFFFFu), (int)(st >> 26)) << sh);
+      int run = 0;
+      for (;;) {
+        const int chunk = br.rice(krun);
+        rice_update(Ar, Nr, chunk);
+        krun = select_k_dec(Ar, Nr);
+        run += chunk;
+        if (chunk < 255) break;
+        if (run > w) break;  // corrupt either way; bounded
       }
-      cprev = bu;
-      a = v;
-      x++;
-      forced = false;
+      if (x + run > w) return br.past_end() ? kDecTruncated : kDecCorrupt;
+      for (int i = 0; i < run; i++) {
+        cur[x + i] = (uint8_t)a;
+        grow[x + i] = (uint8_t)a;
+      }
+      x += run;
+      if (x < w) forced = true;
+      if (up) {  // the look-ahead already moved past x (a run may be empty)
+        cp = up[x > 0 ? x - 1 : 0];
+        bn = up[x];
+      }
     }
     if (br.past_end()) return kDecTruncated;
     up = cur;
@@ -328,7 +338,7 @@ __global__ void __launch_bounds__(160) k_decode_coders(const ImgDesc* __restrict
   if (t == 0) st = decode_dct_image(d);
   else if (with_planes) {
     __shared__ unsigned dec_state[4][4];
-    st = decode_plane_dev(d, t, dec_rows + (long long)(t - 1) * 2 * ((max_w + 3) & ~3), dec_state[t - 1]);
+    st = decode_plane_dev(d, t, dec_rows + (long long)(t - 1) * 2 * dec_row_stride(max_w), dec_state[t - 1]);
   }
   if (st) atomicOr(d.status, 1u << (kDecBadShift + t));
 }
@@ -377,7 +387,7 @@ __global__ void __launch_bounds__(256) k_decode_output(const ImgDesc* __restrict
 }
 
 void launch_decode_coders(const ImgDesc* d_descs, int nimg, bool planes, int max_w, cudaStream_t st) {
-  const size_t smem = planes ? (size_t)8 * ((max_w + 3) & ~3) : 0;
+  const size_t smem = planes ? (size_t)8 * dec_row_stride(max_w) : 0;
   cudaFuncSetAttribute(k_decode_coders, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_decode_coders<<<nimg, planes ? 160 : 32, smem, st>>>(d_descs, planes ? 1 : 0, max_w);
 }
