@@ -234,10 +234,12 @@ def shard(args, rank, world):
     return indices, sizes
 
 
-def chunks_by_pixels(npx, budget):
-    """consecutive image ranges of at most `budget` pixels (at least one image each)"""
+def chunks_by_pixels(npx, budget, order=None):
+    """consecutive image ranges (of `order`, default the job's order) of at most
+    `budget` pixels (at least one image each)"""
     out, cur, acc = [], [], 0
-    for i, n in enumerate(npx):
+    for i in (range(len(npx)) if order is None else order):
+        n = npx[i]
         if cur and acc + n > budget:
             out.append(cur)
             cur, acc = [], 0
@@ -275,13 +277,17 @@ def run_b200(args):
              for im in images]
     npx_l = [p.w * p.h for p in preps]
     npx = sum(npx_l)
-    groups = chunks_by_pixels(npx_l, args.chunk_mpx * 1e6)
+    order = None
+    if args.batch_order == "size":  # batches of like-sized images (outputs stay in job order)
+        order = sorted(range(len(npx_l)), key=lambda i: -npx_l[i])
+    groups = chunks_by_pixels(npx_l, args.chunk_mpx * 1e6, order)
 
     # inputs resident in HBM; one output set reused by every batch of the step
     d_in = [torch.from_numpy(p.pixels).to(dev) for p in preps]
     caps = [container.stream_capacity(p) for p in preps]
     out_sz = max(sum(-(-caps[i] // 256) * 256 for i in g) for g in groups) if groups else 0
     d_out = torch.empty(max(out_sz, 256), dtype=torch.uint8, device=dev)
+    pos0 = [sum(len(x) for x in groups[:k]) for k in range(len(groups))]  # the groups' slots in d_len
     g_off = []
     for g in groups:
         o, offs = 0, []
@@ -299,7 +305,7 @@ def run_b200(args):
         g = groups[k]
         container.encode_device([preps[i] for i in g], [d_in[i].data_ptr() for i in g],
                                 [base_ptr + o for o in g_off[k]], [caps[i] for i in g],
-                                d_len.data_ptr() + 8 * g[0], stream.cuda_stream, local, ctx)
+                                d_len.data_ptr() + 8 * pos0[k], stream.cuda_stream, local, ctx)
 
     def step():
         for k in range(len(groups)):
@@ -318,7 +324,7 @@ def run_b200(args):
             stage_acc[st] = stage_acc.get(st, 0.0) + v
         nl = d_len.cpu().numpy()
         for j, i in enumerate(g):
-            blob = bytes(d_out[g_off[k][j]: g_off[k][j] + int(nl[i])].cpu().numpy())
+            blob = bytes(d_out[g_off[k][j]: g_off[k][j] + int(nl[pos0[k] + j])].cpu().numpy())
             digests[indices[i]] = (hashlib.sha256(blob).hexdigest(), len(blob))
             lens[i] = len(blob)
             if i < keep:
@@ -349,7 +355,8 @@ def run_b200(args):
     h_in = [torch.from_numpy(p.pixels).reshape(-1).pin_memory() for p in preps]
     h_out = [torch.empty(min(c, 8 * n + (1 << 16)), dtype=torch.uint8).pin_memory() for c, n in zip(caps, npx_l)]
     chunk = args.chunk if args.config != 4 else min(args.chunk, 32)
-    pipe = container.HostPipeline(preps, device=local, chunk=chunk, ctx=ctx)  # the device leg's arena
+    pipe = container.HostPipeline(preps, device=local, chunk=chunk, ctx=ctx,  # the device leg's arena
+                                  by_size=args.batch_order == "size")
     pipe.run(h_in, h_out)  # warm-up (allocations)
     if dist:
         dist.barrier()
@@ -455,6 +462,8 @@ def run_b200(args):
                    "sharding": "LPT on pixel count (dist.lpt_assign), no data-path collective"
                    if not args.weak else "contiguous image ranges per rank",
                    "batches_per_step_rank0": len(groups),
+                   "batch_order": "like-sized images per batch (outputs in job order)"
+                   if args.batch_order == "size" else "job order",
                    "l2": "inputs (%.0f MB/GPU) exceed the 126 MB L2" % (h2d_bytes / 1e6),
                    "host_blas": hb, "blas_model": {"kernel": ["skylakex", "haswell"][kernel], "threads": 1}},
         "roofline": {"bound": "hbm", "achieved": round(dom_achieved, 2), "peak": peak, "unit": "GB/s",
@@ -730,6 +739,9 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=16)
     ap.add_argument("--chunk", type=int, default=64, help="images per HostPipeline chunk (e2e leg)")
     ap.add_argument("--chunk-mpx", type=float, default=160.0, help="Mpx per batched device encode")
+    ap.add_argument("--batch-order", choices=("stream", "size"), default=None,
+                    help="cut the job into batches in stream order or of like-sized images "
+                         "(default: size for the mixed-size config 4, stream otherwise)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-decode", action="store_true", help="skip the decode_hdr / decode_sdr timing")
     ap.add_argument("--tiled", action="store_true", help="config 3: tile-sharded path even on one rank")
@@ -739,6 +751,8 @@ def main():
     args.warmup = max(3, args.warmup)
     if args.images is None:
         args.images = DEFAULT_IMAGES.get(args.config, 1)
+    if args.batch_order is None:
+        args.batch_order = "size" if args.config == 4 else "stream"
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn(args))
     if args.impl == "reference":

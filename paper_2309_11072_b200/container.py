@@ -613,7 +613,7 @@ class HostPipeline:
     NSLOT = 4
     ALIGN = 256
 
-    def __init__(self, preps, device: int = 0, chunk: int = 8, ctx=None):
+    def __init__(self, preps, device: int = 0, chunk: int = 8, ctx=None, by_size: bool = False):
         import torch
 
         self.torch = torch
@@ -627,12 +627,18 @@ class HostPipeline:
         self.s_d2h = torch.cuda.Stream(self.dev)
         self.caps = [stream_capacity(p) for p in preps]
         n, c = len(preps), min(self.chunk, len(preps))
+        # the order images are encoded in (their streams land by index either
+        # way): by_size puts like-sized images in the same chunks, whose
+        # batched launches then carry less padding and shorter coder tails
+        # (bench config 4: 327 -> 310 ms per 1024-image stream)
+        self.order = sorted(range(n), key=lambda i: -preps[i].w * preps[i].h) if by_size else list(range(n))
         al = lambda v: (v + self.ALIGN - 1) // self.ALIGN * self.ALIGN
         # a slot holds any `chunk` consecutive images of the cyclic sequence
         ins = [al(p.pixels.nbytes) for p in preps]
         outs = [al(cp) for cp in self.caps]
-        in_mx = max(sum(ins[(i + k) % n] for k in range(c)) for i in range(n))
-        out_mx = max(sum(outs[(i + k) % n] for k in range(c)) for i in range(n))
+        od = self.order
+        in_mx = max(sum(ins[od[(i + k) % n]] for k in range(c)) for i in range(n))
+        out_mx = max(sum(outs[od[(i + k) % n]] for k in range(c)) for i in range(n))
         ns = self.NSLOT
         self.d_in = [torch.empty(in_mx, dtype=torch.uint8, device=self.dev) for _ in range(ns)]
         self.d_out = [torch.empty(out_mx, dtype=torch.uint8, device=self.dev) for _ in range(ns)]
@@ -649,7 +655,7 @@ class HostPipeline:
         only the smallest chunks' upload and download are exposed, and each
         chunk's encode outlasts the next one's upload (measured against
         half-size ends and against a gentler x1.5 ramp: e2e +1.7 %)."""
-        seq = list(range(len(self.preps))) * max(1, repeats)
+        seq = list(self.order) * max(1, repeats)
         c = min(self.chunk, len(self.preps))
         n = len(seq)
         if n <= c:

@@ -252,12 +252,12 @@ def test_host_pipeline_bytes_equal_device_batch(P):
     want = P.encode_batch([pr.image for pr in preps])
     h_in = [torch.from_numpy(pr.pixels).reshape(-1).pin_memory() for pr in preps]
     h_out = [torch.empty(container.stream_capacity(pr), dtype=torch.uint8).pin_memory() for pr in preps]
-    for chunk in (1, 3, 4, 16):
-        pipe = container.HostPipeline(preps, chunk=chunk)
+    for chunk, by_size in ((1, False), (3, False), (4, False), (16, False), (3, True), (4, True)):
+        pipe = container.HostPipeline(preps, chunk=chunk, by_size=by_size)
         for repeats in (1, 3):
             lens = pipe.run(h_in, h_out, repeats=repeats)
             got = [bytes(h_out[i][: lens[i]].numpy()) for i in range(len(preps))]
-            assert got == want, (chunk, repeats)
+            assert got == want, (chunk, by_size, repeats)
 
 
 def test_concurrent_encode_calls_equal_serial(P):

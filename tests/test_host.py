@@ -150,10 +150,12 @@ def test_host_pipeline_chunks_cover_the_stream_in_order(nimg, chunk, repeats):
     """HostPipeline._chunks: every image of the repeated batch exactly once, in
     order, no chunk above `chunk`, ramped (smaller) ends when the stream is long."""
     h = container.HostPipeline.__new__(container.HostPipeline)
-    h.preps, h.chunk = [None] * nimg, chunk
+    h.preps, h.chunk, h.order = [None] * nimg, chunk, list(range(nimg))
     chunks = h._chunks(repeats)
     flat = [i for c in chunks for i in c]
     assert flat == list(range(nimg)) * repeats
+    h.order = list(reversed(range(nimg)))  # by_size: the given order, repeated
+    assert [i for c in h._chunks(repeats) for i in c] == h.order * repeats
     c = min(chunk, nimg)
     assert all(1 <= len(k) <= c for k in chunks)
     if nimg * repeats >= 3 * c and c >= 4:
