@@ -75,7 +75,10 @@ void hdll_b200_ctx_destroy(hdll_b200_ctx *ctx);
 uint64_t hdll_b200_stream_capacity(uint32_t width, uint32_t height, uint32_t hdr_pre_len, uint32_t hdr_post_len);
 
 /* Batched encode, everything resident on the device.  d_out[i] receives image
- * i's stream (capacity out_cap[i] bytes), d_out_len[i] (device) its length.
+ * i's stream (capacity out_cap[i] bytes), d_out_len[i] its length, written
+ * by a kernel: device memory, or pinned host memory (mapped under unified
+ * addressing), which then holds the lengths once `stream` has reached the end
+ * of the batch, without a device-to-host copy.
  * Asynchronous on `stream`; hdll_b200_sync() reports device-side errors. */
 int hdll_b200_encode_batch_device(hdll_b200_ctx *ctx, const hdll_b200_image *imgs, int n, uint8_t *const *d_out,
                                   const uint64_t *out_cap, uint64_t *d_out_len, void *stream);

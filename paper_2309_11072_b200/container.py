@@ -606,8 +606,9 @@ class HostPipeline:
     ramp up at the start and down at the end (`_chunks`): the pipeline waits
     for the first chunk's upload and for the last chunk's download with
     nothing to overlap them, and PCIe (55 GB/s per direction) outruns the
-    encoder, so each chunk still uploads the next, twice as large, in time.  Inputs are pinned host tensors;
-    streams land in pinned host buffers.  This is the `e2e` path of bench.py.
+    encoder, so each chunk uploads the next, larger one in time.  Inputs are
+    pinned host tensors; streams and their lengths land in pinned host
+    buffers.  This is the `e2e` path of bench.py.
     """
 
     NSLOT = 4
@@ -642,8 +643,7 @@ class HostPipeline:
         ns = self.NSLOT
         self.d_in = [torch.empty(in_mx, dtype=torch.uint8, device=self.dev) for _ in range(ns)]
         self.d_out = [torch.empty(out_mx, dtype=torch.uint8, device=self.dev) for _ in range(ns)]
-        self.d_len = [torch.zeros(c, dtype=torch.int64, device=self.dev) for _ in range(ns)]
-        self.h_len = [torch.zeros(c, dtype=torch.int64).pin_memory() for _ in range(ns)]
+        self.h_len = [torch.zeros(c, dtype=torch.int64).pin_memory() for _ in range(ns)]  # device-mapped (UVA)
         self._ins, self._outs = ins, outs
         self.slot_free = [torch.cuda.Event() for _ in range(ns)]
         self.timeline = None
@@ -651,18 +651,24 @@ class HostPipeline:
             e.record(torch.cuda.current_stream(self.dev))
 
     def _chunks(self, repeats: int):
-        """Chunk sizes c/4, c/2, then c, and back down to c/2, c/4 at the end:
-        only the smallest chunks' upload and download are exposed, and each
-        chunk's encode outlasts the next one's upload (measured against
-        half-size ends and against a gentler x1.5 ramp: e2e +1.7 %)."""
+        """Chunk sizes c/4, c/2, 3c/4, then c, and back down at the end: only
+        the smallest chunks' upload and download are exposed, and each chunk's
+        encode outlasts the next one's upload, so the encode never waits for
+        its input while the previous chunk's download is in flight (a batch's
+        first kernel reads its pinned descriptor block over PCIe, and those
+        reads queue behind the download's writes).  Config 1, 10 steps: c/4,
+        c/2 ramp 18.46 ms per step, c/8 .. c/2 18.1, c/4 .. 3c/4 17.76
+        (tools/pipe_timeline.py)."""
         seq = list(self.order) * max(1, repeats)
         c = min(self.chunk, len(self.preps))
         n = len(seq)
         if n <= c:
             return [seq]
-        up = [k for k in (c // 4, c // 2) if k >= 1]
-        if 2 * sum(up) + c > n:
-            up = [c // 2] if c >= 2 else []
+        up = [k for k in (c // 4, c // 2, 3 * c // 4) if k >= 1]
+        if os.environ.get("HDLL_PIPE_RAMP"):  # experiment: ramp fractions of c, e.g. "0.25,0.375,0.625"
+            up = [k for k in (int(c * float(f)) for f in os.environ["HDLL_PIPE_RAMP"].split(",")) if k >= 1]
+        while up and 2 * sum(up) + c > n:  # short streams: a shorter ramp
+            up.pop()
         down = list(reversed(up))
         sizes = list(up)
         left = n - 2 * sum(up)
@@ -732,11 +738,12 @@ class HostPipeline:
             mark("enc_start", ci, self.s_comp)
             oi, oo = layouts[ci]
             bi, bo = self.d_in[s].data_ptr(), self.d_out[s].data_ptr()
+            # the stream lengths land straight in pinned host memory (the
+            # assembly kernel's stores, over the mapped pointer): a copy would
+            # queue on the copy engine behind the previous chunk's download
             encode_device([self.preps[i] for i in idx], [bi + o for o in oi], [bo + o for o in oo],
-                          [self.caps[i] for i in idx], self.d_len[s].data_ptr(), self.s_comp.cuda_stream,
+                          [self.caps[i] for i in idx], self.h_len[s].data_ptr(), self.s_comp.cuda_stream,
                           self.device, self.ctx)
-            with torch.cuda.stream(self.s_comp):
-                self.h_len[s][: len(idx)].copy_(self.d_len[s][: len(idx)], non_blocking=True)
             mark("enc_end", ci, self.s_comp)
             done = torch.cuda.Event()
             done.record(self.s_comp)
