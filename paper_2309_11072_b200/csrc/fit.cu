@@ -99,6 +99,8 @@ __global__ void __launch_bounds__(256) k_sort_scan(const ImgDesc* __restrict__ d
 // shared memory in bin order, then written out so that consecutive threads
 // store consecutive positions of a bin (coalesced).
 struct ScatterSmem {
+  double xw[3][kSortTile];  // the tile's S* window (full, aligned tiles: one bulk copy per channel)
+  uint64_t bar;
   unsigned wcnt[8][256];
   unsigned loc_off[257];
   unsigned g_off[256];
@@ -133,6 +135,22 @@ __global__ void __launch_bounds__(256) k_sort_scatter(const ImgDesc* __restrict_
       }
     }
     return;
+  }
+  // A full tile's S* window (3 x 8 KB) comes in by bulk copies issued first,
+  // so the DRAM stream overlaps the ranking below and the placement gathers
+  // read shared memory instead of scattered global words.
+  const double* xg[3];
+#pragma unroll
+  for (int c = 0; c < 3; c++) xg[c] = d.sstar + (long long)c * d.n + pb + t0;
+  const bool bulk = tn == kSortTile && real &&
+                    ((reinterpret_cast<uintptr_t>(xg[0]) | reinterpret_cast<uintptr_t>(xg[1]) |
+                      reinterpret_cast<uintptr_t>(xg[2])) & 15) == 0;
+  if (bulk && threadIdx.x == 0) {
+    mbar_init(&sm.bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&sm.bar, 3 * kSortTile * sizeof(double));
+#pragma unroll
+    for (int c = 0; c < 3; c++) bulk_g2s(&sm.xw[c][0], xg[c], kSortTile * sizeof(double), &sm.bar);
   }
   constexpr int kPerWarp = kSortTile / 8;
   constexpr int kSteps = kPerWarp / 32;
@@ -210,11 +228,21 @@ __global__ void __launch_bounds__(256) k_sort_scatter(const ImgDesc* __restrict_
   if (tn == kSortTile && real) {  // full tile: every gather in flight before the stores
     constexpr int kR = kSortTile / 256;
     double xv[kR][3];
+    if (bulk) {
+      mbar_wait(&sm.bar, 0);
 #pragma unroll
-    for (int r = 0; r < kR; r++) {
-      const long long p = t0 + sm.src[threadIdx.x + 256 * r];
+      for (int r = 0; r < kR; r++) {
+        const int q = sm.src[threadIdx.x + 256 * r];
 #pragma unroll
-      for (int c = 0; c < 3; c++) xv[r][c] = d.sstar[(long long)c * d.n + pb + p];
+        for (int c = 0; c < 3; c++) xv[r][c] = sm.xw[c][q];
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < kR; r++) {
+        const long long p = t0 + sm.src[threadIdx.x + 256 * r];
+#pragma unroll
+        for (int c = 0; c < 3; c++) xv[r][c] = d.sstar[(long long)c * d.n + pb + p];
+      }
     }
 #pragma unroll
     for (int r = 0; r < kR; r++) {
