@@ -324,24 +324,34 @@ __global__ void __launch_bounds__(kSegs) k_seg_setup(const ImgDesc* __restrict__
 }
 
 // one warp per depth-L node of a segment's pairwise tree
+// one warp per run of kNodesPerWarp consecutive depth-L nodes (of every
+// segment in turn): the node -> segment lookup is one warp-parallel search
+// per run, then a forward walk
+constexpr int kNodesPerWarp = 8;
+
 __global__ void __launch_bounds__(128) k_seg_nodes(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
   if (!d.slrme || d.int_fit) return;
   __shared__ PwScratch pw[4];
-  const int warp = threadIdx.x >> 5;
-  const long long g = (long long)blockIdx.x * 4 + warp;
-  if (g >= d.seg_node_off[kSegs]) return;
-  int lo = 0, hi = kSegs;  // find s with off[s] <= g < off[s+1]
-  while (hi - lo > 1) {
-    int mid = (lo + hi) >> 1;
-    if (d.seg_node_off[mid] <= g) lo = mid; else hi = mid;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long g0 = ((long long)blockIdx.x * 4 + warp) * kNodesPerWarp;
+  const long long gend = d.seg_node_off[kSegs];
+  if (g0 >= gend) return;
+  // s with off[s] <= g0 < off[s+1]: the last of 32 strided probes, then the
+  // last of the 24 entries after it (kSegs = 32 x 24)
+  constexpr int kStride = kSegs / 32;
+  const unsigned b1 = __ballot_sync(0xffffffffu, d.seg_node_off[lane * kStride] <= g0);
+  const int base = (31 - __clz(b1)) * kStride;
+  const unsigned b2 = __ballot_sync(0xffffffffu, lane < kStride && d.seg_node_off[base + lane] <= g0);
+  int s = base + 31 - __clz(b2);
+  for (long long g = g0; g < min(g0 + kNodesPerWarp, gend); g++) {
+    while (d.seg_node_off[s + 1] <= g) s++;  // (segments without nodes are passed over)
+    SegView v = seg_view(d, s);
+    long long off, sz;
+    pairwise_node(v.n, d.seg_level[s], g - d.seg_node_off[s], &off, &sz);
+    const double r = warp_pairwise(x_acc(d, s >> 8, v), off, sz, pw[warp]);
+    if (lane == 0) d.seg_nodes[g] = r;
   }
-  const int s = lo;
-  SegView v = seg_view(d, s);
-  long long off, sz;
-  pairwise_node(v.n, d.seg_level[s], g - d.seg_node_off[s], &off, &sz);
-  const double r = warp_pairwise(x_acc(d, s >> 8, v), off, sz, pw[warp]);
-  if ((threadIdx.x & 31) == 0) d.seg_nodes[g] = r;
 }
 
 // ---------------------------------------------------------------------------
@@ -853,7 +863,7 @@ void launch_fit_sort(const ImgDesc* d_descs, int nimg, int max_sort_tiles, cudaS
 
 void launch_fit_bins(const ImgDesc* d_descs, int nimg, long long max_nodes, int max_chunks, cudaStream_t st) {
   k_seg_setup<<<nimg, kSegs, 0, st>>>(d_descs);
-  k_seg_nodes<<<dim3((unsigned)((max_nodes + 3) / 4), nimg), 128, 0, st>>>(d_descs);
+  k_seg_nodes<<<dim3((unsigned)((max_nodes + 4 * kNodesPerWarp - 1) / (4 * kNodesPerWarp)), nimg), 128, 0, st>>>(d_descs);
   cudaFuncSetAttribute(k_seg_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DotSmem));
   k_seg_dot<<<dim3(kSegs, nimg, max_chunks), 32, sizeof(DotSmem), st>>>(d_descs);
   k_seg_reduce_coef<<<dim3(kSegs, nimg), 256, 0, st>>>(d_descs);

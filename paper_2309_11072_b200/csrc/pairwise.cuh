@@ -119,7 +119,10 @@ static inline void upload_pw_table() {
   cudaMemcpyToSymbol(c_pw_leaves, cnt, sizeof(cnt));
 }
 
-template <class Acc>
+// kTailLanes: a leaf's sequential tail is loaded by the lanes of its group
+// together (cheap accessors: k_seg_nodes); otherwise lane 0 of the group
+// reads it element by element (the tone map's accessor computes a log per read)
+template <class Acc, bool kTailLanes = true>
 __device__ double warp_pairwise(const Acc& a, long long off, long long n, PwScratch& sc) {
   const uint8_t* leaves_of = c_pw_leaves;
   const int lane = threadIdx.x & 31, grp = lane >> 3, j = lane & 7;
@@ -153,6 +156,12 @@ __device__ double warp_pairwise(const Acc& a, long long off, long long n, PwScra
     const long long lo = mine ? sc.lo[li] : 0, ln = mine ? (sc.ln[li] & 0xFFFF) : 0;
     const long long lim = ln - (ln % 8);
     double r = 0.0;
+    // the sequential part (the tail past the last multiple of 8, or a whole
+    // leaf under 8 samples): one element per lane of the group, loaded with
+    // the rest instead of one dependent load per addition
+    const long long tb = ln < 8 ? 0 : lim, tcnt = ln - tb;  // 0..7 elements
+    double tv = 0.0;
+    if (kTailLanes && mine && j < tcnt) tv = a(lo + tb + j);
     if (mine && ln >= 8) {
       // a leaf holds <= 128 samples: issue all 16 loads of the lane before the adds
       double v[16];
@@ -166,17 +175,17 @@ __device__ double warp_pairwise(const Acc& a, long long off, long long n, PwScra
     const double p2 = r + __shfl_down_sync(0xffffffffu, r, 1);    // r0+r1, r2+r3, ...
     const double q4 = p2 + __shfl_down_sync(0xffffffffu, p2, 2);  // (r0+r1)+(r2+r3), ...
     const double s8 = q4 + __shfl_down_sync(0xffffffffu, q4, 4);  // ((..)+(..))+((..)+(..))
-    if (mine && j == 0) {
-      double res;
-      if (ln < 8) {
-        res = 0.0;
-        for (long long i = 0; i < ln; i++) res += a(lo + i);
-      } else {
-        res = s8;
-        for (long long i = lim; i < ln; i++) res += a(lo + i);
+    double res = ln < 8 ? 0.0 : s8;
+    if constexpr (kTailLanes) {
+#pragma unroll
+      for (int t = 0; t < 7; t++) {  // numpy's sequential tail, in order
+        const double x = __shfl_sync(0xffffffffu, tv, (lane & ~7) + t);
+        if (t < tcnt) res += x;
       }
-      sc.leaf[li] = res;
+    } else if (mine && j == 0) {
+      for (long long i = tb; i < ln; i++) res += a(lo + i);
     }
+    if (mine && j == 0) sc.leaf[li] = res;
   }
   __syncwarp();
   double out = 0.0;

@@ -63,8 +63,8 @@ __global__ void __launch_bounds__(128) k_tm_nodes(const ImgDesc* __restrict__ de
   if (idx < d.node1) {
     long long off, sz;
     pairwise_node(d.full_n, d.tm_level, idx, &off, &sz);
-    const double r = warp_pairwise(LogLwAcc{reinterpret_cast<const uint32_t*>(d.rgbe), d.pix_base, d.epsilon, &mx}, off,
-                                   sz, pw[warp]);
+    const double r = warp_pairwise<LogLwAcc, false>(
+        LogLwAcc{reinterpret_cast<const uint32_t*>(d.rgbe), d.pix_base, d.epsilon, &mx}, off, sz, pw[warp]);
     if ((threadIdx.x & 31) == 0) d.tm_nodes[idx] = r;
   }
   // block max -> one atomic (Lw >= 0 so the bit pattern orders like the value)
