@@ -37,14 +37,13 @@ def _unframe(payload: bytes, spec_id: int, what: str):
         raise UnknownCoderError(f"payload coded with id {coder_id}, spec says {spec_id}")
     if coder_id != 1:
         raise UnknownCoderError(f"{what} coder id {coder_id} is not available on the B200 path")
-    body = payload[9:]
     kind = "image" if what == "lossy" else "plane"
-    if len(body) < 8:
+    if len(payload) - 9 < 8:
         raise CorruptPayloadError(f"{kind} body shorter than its dimensions")
-    w, h = struct.unpack_from("<II", body, 0)
+    w, h = struct.unpack_from("<II", payload, 9)
     if w == 0 or h == 0:
         raise CorruptPayloadError(f"zero {kind} dimension")
-    return crc, w, h, body[8:]
+    return crc, w, h, 17  # the coder bits start 17 bytes in: referenced in place, not copied
 
 
 class _Job:
@@ -53,21 +52,22 @@ class _Job:
     def __init__(self, stream: DualLayerStream, sdr_only: bool):
         self.stream, self.sdr_only = stream, sdr_only
         self.errors = [None] * 5
-        self.bodies = [b""] * 5
+        self.bodies = [b""] * 5  # (payload, offset of its coder bits)
+        self.offs = [0] * 5
         self.crcs = [0] * 5
         w = h = None
         pays = [stream.base_payload] if sdr_only else [stream.base_payload, stream.e_payload, *stream.residual_payloads]
         for k, pay in enumerate(pays):
             try:
-                crc, pw, ph, bits = _unframe(pay, stream.lossy_spec.coder_id if k == 0 else stream.lossless_spec.coder_id,
-                                             "lossy" if k == 0 else "lossless")
+                crc, pw, ph, off = _unframe(pay, stream.lossy_spec.coder_id if k == 0 else stream.lossless_spec.coder_id,
+                                            "lossy" if k == 0 else "lossless")
                 if k == 0:
                     w, h = pw, ph
                     if not sdr_only and (pw, ph) != (stream.width, stream.height):
                         raise StreamError("base layer does not match the stream dimensions")
                 elif (pw, ph) != (stream.width, stream.height):
                     raise StreamError(("exponent" if k == 1 else "residual") + " plane does not match the stream dimensions")
-                self.crcs[k], self.bodies[k] = crc, bits
+                self.crcs[k], self.bodies[k], self.offs[k] = crc, bytes(pay), off
             except (CorruptPayloadError, UnknownCoderError, StreamError) as e:
                 self.errors[k] = e
         self.w = w if w is not None else stream.width
@@ -98,9 +98,10 @@ class _Job:
         im.a32 = self.a32.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
         im.b32 = self.b32.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
         for k in range(5):
-            body = self.bodies[k]
-            im.body[k] = ctypes.cast(ctypes.c_char_p(body), ctypes.c_void_p) if body else None
-            im.body_len[k] = len(body)
+            pay, off = self.bodies[k], self.offs[k]
+            n = max(len(pay) - off, 0)
+            im.body[k] = (ctypes.cast(ctypes.c_char_p(pay), ctypes.c_void_p).value + off) if n else None
+            im.body_len[k] = n
             im.crc[k] = self.crcs[k]
         return im
 
