@@ -64,12 +64,23 @@ def generate(cfg: int, indices, scale: float = 1.0, workers: int | None = None):
 
 
 def _oracle_encode(args):
-    px, sigma, kernel = args
+    px, sigma, kernel, threads = args
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     from oracle import hdll_oracle as O
     t = time.perf_counter()
-    blob = O.encode(px, sigma=sigma, header_vars=[("FORMAT", "32-bit_rle_rgbe")], blas_kernel=kernel, blas_threads=1)
+    blob = O.encode(px, sigma=sigma, header_vars=[("FORMAT", "32-bit_rle_rgbe")], blas_kernel=kernel,
+                    blas_threads=threads)
     return blob, time.perf_counter() - t
+
+
+def blas_params(args, hb):
+    """The parity model of the reference's np.dot on this host (SURVEY.md App.
+    A.5): the detected OpenBLAS kernel (SKYLAKEX when the core type is not
+    modelled) and thread count, which fixes the level-1 split of large bins;
+    --blas-threads overrides the count."""
+    kernel = hb["kernel"] if hb["kernel"] is not None else 0
+    threads = args.blas_threads if args.blas_threads else (hb["threads"] or 1)
+    return kernel, max(1, min(int(threads), 64))
 
 
 class ClockSampler:
@@ -197,9 +208,12 @@ def compute_ceilings(stage_ms: dict):
     return {"stages": out, "source": "profiles/ceilings.json", "peaks": d.get("peaks")}
 
 
-def golden_digests(config: int, sigma: float):
-    """{index: (sha256, len)} of the reference's own streams (tests/golden/config_golden.json)."""
-    if not GOLDEN.exists():
+def golden_digests(config: int, sigma: float, threads: int = 1):
+    """{index: (sha256, len)} of the reference's own streams with OpenBLAS at
+    `threads` threads (tests/golden/config_golden.json, config_golden_tT.json;
+    a sigma = 0 stream does not depend on the thread count)."""
+    path = GOLDEN if threads == 1 or sigma == 0.0 else GOLDEN.with_name(f"config_golden_t{threads}.json")
+    if not path.exists():
         return {}
     name = {1: "c1", 2: "c2", 21: "c2b", 3: "c3", 4: "c4"}.get(config)
     if name is None:
@@ -208,7 +222,7 @@ def golden_digests(config: int, sigma: float):
         name += ".s0"
     elif sigma != 1.0:
         return {}
-    return {c["index"]: (c["stream_sha256"], c["stream_len"]) for c in json.loads(GOLDEN.read_text())["cases"]
+    return {c["index"]: (c["stream_sha256"], c["stream_len"]) for c in json.loads(path.read_text())["cases"]
             if c["name"] == name}
 
 
@@ -270,10 +284,10 @@ def run_b200(args):
         dist.init_process_group("nccl", device_id=dev)
 
     hb = container.host_blas()
-    kernel = hb["kernel"] if hb["kernel"] is not None else 0
+    kernel, threads = blas_params(args, hb)
     nimg = len(indices)
     images = [P.RadianceImage(p.shape[1], p.shape[0], p, [("FORMAT", "32-bit_rle_rgbe")]) for p in pix]
-    preps = [container.prepare(im, quality=args.quality, sigma=args.sigma, blas_kernel=kernel, blas_threads=1)
+    preps = [container.prepare(im, quality=args.quality, sigma=args.sigma, blas_kernel=kernel, blas_threads=threads)
              for im in images]
     npx_l = [p.w * p.h for p in preps]
     npx = sum(npx_l)
@@ -388,8 +402,8 @@ def run_b200(args):
         total_px, total_out, total_h2d = float(npx), float(out_bytes), float(h2d_bytes)
     ms, e2e_ms = float(vals[0]), float(vals[1])
 
-    # ---- parity: reference digests (SKYLAKEX, 1 thread) and the oracle on this host ----
-    ref = golden_digests(args.config, args.sigma) if args.scale == 1.0 else {}
+    # ---- parity: reference digests (SKYLAKEX, this thread count) and the oracle on this host ----
+    ref = golden_digests(args.config, args.sigma, threads) if args.scale == 1.0 else {}
     par_ref = None
     if ref and kernel != 0:
         par_ref = {"checked": 0, "note": "the reference digests were made with OpenBLAS SKYLAKEX; this host's "
@@ -407,13 +421,13 @@ def run_b200(args):
         cores = min(sample, os.cpu_count() or 1)
         t0 = time.perf_counter()
         with ProcessPoolExecutor(cores) as ex:
-            res = list(ex.map(_oracle_encode, [(p.pixels, args.sigma, kernel) for p in preps[:sample]]))
+            res = list(ex.map(_oracle_encode, [(p.pixels, args.sigma, kernel, threads) for p in preps[:sample]]))
         wall = time.perf_counter() - t0
         cpu = {"value": sum(npx_l[:sample]) / wall / 1e6, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"{sample} of the job's config-{args.config} images, one per process (oracle/ C+numpy "
                          f"port, bit-identical to the reference), wall {wall:.1f}s on {cores} worker processes"}
         par_oracle = {"checked": sample, "equal": sum(preps[i].blob == res[i][0] for i in range(sample)),
-                      "blas_kernel": kernel, "blas_threads": 1}
+                      "blas_kernel": kernel, "blas_threads": threads}
 
     if rank != 0:
         if dist:
@@ -465,7 +479,7 @@ def run_b200(args):
                    "batch_order": "like-sized images per batch (outputs in job order)"
                    if args.batch_order == "size" else "job order",
                    "l2": "inputs (%.0f MB/GPU) exceed the 126 MB L2" % (h2d_bytes / 1e6),
-                   "host_blas": hb, "blas_model": {"kernel": ["skylakex", "haswell"][kernel], "threads": 1}},
+                   "host_blas": hb, "blas_model": {"kernel": ["skylakex", "haswell"][kernel], "threads": threads}},
         "roofline": {"bound": "hbm", "achieved": round(dom_achieved, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(dom_achieved / peak, 5), "traffic": traffic, "peak_source": peak_src,
                      "kernel": f"stage {dom} (k_entropy_plane + fix-up)" if dom == "entropy_plane" else f"stage {dom}",
@@ -592,7 +606,8 @@ def run_tiled(args):
         dist.init_process_group("nccl", device_id=dev)
     h, w = pix.shape[:2]
     image = P.RadianceImage(w, h, pix, [("FORMAT", "32-bit_rle_rgbe")])
-    prep = container.prepare(image, quality=args.quality, sigma=args.sigma, blas_kernel="skylakex", blas_threads=1)
+    kernel, threads = blas_params(args, container.host_blas())
+    prep = container.prepare(image, quality=args.quality, sigma=args.sigma, blas_kernel=kernel, blas_threads=threads)
     radius = prep.params.radius if prep.sigma_milli else 0
     specs = tiled.band_plan(w, h, world, radius)
     ex = tiled.TorchExchange()
@@ -642,7 +657,7 @@ def run_tiled(args):
         return
     npx = w * h
     blob = bytes(out[0][:n_out].cpu().numpy())
-    ref = golden_digests(3, args.sigma) if args.scale == 1.0 else {}
+    ref = golden_digests(3, args.sigma, threads) if args.scale == 1.0 and kernel == 0 else {}
     par_ref = None
     if ref:
         par_ref = {"checked": 1, "equal": int((hashlib.sha256(blob).hexdigest(), len(blob)) == ref[0]),
@@ -680,7 +695,7 @@ def tiled_cpu_sample(args):
     """Oracle port on a 1920x1080 render of the config-3 scene (bounded sample)."""
     px = generate(3, [0], 0.25)[0]
     t0 = time.perf_counter()
-    _oracle_encode((px, args.sigma, 0))
+    _oracle_encode((px, args.sigma, 0, 1))
     wall = time.perf_counter() - t0
     return {"value": px.shape[0] * px.shape[1] / wall / 1e6, "unit": UNIT, "cores": 1, "kind": "port",
             "sample": f"config-3 scene at scale 0.25 ({px.shape[1]}x{px.shape[0]}), one process, wall {wall:.1f}s"}
@@ -695,15 +710,15 @@ def run_reference(args):
     pix = generate(args.config, list(range(sample)), args.scale)
     from paper_2309_11072_b200.container import host_blas
     hb = host_blas()
-    kernel = hb["kernel"] if hb["kernel"] is not None else 0
+    kernel, threads = blas_params(args, hb)
     shapes = {p.shape[:2] for p in pix}
     with ProcessPoolExecutor(sample) as ex:
-        list(ex.map(_oracle_encode, [(pix[0], args.sigma, kernel)]))  # warm the workers
+        list(ex.map(_oracle_encode, [(pix[0], args.sigma, kernel, threads)]))  # warm the workers
         for _ in range(args.warmup):
-            list(ex.map(_oracle_encode, [(p, args.sigma, kernel) for p in pix]))
+            list(ex.map(_oracle_encode, [(p, args.sigma, kernel, threads) for p in pix]))
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            list(ex.map(_oracle_encode, [(p, args.sigma, kernel) for p in pix]))
+            list(ex.map(_oracle_encode, [(p, args.sigma, kernel, threads) for p in pix]))
         wall = (time.perf_counter() - t0) / args.steps
     value = sum(p.shape[0] * p.shape[1] for p in pix) / wall / 1e6
     desc = (f"{sample} x {pix[0].shape[1]}x{pix[0].shape[0]}" if len(shapes) == 1
@@ -738,6 +753,8 @@ def main():
     ap.add_argument("--sigma", type=float, default=1.0)
     ap.add_argument("--cpu-sample", type=int, default=16)
     ap.add_argument("--chunk", type=int, default=64, help="images per HostPipeline chunk (e2e leg)")
+    ap.add_argument("--blas-threads", type=int, default=None,
+                    help="OpenBLAS thread count of the parity model (default: this host's, as threadpoolctl reports)")
     ap.add_argument("--chunk-mpx", type=float, default=160.0, help="Mpx per batched device encode")
     ap.add_argument("--batch-order", choices=("stream", "size"), default=None,
                     help="cut the job into batches in stream order or of like-sized images "

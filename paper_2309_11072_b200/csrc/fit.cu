@@ -494,7 +494,20 @@ __device__ void warp_ddot2(const XA& X, const YA& Y, long long start, long long 
 // (cp.async.bulk + mbarrier, kStages deep) and each lane's chain only waits on
 // FMA latency.  Blocks hold kBlk samples; the bulk region is [0, nmain) with
 // nmain = n32 (SKYLAKEX, 32 lanes) or n1 (HASWELL, 16 lanes).
-constexpr int kBlk = 2048, kStages = 4;
+// 2 stages of 1024 samples (18.5 KB, twelve warps per SM): measured against
+// 4 x 2048 (74 KB, three warps per SM), 4 x 1024 and 4 x 512 on config 1 at
+// the 1- and 16-thread parity models and on config 3 at 16 threads: with 16
+// OpenBLAS threads most bins of a batch split into 16 short chunks, whose
+// warps are latency-bound, so resident warps count more than depth
+// (config 1 fit 4.85 -> 3.37 ms at 16 threads, 3.04 -> 2.95 at 1; config 3
+// 0.88 -> 0.95 ms).
+#ifndef HDLL_DOT_BLK  // experiment builds: samples per staged block / pipeline depth
+#define HDLL_DOT_BLK 1024
+#endif
+#ifndef HDLL_DOT_STAGES
+#define HDLL_DOT_STAGES 2
+#endif
+constexpr int kBlk = HDLL_DOT_BLK, kStages = HDLL_DOT_STAGES;
 struct DotSmem {
   uint64_t bar[kStages];
   double x[kStages][kBlk + 2];

@@ -132,3 +132,64 @@ def test_config4_stream_matches_reference(P):
     assert len(cases) == 1024
     for k in range(0, len(cases), 64):
         _check_batch(P, cases[k:k + 64], 1.0)
+
+
+# The same configs against the reference run with OpenBLAS at 16 threads
+# (config_golden_t16.json: the level-1 split of every bin above 10,000
+# samples into 16 chunks, as numpy on a 16-thread host computes np.dot) --
+# the parity model bench.py uses on the GPU box, whose host reports 16.
+GOLDEN16 = GOLDEN.with_name("config_golden_t16.json")
+
+
+def _cases16():
+    if not GOLDEN16.exists():
+        return {}
+    out: dict = {}
+    for c in json.loads(GOLDEN16.read_text())["cases"]:
+        out.setdefault(c["name"], []).append(c)
+    return out
+
+
+CASES16 = _cases16()
+
+
+@pytest.mark.skipif("c1" not in CASES16, reason="config_golden_t16.json missing")
+def test_config1_matches_reference_16_threads(P):
+    cases = CASES16["c1"]
+    for k in range(0, len(cases), 32):
+        chunk = cases[k:k + 32]
+        pix = _generate([(c["config"], c["index"]) for c in chunk])
+        imgs = [P.RadianceImage(p.shape[1], p.shape[0], p, HV) for p in pix]
+        blobs = P.encode_batch(imgs, sigma=1.0, blas_kernel="skylakex", blas_threads=16)
+        bad = [c["index"] for c, b in zip(chunk, blobs) if _sha(b) != c["stream_sha256"]]
+        assert not bad, f"c1 images {bad[:8]} differ from the 16-thread reference"
+
+
+@pytest.mark.skipif("c3" not in CASES16, reason="config_golden_t16.json missing")
+@pytest.mark.parametrize("name", ["c2", "c2b", "c3"])
+def test_single_images_match_reference_16_threads(name, P):
+    (case,) = CASES16[name]
+    pix = _gen((case["config"], case["index"]))
+    img = P.RadianceImage(pix.shape[1], pix.shape[0], pix, HV)
+    blob = P.serialize(P.encode(img, sigma=1.0, blas_kernel="skylakex", blas_threads=16))
+    assert _sha(blob) == case["stream_sha256"]
+
+
+@pytest.mark.skipif("c3" not in CASES16, reason="config_golden_t16.json missing")
+def test_config3_tiled_matches_reference_16_threads(P, c3_image):
+    from paper_2309_11072_b200 import tiled
+    (case,) = CASES16["c3"]
+    blob = tiled.encode_tiled(c3_image, 4, sigma=1.0, blas_kernel="skylakex", blas_threads=16, return_bytes=True)
+    assert _sha(blob) == case["stream_sha256"]
+
+
+@pytest.mark.skipif("c4" not in CASES16, reason="config_golden_t16.json missing")
+def test_config4_matches_reference_16_threads(P):
+    cases = CASES16["c4"]
+    for k in range(0, len(cases), 64):
+        chunk = cases[k:k + 64]
+        pix = _generate([(c["config"], c["index"]) for c in chunk])
+        imgs = [P.RadianceImage(p.shape[1], p.shape[0], p, HV) for p in pix]
+        blobs = P.encode_batch(imgs, sigma=1.0, blas_kernel="skylakex", blas_threads=16)
+        bad = [c["index"] for c, b in zip(chunk, blobs) if _sha(b) != c["stream_sha256"]]
+        assert not bad, f"c4 images {bad[:8]} differ from the 16-thread reference"
