@@ -514,8 +514,47 @@ struct DotSmem {
   uint8_t y[kStages][kBlk + 32];
 };
 
+// In a batch (launch_fit_bins: >= 8 images) a segment of at least kParSeg
+// samples spreads its OpenBLAS chunks over several warps and a smaller one
+// streams every chunk through one warp; a launch of fewer images spreads every
+// segment's chunks (config 1 at 16 threads: fit 3.37 -> 3.26 ms; config 3
+// needs the parallel chunks: 0.93 ms against 1.35 with one warp per segment).
+constexpr long long kParSeg = 1LL << 20;
+
+// Position in OpenBLAS's level-1 split of a segment of n samples into T
+// chunks (width = ceil(rem / (T - used)), oracle/hdll_oracle.c ddot_compute):
+// chunk u's start and width, its bulk region [0, nmain) and staged blocks.
+// A warp visits chunks j0, j0 + G, j0 + 2G, ...
+struct ChunkCursor {
+  long long n, start, rem, width, nmain, nblk;
+  int T, G, u, kernel;
+  __device__ __forceinline__ void geom() {
+    width = (rem + (T - u) - 1) / (T - u);
+    if (width > rem) width = rem;
+    const long long n1 = width & ~15LL;
+    nmain = kernel == 0 ? (n1 & ~31LL) : n1;
+    nblk = (nmain + kBlk - 1) / kBlk;
+  }
+  __device__ __forceinline__ void step() {  // to chunk u + 1
+    start += width;
+    rem -= width;
+    u++;
+    if (u < T) geom();
+  }
+  __device__ __forceinline__ void init(long long nn, int TT, int j0, int GG, int kern) {
+    n = nn, T = TT, G = GG, kernel = kern;
+    start = 0, rem = n, u = 0;
+    geom();
+    for (int k = 0; k < j0 && u < T; k++) step();
+  }
+  __device__ __forceinline__ bool next() {  // to chunk u + G; false past the last
+    for (int k = 0; k < G && u < T; k++) step();
+    return u < T;
+  }
+};
+
 // grid: (kSegs, nimg, max chunks); one warp per (segment, OpenBLAS thread-chunk)
-__global__ void __launch_bounds__(32) k_seg_dot(const ImgDesc* __restrict__ descs) {
+__global__ void __launch_bounds__(32) k_seg_dot(const ImgDesc* __restrict__ descs, long long par_seg) {
   const ImgDesc& d = descs[blockIdx.y];
   if (!d.slrme || d.int_fit) return;
   const int s = blockIdx.x;
@@ -533,44 +572,50 @@ __global__ void __launch_bounds__(32) k_seg_dot(const ImgDesc* __restrict__ desc
   fence_mbar_init();
   __syncwarp();
   unsigned phase_bits = 0;  // parity of every stage's barrier, flipped at each consumed block
-  for (int j = blockIdx.z; j < T; j += gridDim.z) {
-    // chunk j of OpenBLAS's level-1 split: width = ceil(rem / (T - used))
-    long long start = 0, rem = v.n, width = 0;
-    for (int u = 0; u <= j; u++) {
-      width = (rem + (T - u) - 1) / (T - u);
-      if (width > rem) width = rem;
-      if (u < j) {
-        start += width;
-        rem -= width;
-      }
+  // A segment below kParSeg samples is one warp's: it streams all its chunks
+  // in turn through one continuous pipeline (the producer runs ahead across
+  // chunk boundaries).  A larger one spreads its chunks over the grid's z.
+  const int G = v.n >= par_seg ? (int)gridDim.z : 1;
+  if ((int)blockIdx.z >= G || (int)blockIdx.z >= T) return;  // no chunk for this warp
+  const int kernel = d.blas_kernel;
+  ChunkCursor pc, cc;  // producer (lane 0) and consumer positions
+  pc.init(v.n, T, (int)blockIdx.z, G, kernel);
+  cc = pc;
+  long long pb = 0, fp = 0, fc = 0;  // producer's block in its chunk; flat blocks issued / consumed
+  auto issue_next = [&]() {  // the next block in flat order into stage fp % kStages, if any
+    while (pb >= pc.nblk) {
+      if (!pc.next()) return;
+      pb = 0;
     }
-    const int kernel = d.blas_kernel;
+    const int st = (int)(fp % kStages);
+    const long long e0 = pb * kBlk, len = min((long long)kBlk, pc.nmain - e0);
+    const char* xa = reinterpret_cast<const char*>(X.p + pc.start + e0);
+    const char* xa0 = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(xa) & ~uintptr_t(15));
+    const unsigned xbytes = (unsigned)(((xa - xa0) + len * 8 + 15) & ~15LL);
+    const char* ya = reinterpret_cast<const char*>(M.p + pc.start + e0);
+    const char* ya0 = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(ya) & ~uintptr_t(15));
+    const unsigned ybytes = (unsigned)(((ya - ya0) + len + 15) & ~15LL);
+    fence_proxy_async_smem();
+    mbar_expect_tx(&sm.bar[st], xbytes + ybytes);
+    bulk_g2s(&sm.x[st][0], xa0, xbytes, &sm.bar[st]);
+    bulk_g2s(&sm.y[st][0], ya0, ybytes, &sm.bar[st]);
+    pb++;
+    fp++;
+  };
+  if (lane == 0)
+    for (int k = 0; k < kStages - 1; k++) issue_next();
+  __syncwarp();
+  const int nl = kernel == 0 ? 32 : 16;  // lanes of the main loop
+  do {
+    const int j = cc.u;
+    const long long start = cc.start, width = cc.width, nmain = cc.nmain, nblk = cc.nblk;
     const long long n1 = width & ~15LL;
-    const long long nmain = kernel == 0 ? (n1 & ~31LL) : n1;
-    const int nl = kernel == 0 ? 32 : 16;  // lanes of the main loop
-    const long long nblk = (nmain + kBlk - 1) / kBlk;
-    auto issue = [&](long long b) {
-      const int st = (int)(b % kStages);
-      const long long e0 = b * kBlk, len = min((long long)kBlk, nmain - e0);
-      const char* xa = reinterpret_cast<const char*>(X.p + start + e0);
-      const char* xa0 = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(xa) & ~uintptr_t(15));
-      const unsigned xbytes = (unsigned)(((xa - xa0) + len * 8 + 15) & ~15LL);
-      const char* ya = reinterpret_cast<const char*>(M.p + start + e0);
-      const char* ya0 = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(ya) & ~uintptr_t(15));
-      const unsigned ybytes = (unsigned)(((ya - ya0) + len + 15) & ~15LL);
-      fence_proxy_async_smem();
-      mbar_expect_tx(&sm.bar[st], xbytes + ybytes);
-      bulk_g2s(&sm.x[st][0], xa0, xbytes, &sm.bar[st]);
-      bulk_g2s(&sm.y[st][0], ya0, ybytes, &sm.bar[st]);
-    };
-    if (lane == 0)
-      for (long long b = 0; b < min((long long)kStages - 1, nblk); b++) issue(b);
-    __syncwarp();
     double axx = 0.0, axy = 0.0;
     unsigned long long sy = 0;
     for (long long b = 0; b < nblk; b++) {
-      if (lane == 0 && b + kStages - 1 < nblk) issue(b + kStages - 1);
-      const int st = (int)(b % kStages);
+      if (lane == 0) issue_next();  // keeps kStages - 1 blocks in flight, across chunks
+      const int st = (int)(fc % kStages);
+      fc++;
       mbar_wait(&sm.bar[st], (phase_bits >> st) & 1u);
       phase_bits ^= 1u << st;
       const long long e0 = b * kBlk, len = min((long long)kBlk, nmain - e0);
@@ -670,7 +715,7 @@ __global__ void __launch_bounds__(32) k_seg_dot(const ImgDesc* __restrict__ desc
       d.dot_part[((long long)s * kMaxBlasThreads + j) * 2 + 1] = dxy;
       atomicAdd(reinterpret_cast<unsigned long long*>(&d.sum_y[s]), sy);
     }
-  }
+  } while (cc.next());
 }
 
 // ---------------------------------------------------------------------------
@@ -878,7 +923,7 @@ void launch_fit_bins(const ImgDesc* d_descs, int nimg, long long max_nodes, int 
   k_seg_setup<<<nimg, kSegs, 0, st>>>(d_descs);
   k_seg_nodes<<<dim3((unsigned)((max_nodes + 4 * kNodesPerWarp - 1) / (4 * kNodesPerWarp)), nimg), 128, 0, st>>>(d_descs);
   cudaFuncSetAttribute(k_seg_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DotSmem));
-  k_seg_dot<<<dim3(kSegs, nimg, max_chunks), 32, sizeof(DotSmem), st>>>(d_descs);
+  k_seg_dot<<<dim3(kSegs, nimg, max_chunks), 32, sizeof(DotSmem), st>>>(d_descs, nimg >= 8 ? kParSeg : 0LL);
   k_seg_reduce_coef<<<dim3(kSegs, nimg), 256, 0, st>>>(d_descs);
 }
 
