@@ -514,12 +514,13 @@ struct DotSmem {
   uint8_t y[kStages][kBlk + 32];
 };
 
-// In a batch (launch_fit_bins: >= 8 images) a segment of at least kParSeg
-// samples spreads its OpenBLAS chunks over several warps and a smaller one
-// streams every chunk through one warp; a launch of fewer images spreads every
-// segment's chunks (config 1 at 16 threads: fit 3.37 -> 3.26 ms; config 3
-// needs the parallel chunks: 0.93 ms against 1.35 with one warp per segment).
-constexpr long long kParSeg = 1LL << 20;
+// A launch over a batch (launch_fit_bins: >= 8 images) has one warp per
+// segment, which streams all its OpenBLAS chunks in turn through one
+// continuous pipeline; a launch over fewer images spreads every segment's
+// chunks over the grid's z, one warp each.  Config 1 at 16 threads: fit 3.37
+// ms with a warp per chunk, 2.98 with a warp per segment (the grid's 16x more,
+// mostly empty CTAs alone cost 0.28 ms); config 3 needs the parallel chunks
+// (fit 0.93 ms, against 1.35 with one warp per segment below 1 Mi samples).
 
 // Position in OpenBLAS's level-1 split of a segment of n samples into T
 // chunks (width = ceil(rem / (T - used)), oracle/hdll_oracle.c ddot_compute):
@@ -554,7 +555,7 @@ struct ChunkCursor {
 };
 
 // grid: (kSegs, nimg, max chunks); one warp per (segment, OpenBLAS thread-chunk)
-__global__ void __launch_bounds__(32) k_seg_dot(const ImgDesc* __restrict__ descs, long long par_seg) {
+__global__ void __launch_bounds__(32) k_seg_dot(const ImgDesc* __restrict__ descs) {
   const ImgDesc& d = descs[blockIdx.y];
   if (!d.slrme || d.int_fit) return;
   const int s = blockIdx.x;
@@ -572,10 +573,9 @@ __global__ void __launch_bounds__(32) k_seg_dot(const ImgDesc* __restrict__ desc
   fence_mbar_init();
   __syncwarp();
   unsigned phase_bits = 0;  // parity of every stage's barrier, flipped at each consumed block
-  // A segment below kParSeg samples is one warp's: it streams all its chunks
-  // in turn through one continuous pipeline (the producer runs ahead across
-  // chunk boundaries).  A larger one spreads its chunks over the grid's z.
-  const int G = v.n >= par_seg ? (int)gridDim.z : 1;
+  // The warp's chunks j0, j0 + G, ... stream through one continuous pipeline
+  // (the producer runs ahead across chunk boundaries).
+  const int G = (int)gridDim.z;
   if ((int)blockIdx.z >= G || (int)blockIdx.z >= T) return;  // no chunk for this warp
   const int kernel = d.blas_kernel;
   ChunkCursor pc, cc;  // producer (lane 0) and consumer positions
@@ -923,7 +923,8 @@ void launch_fit_bins(const ImgDesc* d_descs, int nimg, long long max_nodes, int 
   k_seg_setup<<<nimg, kSegs, 0, st>>>(d_descs);
   k_seg_nodes<<<dim3((unsigned)((max_nodes + 4 * kNodesPerWarp - 1) / (4 * kNodesPerWarp)), nimg), 128, 0, st>>>(d_descs);
   cudaFuncSetAttribute(k_seg_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DotSmem));
-  k_seg_dot<<<dim3(kSegs, nimg, max_chunks), 32, sizeof(DotSmem), st>>>(d_descs, nimg >= 8 ? kParSeg : 0LL);
+  const int zd = nimg >= 8 ? 1 : max_chunks;  // batches: a warp per segment; else a warp per chunk
+  k_seg_dot<<<dim3(kSegs, nimg, zd), 32, sizeof(DotSmem), st>>>(d_descs);
   k_seg_reduce_coef<<<dim3(kSegs, nimg), 256, 0, st>>>(d_descs);
 }
 
