@@ -160,3 +160,25 @@ def test_host_pipeline_chunks_cover_the_stream_in_order(nimg, chunk, repeats):
     assert all(1 <= len(k) <= c for k in chunks)
     if nimg * repeats >= 3 * c and c >= 4:
         assert len(chunks[0]) <= c // 4 and len(chunks[-1]) <= c // 2
+
+
+def test_bench_parity_model_follows_the_host_blas():
+    """bench.py encodes with this host's OpenBLAS kernel and thread count (the
+    streams `hdll.encode` computes here) unless --blas-threads overrides it,
+    and compares with the reference digests made at that thread count."""
+    import argparse
+
+    import bench
+
+    hb = {"kernel": 0, "threads": 16}
+    assert bench.blas_params(argparse.Namespace(blas_threads=None), hb) == (0, 16)
+    assert bench.blas_params(argparse.Namespace(blas_threads=1), hb) == (0, 1)
+    assert bench.blas_params(argparse.Namespace(blas_threads=None), {"kernel": None, "threads": None}) == (0, 1)
+    assert bench.blas_params(argparse.Namespace(blas_threads=None), {"kernel": 1, "threads": 200}) == (1, 64)
+    one = bench.golden_digests(1, 1.0, 1)
+    assert len(one) == 64
+    assert bench.golden_digests(1, 0.0, 16) == bench.golden_digests(1, 0.0, 1)  # sigma 0: thread-independent
+    t16 = bench.golden_digests(1, 1.0, 16)
+    if t16:  # tests/golden/config_golden_t16.json present
+        assert len(t16) == 64 and t16 != one
+    assert bench.golden_digests(1, 1.0, 7) == {}  # no digests at that thread count: the oracle checks
