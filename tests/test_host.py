@@ -180,5 +180,8 @@ def test_bench_parity_model_follows_the_host_blas():
     assert bench.golden_digests(1, 0.0, 16) == bench.golden_digests(1, 0.0, 1)  # sigma 0: thread-independent
     t16 = bench.golden_digests(1, 1.0, 16)
     if t16:  # tests/golden/config_golden_t16.json present
-        assert len(t16) == 64 and t16 != one
+        assert len(t16) == 64
+        # the 16-way split moves float32 a / b only where an fp64 sum sits near a
+        # rounding boundary: config 2's streams differ, config 1's do not
+        assert bench.golden_digests(2, 1.0, 16) != bench.golden_digests(2, 1.0, 1)
     assert bench.golden_digests(1, 1.0, 7) == {}  # no digests at that thread count: the oracle checks
